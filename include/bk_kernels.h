@@ -1,0 +1,153 @@
+/*
+ * bk_kernels.h — internal thin C ABI between the host driver (C++) and the
+ * hand-written sm_100a CUDA kernels of libblockeig_b200.so.
+ *
+ * Plain pointers and sizes only: every function takes raw DEVICE pointers,
+ * an explicit leading dimension per dense operand and a cudaStream_t (passed
+ * as void*), never throws, and returns 0 on success or a cudaError_t code.
+ *
+ * Device layout: dense blocks are ROW-MAJOR n x k with leading dimension ld
+ * (element (i, j) at p[i*ld + j]); a column range of a block is the same
+ * pointer offset by the first column, so the shrink/expand column selection
+ * of the reference (take_leading, rightCols, hcat: proj/src/solvers.cpp:12-23)
+ * is pointer arithmetic plus, where contiguity is needed, bk_copy_cols.
+ * The matrix is full (both triangles) CSR with int32 row_ptr / col.
+ *
+ * Each entry names the reference code it replaces.
+ */
+#ifndef BK_KERNELS_H
+#define BK_KERNELS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(_WIN32)
+#define BK_API __declspec(dllexport)
+#else
+#define BK_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- K1 SpMM: Y = A X  (replaces spmv / spmv_block, proj/src/kernel.cpp:8-33) ---- */
+BK_API int bk_spmm_d(int n, const int32_t* row_ptr, const int32_t* col, const double* val,
+                     const double* x, int ldx, int k, double* y, int ldy, void* stream);
+/* complex Hermitian twin: x, y, val interleaved (re, im); ld in complex elements */
+BK_API int bk_spmm_z(int n, const int32_t* row_ptr, const int32_t* col, const double* val,
+                     const double* x, int ldx, int k, double* y, int ldy, void* stream);
+
+/* ---- K2 Gram: C = X^H Y, X n x a, Y n x b; C a x b row-major (ldc) ----
+ * (replaces s.transpose()*as, proj/src/rr.cpp:11, and q.transpose()*v in CGS2,
+ * proj/src/kernel.cpp:76,79).  FP64 DMMA tensor cores, split-K over n with a
+ * fixed-order reduction (deterministic).  work: >= bk_gram_work_bytes(n, a, b). */
+BK_API size_t bk_gram_work_bytes(int n, int a, int b);
+BK_API int bk_gram_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b,
+                     double* c, int ldc, void* work, void* stream);
+
+/* ---- K3 update: Y = alpha X C + beta Y, X n x d, C d x k (row-major, ldc) ----
+ * (replaces s*e.vectors, proj/src/rr.cpp:13; s*z1 / s*o.q, proj/src/solvers.cpp:195;
+ * q*(q^T v), proj/src/kernel.cpp:76,79).  FP64 DMMA.  Y must not alias X. */
+BK_API int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k,
+                     double alpha, double beta, double* y, int ldy, void* stream);
+
+/* ---- column sums of squares: out[j] = sum_i |X_ij|^2 (deterministic) ---- */
+BK_API size_t bk_colnorm2_work_bytes(int n, int k);
+BK_API int bk_colnorm2_d(int n, const double* x, int ldx, int k, double* out, void* work,
+                         void* stream);
+
+/* ---- K6 residual + norms: R = AV - V diag(lambda); optional W = t .* R ----
+ * (replaces residual_block + apply_precond, proj/src/rr.cpp:16-20,
+ * proj/src/solvers.cpp:105-107).  Column norms of R and V land in
+ * rn2[k], vn2[k] (sums of squares, deterministic).  r may be NULL when only
+ * W is wanted; w (ldw) receives t.*R for columns [w_from, k) when non-NULL
+ * (t == NULL means identity). */
+BK_API size_t bk_residual_work_bytes(int n, int k);
+BK_API int bk_residual_d(int n, const double* v, int ldv, const double* av, int ldav,
+                         const double* lambda, int k, double* r, int ldr, const double* t,
+                         double* w, int ldw, int w_from, double* rn2, double* vn2, void* work,
+                         void* stream);
+
+/* convergence finish (replaces assess_convergence, proj/src/rr.cpp:22-38):
+ * per_pair[i] = sqrt(rn2)/(norm_a*sqrt(vn2) + sqrt(vn2)*|lambda|), overall =
+ * max over i < n_ev, converged = leading prefix with per_pair <= tol.
+ * rec receives {overall, converged, nonfinite_flag} as 3 doubles. */
+BK_API int bk_convergence_d(int k, const double* rn2, const double* vn2, const double* lambda,
+                            double norm_a, int n_ev, double tol, double* per_pair, double* rec,
+                            void* stream);
+
+/* ---- K4 pieces: skip-pivot Cholesky of a Gram block with the CGS2 drop rule ----
+ * (replaces the keep/drop test of project_orthonormalize, proj/src/kernel.cpp:83-85).
+ * g: a x a Gram (row-major, ldg) of the externally projected block; ref2[j] =
+ * squared norm of column j BEFORE any projection (ref2 == NULL: no dropping,
+ * every positive pivot kept).  A column is dropped when its Cholesky pivot is
+ * below drop*ref (or ref == 0).  Output m (a x a, ldm, row-major): W*m has the
+ * kept columns orthonormalised and packed left (rows of R^-1 in kept order,
+ * zero rows for dropped columns).  info[0] = kept; info[1] = 1 when a pivot
+ * decision was not certain (heavy cancellation in the Schur complement, so the
+ * caller re-runs the block with exact column CGS2); info[2] = 1 on a
+ * non-finite value.  work >= bk_chol_work_bytes(a). */
+BK_API size_t bk_chol_work_bytes(int a);
+BK_API int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref2, double drop,
+                          double* m, int ldm, int* info, void* work, void* stream);
+
+/* ---- K5 symmetric eigensolver (replaces sym_eig_small, proj/src/kernel.cpp:95-100) ----
+ * Eigendecomposition of 0.5(H + H^T) (d x d row-major, ldh; destroyed) by
+ * parallel cyclic Jacobi.  values ascending (stable among ties), z (ldz)
+ * row-major with eigenvector j in column j.  info[0] = sweeps used,
+ * info[1] = 1 if not converged. */
+BK_API size_t bk_syev_work_bytes(int d);
+BK_API int bk_syev_d(int d, double* h, int ldh, double* values, double* z, int ldz, void* work,
+                     int* info, void* stream);
+
+/* ---- K7 column movement / elementwise ---- */
+/* dst[:, 0:k] = src[:, 0:k] (row-major; src and dst may overlap in the same rows) */
+BK_API int bk_copy_cols_d(int n, const double* src, int lds, int k, double* dst, int ldd,
+                          void* stream);
+/* column-major host layout <-> row-major device layout */
+BK_API int bk_cm_to_rm_d(int n, int k, const double* cm, int ldcm, double* rm, int ldrm,
+                         void* stream);
+BK_API int bk_rm_to_cm_d(int n, int k, const double* rm, int ldrm, double* cm, int ldcm,
+                         void* stream);
+/* y = a*x + b*y over n x k (row-major) */
+BK_API int bk_axpby_d(int n, int k, double a, const double* x, int ldx, double b, double* y,
+                      int ldy, void* stream);
+/* zero rows [r0, r1) of columns [0, k) */
+BK_API int bk_zero_rows_d(double* x, int ldx, int k, int r0, int r1, void* stream);
+/* out = a*x + b*y over n x k (out may alias x or y) */
+BK_API int bk_lincomb_d(int n, int k, double a, const double* x, int ldx, double b, const double* y,
+                        int ldy, double* out, int ldo, void* stream);
+/* y[i][c] = t[i] * x[i][c] (t == NULL: plain copy); the diagonal preconditioner
+ * W = diag(T) R of proj/src/solvers.cpp:98-107 */
+BK_API int bk_scale_rows_d(int n, int k, const double* t, const double* x, int ldx, double* y,
+                           int ldy, void* stream);
+/* out[c] = sum_i x[i][c] * y[i][c] (deterministic two-level sum) */
+BK_API int bk_coldot_d(int n, const double* x, int ldx, const double* y, int ldy, int k,
+                       double* out, void* work, void* stream);
+/* batched CG bookkeeping for TraceMIN (cg_solve, proj/src/kernel.cpp:139-164):
+ * state per column c: rs[c], bnorm[c], active[c] (1/0).
+ * bk_cg_check: deactivate columns with sqrt(rs) < 1e-14*bnorm; count[0] = #active.
+ * bk_cg_step1: for active c: pap <= 0 deactivates, else alpha = rs/pap,
+ *              x += alpha p, r -= alpha ap.
+ * bk_cg_step2: for active c: beta = rs_new/rs, p = r + beta p, rs = rs_new. */
+BK_API int bk_cg_check_d(int k, const double* rs, const double* bnorm, int* active, int* count,
+                         void* stream);
+BK_API int bk_cg_step1_d(int n, int k, const double* rs, const double* pap, int* active, double* x,
+                         int ldx, double* r, int ldr, const double* p, int ldp, const double* ap,
+                         int ldap, void* stream);
+BK_API int bk_cg_step2_d(int n, int k, double* rs, const double* rs_new, const int* active,
+                         const double* r, int ldr, double* p, int ldp, void* stream);
+
+/* host-only hook (no device use): the product's strategy state machine driven
+ * over a residual sequence, for CPU tests of decide() parity */
+BK_API int bk_host_decide_sequence(int kind, int j_e, int j_s, double mu, int j_p, int j_warm,
+                                   double r_warm, const double* r, int count, int n_es, int n_ex,
+                                   int start_n_now, int start_shrunk, int apply_changes,
+                                   int* decisions);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BK_KERNELS_H */

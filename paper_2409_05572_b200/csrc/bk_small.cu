@@ -1,0 +1,328 @@
+// K4 (Cholesky with the CGS2 drop rule) and K5 (projected eigenproblem) —
+// single-CTA kernels on the small dense side of the iteration.
+//
+// K4: the reference orthonormalises column by column with classical
+// Gram-Schmidt applied twice and drops a column whose remaining norm is below
+// 1e-8 of its original norm (proj/src/kernel.cpp:65-89).  Here the block is
+// projected against the external basis with two K2/K3 passes and then
+// orthonormalised by CholQR2; the keep/drop decision is the Cholesky pivot of
+// the column against the columns kept before it, which in exact arithmetic is
+// the same remaining norm CGS2 measures.  Pivots computed with heavy
+// cancellation (remaining norm < 1e-4 of the projected norm) are reported as
+// uncertain and the caller redoes that block with exact column CGS2.
+//
+// K5: eigendecomposition of 0.5(H + H^T) (sym_eig_small, kernel.cpp:95-100) by
+// two-sided cyclic Jacobi in round-robin parallel order: every round rotates
+// d/2 disjoint pairs at once, each 2x2 block of H is updated by one thread
+// (rows and columns in one pass), and V accumulates the rotations.  H lives in
+// shared memory up to d = 160 and in global memory (L2-resident) above.
+#include <cfloat>
+
+#include "bk_common.cuh"
+
+namespace bk {
+namespace {
+
+// ------------------------------------------------------------------ K4
+__global__ void __launch_bounds__(1024) chol_drop_kernel(int a, const double* __restrict__ g, int ldg,
+                                                          const double* __restrict__ ref2, double drop,
+                                                          double* __restrict__ m, int ldm,
+                                                          int* __restrict__ info, double* __restrict__ s,
+                                                          double* __restrict__ rc, int* __restrict__ slot) {
+    __shared__ int s_keep, s_kept, s_unsure, s_bad;
+    __shared__ double s_rjj;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < a * a; e += nt) s[e] = g[static_cast<size_t>(e / a) * ldg + e % a];
+    if (tid == 0) {
+        s_kept = 0;
+        s_unsure = 0;
+        s_bad = 0;
+    }
+    __syncthreads();
+    for (int j = 0; j < a; ++j) {
+        if (tid == 0) {
+            const double p = s[j * a + j];
+            const double gjj = g[static_cast<size_t>(j) * ldg + j];
+            int keep;
+            if (!isfinite(p) || !isfinite(gjj)) {
+                s_bad = 1;
+                keep = 0;
+            } else if (ref2 == nullptr) {
+                keep = p > 0.0;
+                if (p <= 1e-8 * gjj) s_unsure = 1;  // pass 2 of CholQR2: basis lost rank
+            } else {
+                const double ref = sqrt(ref2[j]);
+                const double thr = drop * ref;
+                if (ref2[j] == 0.0 || gjj < thr * thr) {
+                    keep = 0;  // certain: the pivot can never exceed the projected norm
+                } else {
+                    keep = p >= thr * thr;
+                    if (p < 1e-8 * gjj) s_unsure = 1;  // cancellation: pivot not trustworthy
+                    else if (fabs(sqrt(fmax(p, 0.0)) - thr) < 1e-4 * thr) s_unsure = 1;
+                }
+            }
+            s_keep = keep;
+            if (keep) {
+                s_rjj = sqrt(p);
+                slot[j] = s_kept;
+                rc[s_kept * a + s_kept] = s_rjj;
+                ++s_kept;
+            } else {
+                slot[j] = -1;
+            }
+        }
+        __syncthreads();
+        if (s_keep) {
+            const double inv = 1.0 / s_rjj;
+            for (int l = j + 1 + tid; l < a; l += nt) s[j * a + l] *= inv;  // row j of R
+            __syncthreads();
+            const int w = a - j - 1;
+            const int tri = w * (w + 1) / 2;
+            for (int e = tid; e < tri; e += nt) {
+                // (k, l) with j < k <= l < a, enumerated row by row
+                int kk = static_cast<int>((2.0 * w + 1.0 - sqrt((2.0 * w + 1.0) * (2.0 * w + 1.0) - 8.0 * e)) / 2.0);
+                while (kk > 0 && kk * w - kk * (kk - 1) / 2 > e) --kk;
+                while ((kk + 1) * w - (kk + 1) * kk / 2 <= e) ++kk;
+                const int off = e - (kk * w - kk * (kk - 1) / 2);
+                const int k = j + 1 + kk, l = k + off;
+                s[k * a + l] -= s[j * a + k] * s[j * a + l];
+            }
+        }
+        __syncthreads();
+    }
+    const int kept = s_kept;
+    // compact R (kept x kept, upper) from the rows of kept pivots
+    for (int e = tid; e < a * a; e += nt) {
+        const int j = e / a, l = e % a;
+        if (j < l && slot[j] >= 0 && slot[l] >= 0) rc[slot[j] * a + slot[l]] = s[j * a + l];
+    }
+    __syncthreads();
+    // invert the upper-triangular R column by column (one thread per column);
+    // the inverse overwrites s as a kept x kept block
+    for (int c = tid; c < kept; c += nt) {
+        s[c * a + c] = 1.0 / rc[c * a + c];
+        for (int i = c - 1; i >= 0; --i) {
+            double acc = 0.0;
+            for (int l = i + 1; l <= c; ++l) acc = fma(rc[i * a + l], s[l * a + c], acc);
+            s[i * a + c] = -acc / rc[i * a + i];
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < a * a; e += nt) {
+        const int j = e / a, c = e % a;
+        double v = 0.0;
+        const int sj = slot[j];
+        if (sj >= 0 && c < kept && sj <= c) v = s[sj * a + c];
+        m[static_cast<size_t>(j) * ldm + c] = v;
+    }
+    if (tid == 0) {
+        info[0] = kept;
+        info[1] = s_unsure;
+        info[2] = s_bad;
+    }
+}
+
+// ------------------------------------------------------------------ K5
+constexpr int kJacobiSmemMaxD = 160;
+constexpr int kJacobiThreads = 1024;
+constexpr int kMaxPairs = 1024;  // pairs per round: d <= 2048
+
+__device__ __forceinline__ int rr_index(int r, int i, int m) { return i == 0 ? 0 : 1 + (i - 1 + r) % (m - 1); }
+
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(int d, const double* __restrict__ hin, int ldh,
+                                                                 double* __restrict__ hg, double* __restrict__ v,
+                                                                 double* __restrict__ values,
+                                                                 double* __restrict__ z, int ldz,
+                                                                 int* __restrict__ info, int use_smem) {
+    extern __shared__ double dyn[];
+    __shared__ int pp[kMaxPairs / 2 + 1], pq[kMaxPairs / 2 + 1];
+    __shared__ double pc[kMaxPairs / 2 + 1], ps[kMaxPairs / 2 + 1], pt[kMaxPairs / 2 + 1];
+    __shared__ double red[kJacobiThreads / 32];
+    __shared__ double s_fro, s_sweep_max;
+    double* h = use_smem ? dyn : hg;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    const int m = d + (d & 1);
+    const int np = m / 2;
+
+    // symmetrise, V = I, ||H||_F
+    double f2 = 0.0;
+    for (int e = tid; e < d * d; e += nt) {
+        const int i = e / d, j = e % d;
+        const double hv = 0.5 * (hin[static_cast<size_t>(i) * ldh + j] + hin[static_cast<size_t>(j) * ldh + i]);
+        h[e] = hv;
+        v[e] = i == j ? 1.0 : 0.0;
+        f2 = fma(hv, hv, f2);
+    }
+    f2 = warp_sum(f2);
+    if (lane == 0) red[wid] = f2;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < nt / 32; ++w) s += red[w];
+        s_fro = sqrt(s);
+    }
+    __syncthreads();
+    const double fro = s_fro;
+    const double skip = 1e-18 * fro;
+    const double stop = 1e-16 * fro;
+    int sweep = 0;
+    bool converged = fro == 0.0 || d < 2;
+    for (; sweep < 60 && !converged; ++sweep) {
+        double my_max = 0.0;
+        for (int r = 0; r < m - 1; ++r) {
+            for (int k = tid; k < np; k += nt) {
+                int p = rr_index(r, k, m), q = rr_index(r, m - 1 - k, m);
+                if (p > q) {
+                    const int tmp = p;
+                    p = q;
+                    q = tmp;
+                }
+                pp[k] = p;
+                pq[k] = q;
+                double c = 1.0, s = 0.0, t = 0.0;
+                if (q < d) {
+                    const double apq = h[p * d + q];
+                    my_max = fmax(my_max, fabs(apq));
+                    if (fabs(apq) > skip) {
+                        const double theta = (h[q * d + q] - h[p * d + p]) / (2.0 * apq);
+                        t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+                        c = 1.0 / sqrt(fma(t, t, 1.0));
+                        s = t * c;
+                    }
+                }
+                pc[k] = c;
+                ps[k] = s;
+                pt[k] = t;
+            }
+            __syncthreads();
+            // H <- J^T H J, one thread per 2x2 block (k1 <= k2), mirrored
+            const int nblk = np * (np + 1) / 2;
+            for (int e = tid; e < nblk; e += nt) {
+                int k1 = static_cast<int>((2.0 * np + 1.0 - sqrt((2.0 * np + 1.0) * (2.0 * np + 1.0) - 8.0 * e)) / 2.0);
+                while (k1 > 0 && k1 * np - k1 * (k1 - 1) / 2 > e) --k1;
+                while ((k1 + 1) * np - (k1 + 1) * k1 / 2 <= e) ++k1;
+                const int k2 = k1 + (e - (k1 * np - k1 * (k1 - 1) / 2));
+                const int p1 = pp[k1], q1 = pq[k1], p2 = pp[k2], q2 = pq[k2];
+                const double c1 = pc[k1], s1 = ps[k1], c2 = pc[k2], s2 = ps[k2];
+                if (k1 == k2) {
+                    if (q1 < d && s1 != 0.0) {
+                        const double apq = h[p1 * d + q1];
+                        h[p1 * d + p1] -= pt[k1] * apq;
+                        h[q1 * d + q1] += pt[k1] * apq;
+                        h[p1 * d + q1] = 0.0;
+                        h[q1 * d + p1] = 0.0;
+                    }
+                    continue;
+                }
+                const bool q1ok = q1 < d, q2ok = q2 < d;
+                double a00 = h[p1 * d + p2];
+                double a01 = q2ok ? h[p1 * d + q2] : 0.0;
+                double a10 = q1ok ? h[q1 * d + p2] : 0.0;
+                double a11 = (q1ok && q2ok) ? h[q1 * d + q2] : 0.0;
+                // rows: [x_p; x_q] -> [c x_p - s x_q; s x_p + c x_q]
+                double b00 = c1 * a00 - s1 * a10, b10 = s1 * a00 + c1 * a10;
+                double b01 = c1 * a01 - s1 * a11, b11 = s1 * a01 + c1 * a11;
+                // columns likewise
+                a00 = c2 * b00 - s2 * b01;
+                a01 = s2 * b00 + c2 * b01;
+                a10 = c2 * b10 - s2 * b11;
+                a11 = s2 * b10 + c2 * b11;
+                h[p1 * d + p2] = a00;
+                h[p2 * d + p1] = a00;
+                if (q2ok) {
+                    h[p1 * d + q2] = a01;
+                    h[q2 * d + p1] = a01;
+                }
+                if (q1ok) {
+                    h[q1 * d + p2] = a10;
+                    h[p2 * d + q1] = a10;
+                }
+                if (q1ok && q2ok) {
+                    h[q1 * d + q2] = a11;
+                    h[q2 * d + q1] = a11;
+                }
+            }
+            // V <- V J (rows independent)
+            for (int e = tid; e < d * np; e += nt) {
+                const int i = e / np, k = e % np;
+                const int p = pp[k], q = pq[k];
+                if (q >= d || ps[k] == 0.0) continue;
+                const double c = pc[k], s = ps[k];
+                const double vp = v[i * d + p], vq = v[i * d + q];
+                v[i * d + p] = c * vp - s * vq;
+                v[i * d + q] = s * vp + c * vq;
+            }
+            __syncthreads();
+        }
+        for (int o = 16; o > 0; o >>= 1) my_max = fmax(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
+        if (lane == 0) red[wid] = my_max;
+        __syncthreads();
+        if (tid == 0) {
+            double mx = 0.0;
+            for (int w = 0; w < nt / 32; ++w) mx = fmax(mx, red[w]);
+            s_sweep_max = mx;
+        }
+        __syncthreads();
+        converged = s_sweep_max <= stop;
+    }
+    // ascending stable order: rank_j = #{i : h_i < h_j or (h_i == h_j and i < j)}
+    for (int j = tid; j < d; j += nt) {
+        const double hj = h[j * d + j];
+        int rank = 0;
+        for (int i = 0; i < d; ++i) {
+            const double hi = h[i * d + i];
+            rank += (hi < hj) || (hi == hj && i < j);
+        }
+        values[rank] = hj;
+        for (int i = 0; i < d; ++i) z[static_cast<size_t>(i) * ldz + rank] = v[i * d + j];
+    }
+    if (tid == 0) {
+        info[0] = sweep;
+        info[1] = converged ? 0 : 1;
+    }
+}
+
+}  // namespace
+}  // namespace bk
+
+using namespace bk;
+
+extern "C" size_t bk_chol_work_bytes(int a) {
+    const size_t aa = static_cast<size_t>(a > 0 ? a : 1);
+    return 2 * aa * aa * sizeof(double) + aa * sizeof(int) + 64;
+}
+
+extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
+                              int ldm, int* info, void* work, void* stream) {
+    if (a <= 0) {
+        BK_RET(cudaMemsetAsync(info, 0, 3 * sizeof(int), as_stream(stream)));
+        return 0;
+    }
+    auto s = static_cast<double*>(work);
+    double* rc = s + static_cast<size_t>(a) * a;
+    int* slot = reinterpret_cast<int*>(rc + static_cast<size_t>(a) * a);
+    chol_drop_kernel<<<1, 1024, 0, as_stream(stream)>>>(a, g, ldg, ref2, drop, m, ldm, info, s, rc, slot);
+    BK_LAUNCHED();
+}
+
+extern "C" size_t bk_syev_work_bytes(int d) {
+    const size_t dd = static_cast<size_t>(d > 0 ? d : 1);
+    return 2 * dd * dd * sizeof(double);
+}
+
+extern "C" int bk_syev_d(int d, double* h, int ldh, double* values, double* z, int ldz, void* work,
+                         int* info, void* stream) {
+    if (d <= 0) return 0;
+    if (d > kMaxPairs * 2) return static_cast<int>(cudaErrorInvalidValue);
+    const cudaStream_t s = as_stream(stream);
+    auto hg = static_cast<double*>(work);
+    double* v = hg + static_cast<size_t>(d) * d;
+    const int use_smem = d <= kJacobiSmemMaxD ? 1 : 0;
+    const size_t smem = use_smem ? static_cast<size_t>(d) * d * sizeof(double) : 0;
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(kJacobiSmemMaxD * kJacobiSmemMaxD * sizeof(double)));
+    BK_RET(attr);
+    jacobi_kernel<<<1, kJacobiThreads, smem, s>>>(d, h, ldh, hg, v, values, z, ldz, info, use_smem);
+    BK_LAUNCHED();
+}

@@ -1,0 +1,469 @@
+// K6 / K7 / K8 — residual + column norms, convergence finish, column movement.
+//
+// Replaces: residual_block (proj/src/rr.cpp:16-20), the norms of
+// assess_convergence (rr.cpp:22-38), apply_precond (solvers.cpp:105-107) and the
+// Eigen column selection / hcat copies of the solver loops (solvers.cpp:12-23).
+// All reductions are two-level with a fixed order, so results are bit-stable
+// run to run (the reference's determinism contract, kernel.hpp:21-23).
+#include <cfloat>
+
+#include <algorithm>
+
+#include "bk_common.cuh"
+
+namespace bk {
+namespace {
+
+constexpr int kRowsPerBlock = 256;
+constexpr int kMaxRowBlocks = 512;
+
+int row_blocks(int n) { return max(1, min(ceil_div(n, kRowsPerBlock), kMaxRowBlocks)); }
+
+// column sums of squares over a row range; partial[rb][c]
+__global__ void __launch_bounds__(256) colnorm2_partial(int n, const double* __restrict__ x, int ldx,
+                                                         int k, double* __restrict__ partial) {
+    __shared__ double red[8][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int c = blockIdx.y * 32 + tx;
+    const int nb = gridDim.x;
+    const int r0 = static_cast<int>((static_cast<int64_t>(n) * blockIdx.x) / nb);
+    const int r1 = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.x + 1)) / nb);
+    double acc = 0.0;
+    if (c < k)
+        for (int r = r0 + ty; r < r1; r += 8) {
+            const double v = x[static_cast<size_t>(r) * ldx + c];
+            acc = fma(v, v, acc);
+        }
+    red[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && c < k) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += red[i][tx];
+        partial[static_cast<size_t>(blockIdx.x) * k + c] = s;
+    }
+}
+
+__global__ void sum_partials(int nb, int k, const double* __restrict__ partial, double* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += partial[static_cast<size_t>(b) * k + c];
+    out[c] = s;
+}
+
+// R = AV - V diag(lambda); W = t .* R (columns >= w_from); norms of R and V
+__global__ void __launch_bounds__(256) residual_partial(int n, const double* __restrict__ v, int ldv,
+                                                         const double* __restrict__ av, int ldav,
+                                                         const double* __restrict__ lambda, int k,
+                                                         double* __restrict__ r, int ldr,
+                                                         const double* __restrict__ t,
+                                                         double* __restrict__ w, int ldw, int w_from,
+                                                         double* __restrict__ pr, double* __restrict__ pv) {
+    __shared__ double red_r[8][33];
+    __shared__ double red_v[8][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int c = blockIdx.y * 32 + tx;
+    const int nb = gridDim.x;
+    const int r0 = static_cast<int>((static_cast<int64_t>(n) * blockIdx.x) / nb);
+    const int r1 = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.x + 1)) / nb);
+    double ar = 0.0, avv = 0.0;
+    if (c < k) {
+        const double lam = lambda[c];
+        for (int i = r0 + ty; i < r1; i += 8) {
+            const double vv = v[static_cast<size_t>(i) * ldv + c];
+            const double rr = av[static_cast<size_t>(i) * ldav + c] - lam * vv;
+            if (r) r[static_cast<size_t>(i) * ldr + c] = rr;
+            if (w && c >= w_from) w[static_cast<size_t>(i) * ldw + (c - w_from)] = t ? t[i] * rr : rr;
+            ar = fma(rr, rr, ar);
+            avv = fma(vv, vv, avv);
+        }
+    }
+    red_r[ty][tx] = ar;
+    red_v[ty][tx] = avv;
+    __syncthreads();
+    if (ty == 0 && c < k) {
+        double s = 0.0, sv = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            s += red_r[i][tx];
+            sv += red_v[i][tx];
+        }
+        pr[static_cast<size_t>(blockIdx.x) * k + c] = s;
+        pv[static_cast<size_t>(blockIdx.x) * k + c] = sv;
+    }
+}
+
+__global__ void residual_finish(int nb, int k, const double* __restrict__ pr, const double* __restrict__ pv,
+                                double* __restrict__ rn2, double* __restrict__ vn2) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double s = 0.0, sv = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        s += pr[static_cast<size_t>(b) * k + c];
+        sv += pv[static_cast<size_t>(b) * k + c];
+    }
+    rn2[c] = s;
+    vn2[c] = sv;
+}
+
+// rr.cpp:22-38 on device; one CTA
+__global__ void __launch_bounds__(1024) convergence_kernel(int k, const double* __restrict__ rn2,
+                                                            const double* __restrict__ vn2,
+                                                            const double* __restrict__ lambda,
+                                                            double norm_a, int n_ev, double tol,
+                                                            double* __restrict__ per_pair,
+                                                            double* __restrict__ rec) {
+    __shared__ double s_max[1024];
+    __shared__ int s_first[1024];
+    __shared__ int s_bad[1024];
+    double mx = 0.0;
+    int first = k;
+    int bad = 0;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const double vn = sqrt(vn2[i]);
+        const double rn = sqrt(rn2[i]);
+        const double denom = norm_a * vn + vn * fabs(lambda[i]);
+        const double pp = denom > 0.0 ? rn / denom : rn;
+        if (per_pair) per_pair[i] = pp;
+        if (i < n_ev) mx = fmax(mx, pp);
+        if (!(pp <= tol)) first = min(first, i);  // NaN counts as unconverged
+        if (!isfinite(pp) || !isfinite(lambda[i])) bad = 1;
+    }
+    s_max[threadIdx.x] = mx;
+    s_first[threadIdx.x] = first;
+    s_bad[threadIdx.x] = bad;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off) {
+            s_max[threadIdx.x] = fmax(s_max[threadIdx.x], s_max[threadIdx.x + off]);
+            s_first[threadIdx.x] = min(s_first[threadIdx.x], s_first[threadIdx.x + off]);
+            s_bad[threadIdx.x] |= s_bad[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        rec[0] = s_max[0];
+        rec[1] = static_cast<double>(s_first[0]);
+        rec[2] = static_cast<double>(s_bad[0]);
+    }
+}
+
+// one warp per row; chunks of 32 columns moved through registers in the
+// direction that makes overlapping (same-row) moves safe
+__global__ void __launch_bounds__(256) copy_cols_kernel(int n, const double* src, int lds, int k,
+                                                        double* dst, int ldd) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const double* s = src + static_cast<size_t>(row) * lds;
+        double* d = dst + static_cast<size_t>(row) * ldd;
+        const bool forward = d <= s;
+        const int chunks = ceil_div(k, 32);
+        for (int q = 0; q < chunks; ++q) {
+            const int ch = forward ? q : chunks - 1 - q;
+            const int c = ch * 32 + lane;
+            double v = 0.0;
+            if (c < k) v = s[c];
+            __syncwarp();
+            if (c < k) d[c] = v;
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void cm_to_rm_kernel(int n, int k, const double* __restrict__ cm, int ldcm,
+                                double* __restrict__ rm, int ldrm) {
+    __shared__ double tile[32][33];
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+        const int i = i0 + threadIdx.x, j = j0 + jj;
+        if (i < n && j < k) tile[jj][threadIdx.x] = cm[static_cast<size_t>(j) * ldcm + i];
+    }
+    __syncthreads();
+    for (int ii = threadIdx.y; ii < 32; ii += blockDim.y) {
+        const int i = i0 + ii, j = j0 + threadIdx.x;
+        if (i < n && j < k) rm[static_cast<size_t>(i) * ldrm + j] = tile[threadIdx.x][ii];
+    }
+}
+
+__global__ void rm_to_cm_kernel(int n, int k, const double* __restrict__ rm, int ldrm,
+                                double* __restrict__ cm, int ldcm) {
+    __shared__ double tile[32][33];
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    for (int ii = threadIdx.y; ii < 32; ii += blockDim.y) {
+        const int i = i0 + ii, j = j0 + threadIdx.x;
+        if (i < n && j < k) tile[ii][threadIdx.x] = rm[static_cast<size_t>(i) * ldrm + j];
+    }
+    __syncthreads();
+    for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+        const int i = i0 + threadIdx.x, j = j0 + jj;
+        if (i < n && j < k) cm[static_cast<size_t>(j) * ldcm + i] = tile[threadIdx.x][jj];
+    }
+}
+
+__global__ void axpby_kernel(int n, int k, double a, const double* __restrict__ x, int ldx, double b,
+                             double* __restrict__ y, int ldy) {
+    const int64_t total = static_cast<int64_t>(n) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e / k), j = static_cast<int>(e % k);
+        double* yp = y + static_cast<size_t>(i) * ldy + j;
+        const double xv = x[static_cast<size_t>(i) * ldx + j];
+        *yp = b == 0.0 ? a * xv : a * xv + b * *yp;
+    }
+}
+
+__global__ void zero_rows_kernel(double* x, int ldx, int k, int r0, int r1) {
+    const int64_t total = static_cast<int64_t>(r1 - r0) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = r0 + static_cast<int>(e / k), j = static_cast<int>(e % k);
+        x[static_cast<size_t>(i) * ldx + j] = 0.0;
+    }
+}
+
+__global__ void lincomb_kernel(int n, int k, double a, const double* x, int ldx, double b,
+                               const double* y, int ldy, double* out, int ldo) {
+    const int64_t total = static_cast<int64_t>(n) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e / k), j = static_cast<int>(e % k);
+        const double xv = x[static_cast<size_t>(i) * ldx + j];
+        const double yv = y[static_cast<size_t>(i) * ldy + j];
+        out[static_cast<size_t>(i) * ldo + j] = a * xv + b * yv;
+    }
+}
+
+__global__ void scale_rows_kernel(int n, int k, const double* __restrict__ t, const double* __restrict__ x,
+                                  int ldx, double* __restrict__ y, int ldy) {
+    const int64_t total = static_cast<int64_t>(n) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e / k), j = static_cast<int>(e % k);
+        const double xv = x[static_cast<size_t>(i) * ldx + j];
+        y[static_cast<size_t>(i) * ldy + j] = t ? t[i] * xv : xv;
+    }
+}
+
+__global__ void __launch_bounds__(256) coldot_partial(int n, const double* __restrict__ x, int ldx,
+                                                       const double* __restrict__ y, int ldy, int k,
+                                                       double* __restrict__ partial) {
+    __shared__ double red[8][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int c = blockIdx.y * 32 + tx;
+    const int nb = gridDim.x;
+    const int r0 = static_cast<int>((static_cast<int64_t>(n) * blockIdx.x) / nb);
+    const int r1 = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.x + 1)) / nb);
+    double acc = 0.0;
+    if (c < k)
+        for (int r = r0 + ty; r < r1; r += 8)
+            acc = fma(x[static_cast<size_t>(r) * ldx + c], y[static_cast<size_t>(r) * ldy + c], acc);
+    red[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && c < k) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += red[i][tx];
+        partial[static_cast<size_t>(blockIdx.x) * k + c] = s;
+    }
+}
+
+__global__ void cg_check_kernel(int k, const double* rs, const double* bnorm, int* active, int* count) {
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        if (active[c] && sqrt(rs[c]) < 1e-14 * bnorm[c]) active[c] = 0;
+        if (active[c]) atomicAdd(&cnt, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) count[0] = cnt;
+}
+
+__global__ void cg_step1_kernel(int n, int k, const double* rs, const double* pap, int* active, double* x,
+                                int ldx, double* r, int ldr, const double* p, int ldp, const double* ap,
+                                int ldap) {
+    const int64_t total = static_cast<int64_t>(n) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e / k), c = static_cast<int>(e % k);
+        if (!active[c] || !(pap[c] > 0.0)) continue;
+        const double alpha = rs[c] / pap[c];
+        x[static_cast<size_t>(i) * ldx + c] += alpha * p[static_cast<size_t>(i) * ldp + c];
+        r[static_cast<size_t>(i) * ldr + c] -= alpha * ap[static_cast<size_t>(i) * ldap + c];
+    }
+}
+
+__global__ void cg_deactivate_kernel(int k, const double* pap, int* active) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x)
+        if (active[c] && !(pap[c] > 0.0)) active[c] = 0;
+}
+
+__global__ void cg_step2_kernel(int n, int k, const double* rs, const double* rs_new, const int* active,
+                                const double* r, int ldr, double* p, int ldp) {
+    const int64_t total = static_cast<int64_t>(n) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e / k), c = static_cast<int>(e % k);
+        if (!active[c]) continue;
+        const double beta = rs_new[c] / rs[c];
+        double* pp = p + static_cast<size_t>(i) * ldp + c;
+        *pp = r[static_cast<size_t>(i) * ldr + c] + beta * *pp;
+    }
+}
+
+__global__ void cg_commit_rs(int k, double* rs, const double* rs_new, const int* active) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x)
+        if (active[c]) rs[c] = rs_new[c];
+}
+
+int elem_grid(int64_t total) {
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div64(total, 256), kSMs * 8)));
+}
+
+}  // namespace
+}  // namespace bk
+
+using namespace bk;
+
+extern "C" size_t bk_colnorm2_work_bytes(int n, int k) {
+    return static_cast<size_t>(row_blocks(n)) * static_cast<size_t>(k > 0 ? k : 1) * sizeof(double);
+}
+
+extern "C" int bk_colnorm2_d(int n, const double* x, int ldx, int k, double* out, void* work,
+                             void* stream) {
+    if (k <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    if (n <= 0) {
+        BK_RET(cudaMemsetAsync(out, 0, sizeof(double) * k, s));
+        return 0;
+    }
+    const int nb = row_blocks(n);
+    auto partial = static_cast<double*>(work);
+    colnorm2_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(n, x, ldx, k, partial);
+    sum_partials<<<ceil_div(k, 128), 128, 0, s>>>(nb, k, partial, out);
+    BK_LAUNCHED();
+}
+
+extern "C" size_t bk_residual_work_bytes(int n, int k) { return 2 * bk_colnorm2_work_bytes(n, k); }
+
+extern "C" int bk_residual_d(int n, const double* v, int ldv, const double* av, int ldav,
+                             const double* lambda, int k, double* r, int ldr, const double* t,
+                             double* w, int ldw, int w_from, double* rn2, double* vn2, void* work,
+                             void* stream) {
+    if (k <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    const int nb = row_blocks(n);
+    auto pr = static_cast<double*>(work);
+    auto pv = pr + static_cast<size_t>(nb) * k;
+    residual_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(
+        n, v, ldv, av, ldav, lambda, k, r, ldr, t, w, ldw, w_from, pr, pv);
+    residual_finish<<<ceil_div(k, 128), 128, 0, s>>>(nb, k, pr, pv, rn2, vn2);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_convergence_d(int k, const double* rn2, const double* vn2, const double* lambda,
+                                double norm_a, int n_ev, double tol, double* per_pair, double* rec,
+                                void* stream) {
+    convergence_kernel<<<1, 1024, 0, as_stream(stream)>>>(k, rn2, vn2, lambda, norm_a, n_ev, tol,
+                                                          per_pair, rec);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_copy_cols_d(int n, const double* src, int lds, int k, double* dst, int ldd,
+                              void* stream) {
+    if (n <= 0 || k <= 0 || src == dst) return 0;
+    const int grid = max(1, min(ceil_div(n, 8), kSMs * 16));
+    copy_cols_kernel<<<grid, 256, 0, as_stream(stream)>>>(n, src, lds, k, dst, ldd);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_cm_to_rm_d(int n, int k, const double* cm, int ldcm, double* rm, int ldrm,
+                             void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    cm_to_rm_kernel<<<dim3(ceil_div(n, 32), ceil_div(k, 32)), dim3(32, 8), 0, as_stream(stream)>>>(
+        n, k, cm, ldcm, rm, ldrm);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_rm_to_cm_d(int n, int k, const double* rm, int ldrm, double* cm, int ldcm,
+                             void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    rm_to_cm_kernel<<<dim3(ceil_div(n, 32), ceil_div(k, 32)), dim3(32, 8), 0, as_stream(stream)>>>(
+        n, k, rm, ldrm, cm, ldcm);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_axpby_d(int n, int k, double a, const double* x, int ldx, double b, double* y,
+                          int ldy, void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    axpby_kernel<<<elem_grid(static_cast<int64_t>(n) * k), 256, 0, as_stream(stream)>>>(n, k, a, x, ldx,
+                                                                                       b, y, ldy);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_zero_rows_d(double* x, int ldx, int k, int r0, int r1, void* stream) {
+    if (r1 <= r0 || k <= 0) return 0;
+    zero_rows_kernel<<<elem_grid(static_cast<int64_t>(r1 - r0) * k), 256, 0, as_stream(stream)>>>(
+        x, ldx, k, r0, r1);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_lincomb_d(int n, int k, double a, const double* x, int ldx, double b, const double* y,
+                            int ldy, double* out, int ldo, void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    lincomb_kernel<<<elem_grid(static_cast<int64_t>(n) * k), 256, 0, as_stream(stream)>>>(n, k, a, x, ldx, b,
+                                                                                          y, ldy, out, ldo);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_scale_rows_d(int n, int k, const double* t, const double* x, int ldx, double* y, int ldy,
+                               void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    scale_rows_kernel<<<elem_grid(static_cast<int64_t>(n) * k), 256, 0, as_stream(stream)>>>(n, k, t, x, ldx,
+                                                                                             y, ldy);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_coldot_d(int n, const double* x, int ldx, const double* y, int ldy, int k, double* out,
+                           void* work, void* stream) {
+    if (k <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    if (n <= 0) {
+        BK_RET(cudaMemsetAsync(out, 0, sizeof(double) * k, s));
+        return 0;
+    }
+    const int nb = row_blocks(n);
+    auto partial = static_cast<double*>(work);
+    coldot_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(n, x, ldx, y, ldy, k, partial);
+    sum_partials<<<ceil_div(k, 128), 128, 0, s>>>(nb, k, partial, out);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_cg_check_d(int k, const double* rs, const double* bnorm, int* active, int* count,
+                             void* stream) {
+    cg_check_kernel<<<1, 1024, 0, as_stream(stream)>>>(k, rs, bnorm, active, count);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_cg_step1_d(int n, int k, const double* rs, const double* pap, int* active, double* x,
+                             int ldx, double* r, int ldr, const double* p, int ldp, const double* ap, int ldap,
+                             void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    cg_step1_kernel<<<elem_grid(static_cast<int64_t>(n) * k), 256, 0, s>>>(n, k, rs, pap, active, x, ldx, r,
+                                                                           ldr, p, ldp, ap, ldap);
+    cg_deactivate_kernel<<<ceil_div(k, 256), 256, 0, s>>>(k, pap, active);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_cg_step2_d(int n, int k, double* rs, const double* rs_new, const int* active,
+                             const double* r, int ldr, double* p, int ldp, void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    cg_step2_kernel<<<elem_grid(static_cast<int64_t>(n) * k), 256, 0, s>>>(n, k, rs, rs_new, active, r, ldr,
+                                                                           p, ldp);
+    cg_commit_rs<<<ceil_div(k, 256), 256, 0, s>>>(k, rs, rs_new, active);
+    BK_LAUNCHED();
+}

@@ -1,0 +1,853 @@
+// Solver loops over device-resident blocks (single B200).
+//
+// This file restates the control flow of the reference's four solvers
+// (proj/src/solvers.cpp:204-463) — the same decisions, events, lock handling,
+// work-meter formulas and history records — while every O(n) operation runs
+// as a bk_* kernel on one CUDA stream.  Blocks are row-major n x ld buffers;
+// X (Ritz vectors), P (LOBPCG momentum) and W (preconditioned residual) are
+// adjacent column ranges of one buffer S, so the reference's hcat / leftCols /
+// rightCols become column offsets, and shrink/expand is a width change plus a
+// strided compaction copy (K7).  The host reads back one small record per
+// iteration (r_overall, converged prefix, non-finite flag) plus the kept count
+// of each orthonormalisation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+
+#include "host.hpp"
+
+namespace b2 {
+
+namespace {
+
+constexpr double kDropTol = 1e-8;  // kDropTolDefault, proj/src/kernel.hpp:17
+
+int round8(int x) { return (x + 7) & ~7; }
+
+struct Blk {
+    double* p;
+    int ld;
+    Blk at(int c) const { return {p + c, ld}; }
+};
+
+#define BKC(call) cuda_check((call), #call)
+
+// pinned host staging for the per-iteration record and small infos
+struct Pinned {
+    double* rec = nullptr;  // 4 doubles
+    int* info = nullptr;    // 16 ints
+    Pinned() {
+        BKC(cudaMallocHost(reinterpret_cast<void**>(&rec), 4 * sizeof(double)));
+        BKC(cudaMallocHost(reinterpret_cast<void**>(&info), 16 * sizeof(int)));
+    }
+    ~Pinned() {
+        cudaFreeHost(rec);
+        cudaFreeHost(info);
+    }
+};
+
+// Work counters with the reference formulas (proj/src/solvers.cpp:26-60).
+struct Meter {
+    Work w;
+    int64_t rr_flops = 0;
+    int iter_rr_dim = 0;
+    void begin_iteration() { iter_rr_dim = 0; }
+    void ortho(int64_t n, int64_t k) { w.ortho_flops += n * k * k; }
+    void proj_ortho(int64_t n, int64_t k, int64_t m) { w.ortho_flops += n * k * (2 * m + k); }
+    void rr(int64_t n, int64_t d) {
+        w.spmv_cols += d;
+        rr_flops += 2 * n * d * d + d * d * d;
+        iter_rr_dim = static_cast<int>(d);
+    }
+};
+
+// reference StagnationGuard (solvers.cpp:128-143)
+struct Stagnation {
+    double mark = std::numeric_limits<double>::infinity();
+    int mark_iter = 0;
+    bool update(int j, double overall) {
+        const double lg = std::log10(std::max(overall, 1e-300));
+        if (lg <= mark - 0.01) {
+            mark = lg;
+            mark_iter = j;
+            return false;
+        }
+        return j - mark_iter >= 50;
+    }
+};
+
+class Engine {
+public:
+    Engine(const SparseSym& a, const SolverConfig& cfg, SolverKind kind)
+        : a_(a), cfg_(cfg), kind_(kind), n_(a.rows()), rng_(cfg.seed) {
+        BKC(cudaSetDevice(cfg.device));
+        csr_ = &a.device_csr(cfg.device, cfg.largest);
+        BKC(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        const int n_ex = cfg.n_ex, n_es = cfg.n_es;
+        const int xd = std::max(1, 2 * (n_ex - n_es));
+        tcap_ = std::max(n_ex, xd);
+        dcap_ = 3 * n_ex + xd;
+        dcap_ = std::min(dcap_, std::max(n_, 1));
+        dcap_ = std::max(dcap_, n_ex);
+        ldS_ = round8(std::max(dcap_ + tcap_, 8));
+        ldT_ = round8(std::max(tcap_, 8));
+        const size_t n = static_cast<size_t>(std::max(n_, 1));
+        for (auto& s : S_) s.alloc(n * ldS_ * sizeof(double));
+        AS_.alloc(n * ldS_ * sizeof(double));
+        R_.alloc(n * ldT_ * sizeof(double));
+        XD_.alloc(n * ldT_ * sizeof(double));
+        T1_.alloc(n * ldT_ * sizeof(double));
+        T2_.alloc(n * ldT_ * sizeof(double));
+        PT_.alloc(n * ldT_ * sizeof(double));
+        VEC_.alloc(n * sizeof(double));
+        const size_t dc = static_cast<size_t>(dcap_) + tcap_;
+        ldH_ = static_cast<int>(dc);
+        H_.alloc(dc * dc * sizeof(double));
+        Z_.alloc(dc * dc * sizeof(double));
+        ZC_.alloc(dc * dc * sizeof(double));
+        CZ_.alloc(dc * dc * sizeof(double));
+        VALS_.alloc(dc * sizeof(double));
+        COEF_.alloc(dc * static_cast<size_t>(tcap_) * sizeof(double) + 64);
+        GB_.alloc(static_cast<size_t>(tcap_) * tcap_ * sizeof(double));
+        M1_.alloc(static_cast<size_t>(tcap_) * tcap_ * sizeof(double));
+        M2_.alloc(static_cast<size_t>(tcap_) * tcap_ * sizeof(double));
+        SMALL_.alloc(8 * dc * sizeof(double));
+        INFO_.alloc(64 * sizeof(int));
+        size_t work = bk_gram_work_bytes(n_, static_cast<int>(dc), static_cast<int>(dc));
+        work = std::max(work, bk_chol_work_bytes(std::max(tcap_, 1)));
+        work = std::max(work, bk_syev_work_bytes(static_cast<int>(dc)));
+        work = std::max(work, bk_residual_work_bytes(n_, static_cast<int>(dc)));
+        work = std::max(work, bk_colnorm2_work_bytes(n_, static_cast<int>(dc)));
+        WORK_.alloc(work);
+        if (cfg.precond == Precond::diagonal) {
+            std::vector<double> t(n);
+            for (int i = 0; i < n_; ++i) t[i] = 1.0 / std::max(std::fabs(a.diagonal(i)), 1e-12);
+            TD_.alloc(n * sizeof(double));
+            BKC(cudaMemcpyAsync(TD_.d(), t.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream_));
+        }
+        norm_a_ = a.norm_est();
+    }
+    ~Engine() {
+        if (stream_) {
+            cudaStreamSynchronize(stream_);
+            cudaStreamDestroy(stream_);
+        }
+    }
+
+    SolveOutput run(const double* x0, int x0_cols);
+    void set_strategy(const StrategyConfig& s) { strategy_ = s; }
+
+private:
+    StrategyConfig strategy_;
+    // ---------------------------------------------------------------- primitives
+    void* st() const { return stream_; }
+    Blk S(int i) const { return {S_[i].d(), ldS_}; }
+    Blk AS() const { return {AS_.d(), ldS_}; }
+    Blk T1() const { return {T1_.d(), ldT_}; }
+    Blk T2() const { return {T2_.d(), ldT_}; }
+
+    void sync() { BKC(cudaStreamSynchronize(stream_)); }
+
+    void spmm(Blk x, int k, Blk y) {
+        if (k <= 0) return;
+        BKC(bk_spmm_d(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
+                      y.ld, st()));
+    }
+    void copy(int rows, Blk src, int k, Blk dst) {
+        if (k > 0 && rows > 0) BKC(bk_copy_cols_d(rows, src.p, src.ld, k, dst.p, dst.ld, st()));
+    }
+
+    // host std::mt19937_64 / normal_distribution block (random_block,
+    // kernel.cpp:166-172: a fresh distribution per call, column-major fill),
+    // uploaded into dst (row-major)
+    void random_block(int cols, Blk dst) {
+        if (cols <= 0) return;
+        std::normal_distribution<double> dist(0.0, 1.0);
+        std::vector<double> h(static_cast<size_t>(n_) * cols);
+        for (auto& x : h) x = dist(rng_);
+        upload_colmajor(h.data(), cols, dst);
+    }
+    void upload_colmajor(const double* h, int cols, Blk dst) {
+        const size_t bytes = static_cast<size_t>(n_) * cols * sizeof(double);
+        if (stage_.bytes() < bytes) stage_.alloc(bytes);
+        BKC(cudaMemcpyAsync(stage_.d(), h, bytes, cudaMemcpyHostToDevice, stream_));
+        BKC(bk_cm_to_rm_d(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
+        sync();  // the host buffer may be released by the caller
+    }
+
+    // K4: project w (rows x a, clobbered) against q (rows x m), orthonormalise
+    // the rest with the CGS2 drop rule; kept columns land packed in out.
+    // (project_orthonormalize, proj/src/kernel.cpp:65-89)
+    int proj_ortho(int rows, Blk w, int a, Blk q, int m, Blk out) {
+        if (a <= 0) return 0;
+        double* ref2 = SMALL_.d();  // a doubles
+        BKC(bk_colnorm2_d(rows, w.p, w.ld, a, ref2, WORK_.p(), st()));
+        if (m > 0)
+            for (int pass = 0; pass < 2; ++pass) {
+                BKC(bk_gram_d(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a, WORK_.p(), st()));
+                BKC(bk_gemm_d(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld, st()));
+            }
+        BKC(bk_gram_d(rows, w.p, w.ld, a, w.p, w.ld, a, GB_.d(), a, WORK_.p(), st()));
+        int* info = INFO_.as<int>();
+        BKC(bk_chol_drop_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
+        BKC(cudaMemcpyAsync(pin_.info, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        sync();
+        if (debug_) debug_pivots(a, ref2);
+        if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
+        if (pin_.info[1]) return cgs2_fallback(rows, w, a, q, m, out);
+        const int kept = pin_.info[0];
+        if (kept == 0) return 0;
+        Blk pt{PT_.d(), ldT_};
+        BKC(bk_gemm_d(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld, st()));
+        // second CholQR pass (no dropping: every pivot is ~1 after pass one)
+        BKC(bk_gram_d(rows, pt.p, pt.ld, kept, pt.p, pt.ld, kept, GB_.d(), kept, WORK_.p(), st()));
+        BKC(bk_chol_drop_d(kept, GB_.d(), kept, nullptr, 0.0, M2_.d(), kept, info, WORK_.p(), st()));
+        BKC(cudaMemcpyAsync(pin_.info, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        BKC(bk_gemm_d(rows, pt.p, pt.ld, kept, M2_.d(), kept, kept, 1.0, 0.0, out.p, out.ld, st()));
+        sync();
+        if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
+        if (pin_.info[1] || pin_.info[0] != kept) return cgs2_fallback(rows, w, a, q, m, out);
+        return kept;
+    }
+
+    // BLOCKEIG_DEBUG=1: recompute the pivot ratios on the host and log them
+    void debug_pivots(int a, const double* ref2_dev) {
+        std::vector<double> g(static_cast<size_t>(a) * a), ref2(a);
+        BKC(cudaMemcpy(g.data(), GB_.d(), g.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        BKC(cudaMemcpy(ref2.data(), ref2_dev, a * sizeof(double), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[blockeig] proj_ortho a=%d kept=%d unsure=%d:", a, pin_.info[0], pin_.info[1]);
+        std::vector<double> s = g;  // host replica of the right-looking skip-pivot Cholesky
+        for (int j = 0; j < a; ++j) {
+            const double p = s[static_cast<size_t>(j) * a + j];
+            const double gjj = g[static_cast<size_t>(j) * a + j];
+            const double ratio = ref2[j] > 0 ? std::sqrt(std::max(p, 0.0) / ref2[j]) : 0.0;
+            const double proj = ref2[j] > 0 ? std::sqrt(gjj / ref2[j]) : 0.0;
+            const bool keep = ref2[j] > 0 && p >= kDropTol * kDropTol * ref2[j];
+            if (ratio < 1e-1 || !keep)
+                std::fprintf(stderr, " [col %d piv/ref=%.3e proj/ref=%.3e keep=%d]", j, ratio, proj, keep);
+            if (!keep) continue;
+            const double r = std::sqrt(p);
+            for (int l = j + 1; l < a; ++l) s[static_cast<size_t>(j) * a + l] /= r;
+            for (int k = j + 1; k < a; ++k)
+                for (int l = k; l < a; ++l)
+                    s[static_cast<size_t>(k) * a + l] -= s[static_cast<size_t>(j) * a + k] * s[static_cast<size_t>(j) * a + l];
+        }
+        std::fprintf(stderr, "\n");
+    }
+
+    // exact column CGS2 (kernel.cpp:71-86) for blocks whose Cholesky pivots
+    // were not decisive; w already carries the external projection
+    int cgs2_fallback(int rows, Blk w, int a, Blk q, int m, Blk out) {
+        ++fallbacks_;
+        std::vector<double> ref2(a);
+        BKC(cudaMemcpyAsync(ref2.data(), SMALL_.d(), a * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        sync();
+        Blk v{VEC_.d(), 1};
+        double* c = COEF_.d();
+        double* nrm2 = SMALL_.d() + tcap_;
+        int kept = 0;
+        for (int j = 0; j < a; ++j) {
+            if (ref2[j] == 0.0) continue;
+            copy(rows, w.at(j), 1, v);
+            for (int pass = 0; pass < 2; ++pass) {
+                if (m > 0) {
+                    BKC(bk_gram_d(rows, q.p, q.ld, m, v.p, 1, 1, c, 1, WORK_.p(), st()));
+                    BKC(bk_gemm_d(rows, q.p, q.ld, m, c, 1, 1, -1.0, 1.0, v.p, 1, st()));
+                }
+                if (kept > 0) {
+                    BKC(bk_gram_d(rows, out.p, out.ld, kept, v.p, 1, 1, c, 1, WORK_.p(), st()));
+                    BKC(bk_gemm_d(rows, out.p, out.ld, kept, c, 1, 1, -1.0, 1.0, v.p, 1, st()));
+                }
+            }
+            BKC(bk_colnorm2_d(rows, v.p, 1, 1, nrm2, WORK_.p(), st()));
+            double h = 0.0;
+            BKC(cudaMemcpyAsync(&pin_.rec[3], nrm2, sizeof(double), cudaMemcpyDeviceToHost, stream_));
+            sync();
+            h = pin_.rec[3];
+            const double nrm = std::sqrt(h);
+            if (!std::isfinite(nrm)) throw std::runtime_error("orthonormalization: non-finite values");
+            if (nrm < kDropTol * std::sqrt(ref2[j])) continue;
+            BKC(bk_axpby_d(rows, 1, 1.0 / nrm, v.p, 1, 0.0, out.at(kept).p, out.ld, st()));
+            ++kept;
+        }
+        return kept;
+    }
+
+    // count fresh orthonormal random columns orthogonal to q = [vs | acc],
+    // written right after q (out == q.at(m)) — fresh_cols, solvers.cpp:64-74
+    void fresh_cols(int count, Blk q, int m) {
+        int acc = 0;
+        for (int attempt = 0; acc < count && attempt < 8; ++attempt) {
+            const int want = count - acc;
+            random_block(want, T2());
+            meter_.proj_ortho(n_, want, m + acc);
+            const int kept = proj_ortho(n_, T2(), want, q, m + acc, q.at(m + acc));
+            acc += kept;
+        }
+        if (acc < count) throw std::runtime_error("block rank collapsed beyond recovery");
+    }
+
+    // Rayleigh-Ritz on s[:, 0:d]; columns [0, as_from) of AS already hold A s.
+    // values -> VALS (ascending), coefficients -> Z (ldH)  (rr.cpp:8-14)
+    void rayleigh_ritz(Blk s, int d, int as_from) {
+        meter_.rr(n_, d);
+        spmm(s.at(as_from), d - as_from, AS().at(as_from));
+        BKC(bk_gram_d(n_, s.p, s.ld, d, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
+        int* info = INFO_.as<int>() + 8;
+        BKC(bk_syev_d(d, H_.d(), ldH_, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
+        BKC(cudaMemcpyAsync(pin_.info + 8, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        syev_pending_ = true;
+    }
+    void check_syev() {
+        if (!syev_pending_) return;
+        syev_pending_ = false;
+        max_sweeps_ = std::max(max_sweeps_, pin_.info[8]);
+        if (pin_.info[9]) throw std::runtime_error("sym_eig_small: eigensolver failed");
+    }
+
+    // out[:, 0:k] = s[:, 0:d] Z[:, 0:k]
+    void lift(Blk s, int d, const double* z, int ldz, int k, Blk out) {
+        BKC(bk_gemm_d(n_, s.p, s.ld, d, z, ldz, k, 1.0, 0.0, out.p, out.ld, st()));
+    }
+
+    struct Rep {
+        double overall;
+        int converged;
+    };
+    // AV into AS[:, 0:k], R = AV - V diag(VALS) into R, record read back
+    // (residual_block + assess_convergence, rr.cpp:16-38)
+    Rep residual(Blk v, int k, int n_ev) {
+        meter_.w.spmv_cols += k;
+        if (debug_) std::fprintf(stderr, "[blockeig] iteration %zu k=%d\n", out_.history.size() + 1, k);
+        spmm(v, k, AS());
+        double* rn2 = SMALL_.d();
+        double* vn2 = SMALL_.d() + dcap_ + tcap_;
+        BKC(bk_residual_d(n_, v.p, v.ld, AS_.d(), ldS_, VALS_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0, rn2,
+                          vn2, WORK_.p(), st()));
+        double* rec = SMALL_.d() + 2 * (dcap_ + tcap_);
+        BKC(bk_convergence_d(k, rn2, vn2, VALS_.d(), norm_a_, n_ev, cfg_.tol, nullptr, rec, st()));
+        BKC(cudaMemcpyAsync(pin_.rec, rec, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        sync();
+        check_syev();
+        if (pin_.rec[2] != 0.0) throw std::runtime_error("non-finite residual or Ritz value");
+        return {pin_.rec[0], static_cast<int>(pin_.rec[1])};
+    }
+
+    // y = op(x): shifted operator c x - M x (extension) or shift-and-invert
+    // (A - zeta I)^{-1} x through the dense factor (reference SpdFactor dense path)
+    void apply_op(Blk x, int k, Blk ax_known, bool have_ax, Blk y) {
+        if (k <= 0) return;
+        if (cfg_.op_shifted) {
+            if (!have_ax) {
+                spmm(x, k, T2());
+                ax_known = T2();
+            }
+            BKC(bk_lincomb_d(n_, k, cfg_.op_c, x.p, x.ld, -1.0, ax_known.p, ax_known.ld, y.p, y.ld, st()));
+            return;
+        }
+        // (A - zeta I)^{-1} = M M^T with M = R^{-1} from the dense Cholesky
+        BKC(bk_gram_d(n_, INV_.d(), n_, n_, x.p, x.ld, k, PT_.d(), ldT_, WORK_.p(), st()));
+        BKC(bk_gemm_d(n_, INV_.d(), n_, n_, PT_.d(), ldT_, k, 1.0, 0.0, y.p, y.ld, st()));
+    }
+    void factor_shift_invert();
+
+    void push(int j, double overall, int n_now, Event ev, int lock) {
+        Record r{j, overall, n_now, ev, lock, meter_.w};
+        r.work.rr_dim = meter_.iter_rr_dim;
+        out_.history.push_back(r);
+    }
+    void finish(Status status, Blk v, int n_ev) {
+        sync();
+        check_syev();
+        out_.status = status;
+        out_.values.resize(n_ev);
+        BKC(cudaMemcpyAsync(out_.values.data(), VALS_.d(), n_ev * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        BKC(bk_rm_to_cm_d(n_, n_ev, v.p, v.ld, PT_.d(), n_, st()));
+        out_.vectors.resize(static_cast<size_t>(n_) * n_ev);
+        BKC(cudaMemcpyAsync(out_.vectors.data(), PT_.d(), out_.vectors.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, stream_));
+        sync();
+        if (cfg_.largest)
+            for (auto& x : out_.values) x = -x;
+        out_.iterations = static_cast<int>(out_.history.size());
+        out_.work = meter_.w;
+        out_.work.rr_dim = meter_.iter_rr_dim;
+        out_.rr_flops = meter_.rr_flops;
+        out_.cgs2_fallbacks = fallbacks_;
+        out_.max_jacobi_sweeps = max_sweeps_;
+    }
+
+    int initial_block(const double* x0, int x0_cols, Blk dst);
+    void solve_si();
+    void solve_sd();
+    void solve_lobpcg();
+    void solve_tracemin();
+
+    const SparseSym& a_;
+    SolverConfig cfg_;
+    SolverKind kind_;
+    int n_;
+    std::mt19937_64 rng_;
+    const DeviceCsr* csr_ = nullptr;
+    cudaStream_t stream_ = nullptr;
+    int tcap_ = 0, dcap_ = 0, ldS_ = 0, ldT_ = 0, ldH_ = 0;
+    DevMem S_[2], AS_, R_, XD_, T1_, T2_, PT_, VEC_, H_, Z_, ZC_, CZ_, VALS_, COEF_, GB_, M1_, M2_, SMALL_,
+        INFO_, WORK_, TD_, INV_, stage_;
+    DevMem CG_[6];
+    Pinned pin_;
+    double norm_a_ = 0.0;
+    Meter meter_;
+    SolveOutput out_;
+    int fallbacks_ = 0, max_sweeps_ = 0;
+    bool syev_pending_ = false;
+    const bool debug_ = std::getenv("BLOCKEIG_DEBUG") != nullptr;
+    int cur_ = 0;  // which S buffer holds the current block
+    int xd_cols_ = 0;
+    const double* x0_ = nullptr;
+    int x0_cols_ = 0;
+};
+
+// Dense factor of A - zeta I for the reference's shift-and-invert SI (the
+// SpdFactor dense path, kernel.cpp:102-137, n <= 2000): K4's Cholesky kernel
+// without dropping gives M = R^{-1}, so (A - zeta I)^{-1} = M M^T.
+void Engine::factor_shift_invert() {
+    if (n_ > 2000)
+        throw std::invalid_argument(
+            "shift-and-invert SI is limited to n <= 2000 on the device build; use the shifted operator mode");
+    const size_t nn = static_cast<size_t>(n_) * n_;
+    std::vector<double> dense(nn, 0.0);
+    const double sgn = cfg_.largest ? -1.0 : 1.0;
+    for (int r = 0; r < n_; ++r)
+        for (int64_t p = a_.row_ptr()[r]; p < a_.row_ptr()[r + 1]; ++p) {
+            const int c = a_.col()[p];
+            dense[static_cast<size_t>(r) * n_ + c] = sgn * a_.val()[p];
+            dense[static_cast<size_t>(c) * n_ + r] = sgn * a_.val()[p];
+        }
+    for (int i = 0; i < n_; ++i) dense[static_cast<size_t>(i) * n_ + i] -= cfg_.shift;
+    DevMem g(nn * sizeof(double)), work(bk_chol_work_bytes(n_));
+    INV_.alloc(nn * sizeof(double));
+    BKC(cudaMemcpyAsync(g.d(), dense.data(), nn * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    int* info = INFO_.as<int>() + 16;
+    BKC(bk_chol_drop_d(n_, g.d(), n_, nullptr, 0.0, INV_.d(), n_, info, work.p(), st()));
+    BKC(cudaMemcpyAsync(pin_.info + 4, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    sync();
+    if (pin_.info[4] != n_ || pin_.info[6]) throw std::runtime_error("SpdFactor: matrix is not positive definite");
+}
+
+// solvers.cpp:82-96
+int Engine::initial_block(const double* x0, int x0_cols, Blk dst) {
+    const int n_ex = cfg_.n_ex;
+    if (x0 != nullptr) {
+        if (x0_cols != n_ex) throw std::invalid_argument("initial block must be n x n_ex");
+        upload_colmajor(x0, n_ex, T1());
+    } else {
+        random_block(n_ex, T1());
+    }
+    meter_.ortho(n_, n_ex);
+    const int kept = proj_ortho(n_, T1(), n_ex, {nullptr, 0}, 0, dst);
+    if (x0 != nullptr && kept < n_ex) throw std::invalid_argument("initial block is rank deficient");
+    if (kept < n_ex) fresh_cols(n_ex - kept, dst, kept);
+    return n_ex;
+}
+
+// solvers.cpp:204-259 (+ operator mode)
+void Engine::solve_si() {
+    const int n_ex = cfg_.n_ex, n_es = cfg_.n_es, n_ev = cfg_.n_ev;
+    if (!cfg_.op_shifted) factor_shift_invert();
+    initial_block(x0_, x0_cols_, S(cur_));
+    rayleigh_ritz(S(cur_), n_ex, 0);
+    lift(S(cur_), n_ex, Z_.d(), ldH_, n_ex, S(1 - cur_));
+    cur_ ^= 1;
+    int n_now = n_ex;
+    BlockSizer sizer(strategy_);
+    Stagnation guard;
+    const Blk xd{XD_.d(), ldT_};
+    for (int j = 1; j <= cfg_.max_iters; ++j) {
+        meter_.begin_iteration();
+        const Blk v = S(cur_);
+        const Rep rep = residual(v, n_now, n_ev);
+        if (rep.converged >= n_ev) {
+            push(j, rep.overall, n_now, Event::none, 0);
+            return finish(Status::converged, v, n_ev);
+        }
+        if (guard.update(j, rep.overall)) {
+            push(j, rep.overall, n_now, Event::none, 0);
+            return finish(Status::stagnated, v, n_ev);
+        }
+        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        meter_.w.solve_cols += n_now;
+        apply_op(v, n_now, AS(), true, T1());
+        if (cfg_.expand == ExpandMode::powered && xd_cols_ > 0) {
+            meter_.w.solve_cols += xd_cols_;
+            apply_op(xd, xd_cols_, AS(), false, xd);
+        }
+        Event ev = Event::none;
+        int ycols = n_now;
+        if (d == Decision::expand) {
+            const int e = cfg_.expand == ExpandMode::random ? n_ex - n_now : xd_cols_;
+            if (e > 0) {
+                if (cfg_.expand == ExpandMode::random) random_block(e, T1().at(n_now));
+                else copy(n_, xd, e, T1().at(n_now));
+                ycols += e;
+                xd_cols_ = 0;
+                n_now = n_ex;
+                ev = Event::expand;
+            }
+        }
+        meter_.ortho(n_, ycols);
+        const int kept = proj_ortho(n_, T1(), ycols, {nullptr, 0}, 0, S(cur_));
+        if (kept < n_now) fresh_cols(n_now - kept, S(cur_), kept);
+        rayleigh_ritz(S(cur_), n_now, 0);
+        lift(S(cur_), n_now, Z_.d(), ldH_, n_now, S(1 - cur_));
+        cur_ ^= 1;
+        if (d == Decision::shrink) {
+            copy(n_, S(cur_).at(n_es), n_now - n_es, xd);
+            xd_cols_ = n_now - n_es;
+            n_now = n_es;
+            ev = Event::shrink;
+        }
+        push(j, rep.overall, n_now, ev, 0);
+    }
+    finish(Status::max_iters, S(cur_), n_ev);
+}
+
+// solvers.cpp:261-314
+void Engine::solve_sd() {
+    const int n_ex = cfg_.n_ex, n_es = cfg_.n_es, n_ev = cfg_.n_ev;
+    initial_block(x0_, x0_cols_, S(cur_));
+    rayleigh_ritz(S(cur_), n_ex, 0);
+    lift(S(cur_), n_ex, Z_.d(), ldH_, n_ex, S(1 - cur_));
+    cur_ ^= 1;
+    int n_now = n_ex;
+    BlockSizer sizer(strategy_);
+    const Blk xd{XD_.d(), ldT_};
+    const double* td = TD_.bytes() ? TD_.d() : nullptr;
+    for (int j = 1; j <= cfg_.max_iters; ++j) {
+        meter_.begin_iteration();
+        const Blk v = S(cur_);
+        const Rep rep = residual(v, n_now, n_ev);
+        if (rep.converged >= n_ev) {
+            push(j, rep.overall, n_now, Event::none, 0);
+            return finish(Status::converged, v, n_ev);
+        }
+        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        Event ev = Event::none;
+        const int n_old = n_now;
+        int xb = n_now;
+        if (d == Decision::expand) {
+            const int e = cfg_.expand == ExpandMode::random ? n_ex - n_now : xd_cols_;
+            if (e > 0) {
+                if (cfg_.expand == ExpandMode::random) random_block(e, T1());
+                else copy(n_, xd, e, T1());
+                meter_.proj_ortho(n_, e, xb);
+                xb += proj_ortho(n_, T1(), e, v, xb, v.at(xb));
+                if (xb < n_ex) {
+                    fresh_cols(n_ex - xb, v, xb);
+                    xb = n_ex;
+                }
+                xd_cols_ = 0;
+                n_now = n_ex;
+                ev = Event::expand;
+            }
+        }
+        BKC(bk_scale_rows_d(n_, n_old, td, R_.d(), ldT_, T1().p, ldT_, st()));
+        meter_.proj_ortho(n_, n_old, xb);
+        const int kw = proj_ortho(n_, T1(), n_old, v, xb, v.at(xb));
+        if (kw == 0) {
+            push(j, rep.overall, n_now, ev, 0);
+            return finish(Status::stagnated, v, n_ev);
+        }
+        const int ds = xb + kw;
+        rayleigh_ritz(v, ds, n_old);
+        lift(v, ds, Z_.d(), ldH_, n_now, S(1 - cur_));
+        cur_ ^= 1;
+        if (d == Decision::shrink) {
+            copy(n_, S(cur_).at(n_es), n_now - n_es, xd);
+            xd_cols_ = n_now - n_es;
+            n_now = n_es;
+            ev = Event::shrink;
+        }
+        push(j, rep.overall, n_now, ev, 0);
+    }
+    finish(Status::max_iters, S(cur_), n_ev);
+}
+
+// solvers.cpp:316-401.  Layout of the current buffer: [X (n_now) | P (np)],
+// with W appended after P inside the iteration.
+void Engine::solve_lobpcg() {
+    const int n_ex = cfg_.n_ex, n_es = cfg_.n_es, n_ev = cfg_.n_ev;
+    initial_block(x0_, x0_cols_, S(cur_));
+    rayleigh_ritz(S(cur_), n_ex, 0);
+    lift(S(cur_), n_ex, Z_.d(), ldH_, n_ex, S(1 - cur_));
+    cur_ ^= 1;
+    int n_now = n_ex, np = 0, prev_lock = 0;
+    BlockSizer sizer(strategy_);
+    const Blk xd{XD_.d(), ldT_};
+    const double* td = TD_.bytes() ? TD_.d() : nullptr;
+    const Blk zc{ZC_.d(), ldH_}, cz{CZ_.d(), ldH_}, z{Z_.d(), ldH_};
+    for (int j = 1; j <= cfg_.max_iters; ++j) {
+        meter_.begin_iteration();
+        Blk s = S(cur_);
+        const Rep rep = residual(s, n_now, n_ev);
+        const int lock = std::min(rep.converged, n_now - 1);
+        if (rep.converged >= n_ev) {
+            push(j, rep.overall, n_now, Event::none, lock);
+            return finish(Status::converged, s, n_ev);
+        }
+        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        const int active = n_now - lock;
+        // soft locking: P loses its leading (lock - prev_lock) columns
+        if (lock > prev_lock && np > 0) {
+            const int drop = std::min(lock - prev_lock, np);
+            copy(n_, s.at(n_now + drop), np - drop, s.at(n_now));
+            np -= drop;
+        }
+        // W = T R(:, lock:) orthonormalised against [X, P]
+        BKC(bk_scale_rows_d(n_, active, td, R_.d() + lock, ldT_, T1().p, ldT_, st()));
+        int m = n_now + np;
+        meter_.proj_ortho(n_, active, m);
+        const int kw = proj_ortho(n_, T1(), active, s, m, s.at(m));
+        if (kw == 0) {
+            push(j, rep.overall, n_now, Event::none, lock);
+            return finish(Status::stagnated, s, n_ev);
+        }
+        Event ev = Event::none;
+        const int n_old = n_now;
+        int ds = m + kw;
+        if (d == Decision::expand) {
+            const int want = 2 * (n_ex - n_es);
+            const int e = cfg_.expand == ExpandMode::random ? want : xd_cols_;
+            if (e > 0) {
+                if (cfg_.expand == ExpandMode::random) random_block(e, T1());
+                else copy(n_, xd, e, T1());
+                meter_.proj_ortho(n_, e, ds);
+                const int oe = proj_ortho(n_, T1(), e, s, ds, T2());
+                const int hx = std::min((oe + 1) / 2, n_ex - n_now);
+                // other buffer: [X | oe(:, :hx) | P | oe(:, hx:) | W]
+                Blk o = S(1 - cur_);
+                int c = 0;
+                copy(n_, s, n_now, o);
+                c += n_now;
+                copy(n_, T2(), hx, o.at(c));
+                c += hx;
+                const int xb = c;
+                copy(n_, s.at(n_now), np, o.at(c));
+                c += np;
+                copy(n_, T2().at(hx), oe - hx, o.at(c));
+                c += oe - hx;
+                const int pn = np + oe - hx;
+                copy(n_, s.at(m), kw, o.at(c));
+                c += kw;
+                if (xb < n_ex) {
+                    // fresh columns orthogonal to [xb, p, W]; then insert them after xb
+                    const int f = n_ex - xb;
+                    fresh_cols(f, o, c);
+                    copy(n_, o, xb, s);
+                    copy(n_, o.at(c), f, s.at(xb));
+                    copy(n_, o.at(xb), pn + kw, s.at(n_ex));
+                } else {
+                    cur_ ^= 1;
+                    s = S(cur_);
+                }
+                xd_cols_ = 0;
+                n_now = n_ex;
+                np = pn;
+                ev = Event::expand;
+                m = n_now + np;
+                ds = m + kw;
+            }
+        }
+        // Rayleigh-Ritz on S = [X, P, W]; A X is still in AS(:, 0:n_old)
+        rayleigh_ritz(s, ds, n_old);
+        // HL trick (solvers.cpp:187-196) in coefficient space:
+        // ZC = [Z(:, :n_now) | orth(Zp)], Zp = Z(:, lock:n_now) with rows < n_now zeroed
+        const int ahl = n_now - lock;  // n_now is post-expansion here
+        copy(ds, z, n_now, zc);
+        copy(ds, z.at(lock), ahl, cz);
+        BKC(bk_zero_rows_d(cz.p, cz.ld, ahl, 0, n_now, st()));
+        const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now));
+        meter_.w.ortho_flops += static_cast<int64_t>(ds) * (n_now - lock) * (2 * n_now + (n_now - lock));
+        // [X, P] = S ZC
+        lift(s, ds, zc.p, zc.ld, n_now + pk, S(1 - cur_));
+        cur_ ^= 1;
+        np = pk;
+        if (d == Decision::shrink) {
+            const Blk nx = S(cur_);
+            const int dx = n_now - n_es;
+            const int dp = np > n_es ? np - n_es : 0;
+            copy(n_, nx.at(n_es), dx, xd);
+            copy(n_, nx.at(n_now + n_es), dp, xd.at(dx));
+            xd_cols_ = dx + dp;
+            np = std::min(np, n_es);
+            copy(n_, nx.at(n_now), np, nx.at(n_es));
+            n_now = n_es;
+            ev = Event::shrink;
+        }
+        if (ev == Event::none && lock > prev_lock) ev = Event::lock;
+        push(j, rep.overall, n_now, ev, lock);
+        prev_lock = lock;
+    }
+    finish(Status::max_iters, S(cur_), n_ev);
+}
+
+// solvers.cpp:403-463 with cg_solve (kernel.cpp:139-164) batched over columns
+void Engine::solve_tracemin() {
+    const int n_ex = cfg_.n_ex, n_es = cfg_.n_es, n_ev = cfg_.n_ev;
+    initial_block(x0_, x0_cols_, S(cur_));
+    rayleigh_ritz(S(cur_), n_ex, 0);
+    lift(S(cur_), n_ex, Z_.d(), ldH_, n_ex, S(1 - cur_));
+    cur_ ^= 1;
+    const size_t blk = static_cast<size_t>(std::max(n_, 1)) * ldT_ * sizeof(double);
+    for (int i = 0; i < 4; ++i) CG_[i].alloc(blk);
+    CG_[4].alloc(8 * static_cast<size_t>(tcap_) * sizeof(double));
+    CG_[5].alloc(static_cast<size_t>(tcap_) * sizeof(int) + 64);
+    const Blk cx{CG_[0].d(), ldT_}, cr{CG_[1].d(), ldT_}, cp{CG_[2].d(), ldT_}, cap{CG_[3].d(), ldT_};
+    double* rs = CG_[4].d();
+    double* bnorm = rs + tcap_;
+    double* pap = rs + 2 * tcap_;
+    double* rs_new = rs + 3 * tcap_;
+    int* act = CG_[5].as<int>();
+    int n_now = n_ex;
+    BlockSizer sizer(strategy_);
+    const Blk xd{XD_.d(), ldT_};
+    for (int j = 1; j <= cfg_.max_iters; ++j) {
+        meter_.begin_iteration();
+        const Blk v = S(cur_);
+        const Rep rep = residual(v, n_now, n_ev);
+        if (rep.converged >= n_ev) {
+            push(j, rep.overall, n_now, Event::none, 0);
+            return finish(Status::converged, v, n_ev);
+        }
+        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        const int k = n_now;
+        // project(u) = u - V (V^T u), in place
+        auto project = [&](Blk u) {
+            BKC(bk_gram_d(n_, v.p, v.ld, k, u.p, u.ld, k, COEF_.d(), k, WORK_.p(), st()));
+            BKC(bk_gemm_d(n_, v.p, v.ld, k, COEF_.d(), k, k, -1.0, 1.0, u.p, u.ld, st()));
+        };
+        // rhs = P_V R; x = 0; p = r = rhs
+        copy(n_, {R_.d(), ldT_}, k, cr);
+        project(cr);
+        BKC(bk_axpby_d(n_, k, 0.0, cr.p, cr.ld, 0.0, cx.p, cx.ld, st()));
+        copy(n_, cr, k, cp);
+        BKC(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs, WORK_.p(), st()));
+        std::vector<double> h_rs(k);
+        BKC(cudaMemcpyAsync(h_rs.data(), rs, k * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        sync();
+        std::vector<double> h_b(k);
+        std::vector<int> h_act(k);
+        for (int c = 0; c < k; ++c) {
+            h_b[c] = std::sqrt(h_rs[c]);
+            h_act[c] = h_b[c] != 0.0;
+        }
+        BKC(cudaMemcpyAsync(bnorm, h_b.data(), k * sizeof(double), cudaMemcpyHostToDevice, stream_));
+        BKC(cudaMemcpyAsync(act, h_act.data(), k * sizeof(int), cudaMemcpyHostToDevice, stream_));
+        int* cnt = INFO_.as<int>() + 24;
+        for (int it = 0; it < cfg_.cg_iters; ++it) {
+            BKC(bk_cg_check_d(k, rs, bnorm, act, cnt, st()));
+            BKC(cudaMemcpyAsync(pin_.info + 12, cnt, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+            sync();
+            const int live = pin_.info[12];
+            if (live == 0) break;
+            meter_.w.spmv_cols += live;
+            // ap = P_V A P_V p
+            copy(n_, cp, k, T2());
+            project(T2());
+            spmm(T2(), k, cap);
+            project(cap);
+            BKC(bk_coldot_d(n_, cp.p, cp.ld, cap.p, cap.ld, k, pap, WORK_.p(), st()));
+            BKC(bk_cg_step1_d(n_, k, rs, pap, act, cx.p, cx.ld, cr.p, cr.ld, cp.p, cp.ld, cap.p, cap.ld, st()));
+            BKC(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs_new, WORK_.p(), st()));
+            BKC(bk_cg_step2_d(n_, k, rs, rs_new, act, cr.p, cr.ld, cp.p, cp.ld, st()));
+        }
+        // y = V - delta
+        BKC(bk_lincomb_d(n_, k, 1.0, v.p, v.ld, -1.0, cx.p, cx.ld, T1().p, ldT_, st()));
+        Event ev = Event::none;
+        int ycols = n_now;
+        if (d == Decision::expand) {
+            const int e = cfg_.expand == ExpandMode::random ? n_ex - n_now : xd_cols_;
+            if (e > 0) {
+                if (cfg_.expand == ExpandMode::random) random_block(e, T1().at(n_now));
+                else copy(n_, xd, e, T1().at(n_now));
+                ycols += e;
+                xd_cols_ = 0;
+                n_now = n_ex;
+                ev = Event::expand;
+            }
+        }
+        meter_.ortho(n_, ycols);
+        const int kept = proj_ortho(n_, T1(), ycols, {nullptr, 0}, 0, S(cur_));
+        if (kept < n_now) fresh_cols(n_now - kept, S(cur_), kept);
+        rayleigh_ritz(S(cur_), n_now, 0);
+        lift(S(cur_), n_now, Z_.d(), ldH_, n_now, S(1 - cur_));
+        cur_ ^= 1;
+        if (d == Decision::shrink) {
+            copy(n_, S(cur_).at(n_es), n_now - n_es, xd);
+            xd_cols_ = n_now - n_es;
+            n_now = n_es;
+            ev = Event::shrink;
+        }
+        push(j, rep.overall, n_now, ev, 0);
+    }
+    finish(Status::max_iters, S(cur_), n_ev);
+}
+
+SolveOutput Engine::run(const double* x0, int x0_cols) {
+    x0_ = x0;
+    x0_cols_ = x0_cols;
+    switch (kind_) {
+        case SolverKind::si: solve_si(); break;
+        case SolverKind::sd: solve_sd(); break;
+        case SolverKind::lobpcg: solve_lobpcg(); break;
+        case SolverKind::tracemin: solve_tracemin(); break;
+    }
+    return std::move(out_);
+}
+
+}  // namespace
+
+// solvers.cpp:147-169 (+ extension checks)
+SolverConfig resolve_config(SolverConfig cfg, SolverKind kind, const StrategyConfig& s, int n) {
+    if (n < 1) throw std::invalid_argument("matrix is empty");
+    if (cfg.n_ev < 1) throw std::invalid_argument("n_ev must be positive");
+    if (cfg.n_ev > n) throw std::invalid_argument("n_ev exceeds the matrix dimension");
+    if (cfg.n_ex == 0) {
+        const double mult = kind == SolverKind::lobpcg ? 1.5 : 2.0;
+        cfg.n_ex = std::min(n, static_cast<int>(std::ceil(mult * cfg.n_ev)));
+    }
+    const bool nes_given = cfg.n_es != 0;
+    if (!nes_given) cfg.n_es = std::max(cfg.n_ev, std::min(cfg.n_ev + 5, cfg.n_ex - 1));
+    if (cfg.n_ex < cfg.n_ev || cfg.n_ex > n) throw std::invalid_argument("need n_ev <= n_ex <= n");
+    const bool se = s.kind != StrategyKind::none;
+    if ((se || nes_given) && !(cfg.n_ev <= cfg.n_es && cfg.n_es < cfg.n_ex))
+        throw std::invalid_argument("need n_ev <= n_es < n_ex");
+    if (!(cfg.tol > 0)) throw std::invalid_argument("tol must be positive");
+    if (cfg.max_iters < 1) throw std::invalid_argument("max_iters must be positive");
+    if (cfg.cg_iters < 1) throw std::invalid_argument("cg_iters must be positive");
+    if (cfg.expand == ExpandMode::powered && kind != SolverKind::si)
+        throw std::invalid_argument("powered expansion vectors require the SI solver");
+    if (cfg.op_shifted && kind != SolverKind::si)
+        throw std::invalid_argument("the shifted operator mode applies to the SI solver only");
+    validate_strategy(s);
+    return cfg;
+}
+
+SolveOutput solve(SolverKind kind, const SparseSym& a, const SolverConfig& cfg_in, const StrategyConfig& s,
+                  const double* x0, int x0_cols) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (a.is_complex()) throw std::invalid_argument("complex Hermitian solves are not available in this build");
+    const SolverConfig cfg = resolve_config(cfg_in, kind, s, a.rows());
+    Engine e(a, cfg, kind);
+    e.set_strategy(s);
+    SolveOutput out = e.run(x0, x0_cols);
+    out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return out;
+}
+
+}  // namespace b2

@@ -1,0 +1,198 @@
+// Host-side core of libblockeig_b200.so: matrix handle, strategy state
+// machine, device workspace and the four solver loops.  The loops restate the
+// reference's control flow (proj/src/solvers.cpp) over device-resident blocks;
+// every dense / sparse operation is a bk_* CUDA kernel (include/bk_kernels.h).
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/bk_kernels.h"
+
+namespace b2 {
+
+// ---------------------------------------------------------------- errors
+// Mapped by the C ABI exactly like the reference (proj/src/capi.cpp:24-49):
+// invalid_argument -> INVALID, runtime_error -> NUMERIC, ParseError -> PARSE,
+// IoError -> IO, anything else -> INTERNAL.  A CUDA failure is deliberately
+// NOT a runtime_error so that it surfaces as BEIG_ERR_INTERNAL.
+class ParseError : public std::runtime_error {
+public:
+    ParseError(const std::string& what, long line)
+        : std::runtime_error("line " + std::to_string(line) + ": " + what) {}
+};
+class IoError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class CudaError : public std::exception {
+public:
+    explicit CudaError(std::string m) : msg_(std::move(m)) {}
+    const char* what() const noexcept override { return msg_.c_str(); }
+
+private:
+    std::string msg_;
+};
+
+void cuda_check(int code, const char* what);  // throws CudaError when code != 0
+
+// ---------------------------------------------------------------- device memory
+class DevMem {
+public:
+    DevMem() = default;
+    explicit DevMem(size_t bytes) { alloc(bytes); }
+    ~DevMem();
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    DevMem(DevMem&& o) noexcept : p_(o.p_), bytes_(o.bytes_) { o.p_ = nullptr, o.bytes_ = 0; }
+    void alloc(size_t bytes);
+    template <class T> T* as() const { return static_cast<T*>(p_); }
+    void* p() const { return p_; }
+    double* d() const { return static_cast<double*>(p_); }
+    size_t bytes() const { return bytes_; }
+
+private:
+    void* p_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+// ---------------------------------------------------------------- matrix
+// Lower-triangle CSR with the reference invariants (proj/src/matio.cpp:17-35):
+// int64 row_ptr, int32 strictly increasing columns <= row.  Immutable after
+// construction; the norm estimate and the device copy (full CSR, int32) are
+// cached and shared between copies of the handle.
+struct DeviceCsr {
+    int device = -1;
+    int n = 0;
+    int64_t nnz_full = 0;
+    DevMem row_ptr, col, val;
+    bool negated = false;
+};
+
+class SparseSym {
+public:
+    SparseSym();
+    SparseSym(int n, std::vector<int64_t> rp, std::vector<int> col, std::vector<double> val,
+              bool complex_values = false);
+    int rows() const { return n_; }
+    int64_t nnz_lower() const { return static_cast<int64_t>(col_.size()); }
+    bool is_complex() const { return complex_; }
+    const std::vector<int64_t>& row_ptr() const { return rp_; }
+    const std::vector<int>& col() const { return col_; }
+    const std::vector<double>& val() const { return val_; }  // interleaved when complex
+    double diagonal(int i) const;                             // real part; 0 when absent
+    double norm_est() const;                                  // estimate_norm2, cached
+    // full (both triangles) CSR on `device`, optionally with negated values (M = -A)
+    const DeviceCsr& device_csr(int device, bool negate) const;
+
+private:
+    int n_;
+    bool complex_;
+    std::vector<int64_t> rp_;
+    std::vector<int> col_;
+    std::vector<double> val_;
+    std::shared_ptr<std::atomic<double>> norm_cache_;
+    struct DevCache {
+        std::mutex mu;
+        std::vector<std::unique_ptr<DeviceCsr>> entries;
+    };
+    std::shared_ptr<DevCache> dev_;
+};
+
+SparseSym gen_from_spec(const std::string& spec);
+SparseSym apply_spd_shift(const SparseSym& a, double lambda1);
+double spd_shift_value(double lambda1);
+SparseSym parse_matrix_market_file(const std::string& path);
+void write_matrix_market_file(const SparseSym& a, const std::string& path);
+
+// ---------------------------------------------------------------- strategy
+// proj/src/strategy.{hpp,cpp}: same knobs, same decisions.
+enum class StrategyKind { none = 0, fix = 1, slope = 2, slopek = 3 };
+enum class Decision { hold = 0, shrink = 1, expand = 2 };
+struct StrategyConfig {
+    StrategyKind kind = StrategyKind::none;
+    int j_e = 12, j_s = 2;
+    double mu = 1.1;
+    int j_p = 10, j_warm = 5;
+    double r_warm = 1e-4;
+};
+class BlockSizer {
+public:
+    explicit BlockSizer(const StrategyConfig& c) : c_(c) {}
+    Decision step(double r_now, int n_now, int n_es, int n_ex);
+    double c_max() const { return c_max_; }
+    // enter the post-warm-up state (reference tests' shrunken_state(), test_strategy.cpp:15-20)
+    void mark_warmed() { warmed_ = true; }
+
+private:
+    StrategyConfig c_;
+    int j_ = 0;
+    std::vector<double> lg_;
+    bool warmed_ = false;
+    int last_expand_ = -1;
+    bool have_ref_ = false;
+    double c_max_ = 0.0;
+};
+void validate_strategy(const StrategyConfig& c);
+
+// ---------------------------------------------------------------- solver
+enum class SolverKind { si = 0, sd = 1, lobpcg = 2, tracemin = 3 };
+enum class Precond { identity = 0, diagonal = 1 };
+enum class ExpandMode { x_drop = 0, powered = 1, random = 2 };
+enum class Status { converged = 0, max_iters = 1, stagnated = 2 };
+enum class Event { none = 0, shrink = 1, expand = 2, lock = 3 };
+
+struct SolverConfig {
+    int n_ev = 1, n_ex = 0, n_es = 0;
+    double tol = 1e-10;
+    int max_iters = 2000;
+    double shift = 0.0;
+    int cg_iters = 5;
+    Precond precond = Precond::identity;
+    ExpandMode expand = ExpandMode::x_drop;
+    uint64_t seed = 0;
+    // extensions (beig_solve_ex)
+    bool op_shifted = false;
+    double op_c = 0.0;
+    bool largest = false;
+    int device = 0;
+};
+
+struct Work {
+    int64_t spmv_cols = 0, solve_cols = 0, ortho_flops = 0;
+    int rr_dim = 0;
+};
+struct Record {
+    int iteration;
+    double r_overall;
+    int n_now;
+    Event event;
+    int lock_count;
+    Work work;
+};
+struct SolveOutput {
+    Status status = Status::max_iters;
+    std::vector<double> values;   // n_ev, ascending (descending for `largest`)
+    std::vector<double> vectors;  // n x n_ev column-major (interleaved when complex)
+    bool complex_vectors = false;
+    std::vector<Record> history;
+    int iterations = 0;
+    Work work;
+    int64_t rr_flops = 0;
+    double seconds = 0.0;
+    // device-side diagnostics (not part of the reference record)
+    int cgs2_fallbacks = 0;
+    int max_jacobi_sweeps = 0;
+};
+
+SolverConfig resolve_config(SolverConfig cfg, SolverKind kind, const StrategyConfig& s, int n);
+SolveOutput solve(SolverKind kind, const SparseSym& a, const SolverConfig& cfg,
+                  const StrategyConfig& s, const double* x0_colmajor, int x0_cols);
+
+}  // namespace b2

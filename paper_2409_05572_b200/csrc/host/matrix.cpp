@@ -1,0 +1,450 @@
+// Matrix handle: lower-CSR storage, generators, norm estimate, Matrix Market
+// ingest/export and the cached device copy (full CSR) used by the SpMM kernel.
+// Reference: proj/src/matio.{hpp,cpp}, proj/src/kernel.cpp:166-196.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+#include <unordered_map>
+
+#include "host.hpp"
+
+namespace b2 {
+
+void cuda_check(int code, const char* what) {
+    if (code != 0)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(static_cast<cudaError_t>(code)));
+}
+
+DevMem::~DevMem() {
+    if (p_) cudaFree(p_);
+}
+
+void DevMem::alloc(size_t bytes) {
+    if (p_) {
+        cudaFree(p_);
+        p_ = nullptr;
+        bytes_ = 0;
+    }
+    if (bytes == 0) return;
+    cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc");
+    bytes_ = bytes;
+}
+
+// ---------------------------------------------------------------- SparseSym
+
+SparseSym::SparseSym()
+    : n_(0), complex_(false), rp_(1, 0),
+      norm_cache_(std::make_shared<std::atomic<double>>(-1.0)), dev_(std::make_shared<DevCache>()) {}
+
+SparseSym::SparseSym(int n, std::vector<int64_t> rp, std::vector<int> col, std::vector<double> val,
+                     bool complex_values)
+    : n_(n), complex_(complex_values), rp_(std::move(rp)), col_(std::move(col)), val_(std::move(val)),
+      norm_cache_(std::make_shared<std::atomic<double>>(-1.0)), dev_(std::make_shared<DevCache>()) {
+    const size_t per = complex_ ? 2 : 1;
+    if (n_ < 0 || rp_.size() != static_cast<size_t>(n_) + 1 || val_.size() != per * col_.size() ||
+        rp_.front() != 0 || rp_.back() != static_cast<int64_t>(col_.size()))
+        throw std::invalid_argument("SparseSym: inconsistent CSR arrays");
+    for (int r = 0; r < n_; ++r) {
+        if (rp_[r + 1] < rp_[r]) throw std::invalid_argument("SparseSym: inconsistent CSR arrays");
+        int prev = -1;
+        for (int64_t p = rp_[r]; p < rp_[r + 1]; ++p) {
+            const int c = col_[p];
+            if (c < 0 || c > r || c <= prev)
+                throw std::invalid_argument("SparseSym: columns must be strictly increasing and <= row");
+            prev = c;
+            if (complex_ && c == r && val_[2 * p + 1] != 0.0)
+                throw std::invalid_argument("Hermitian matrix needs a real diagonal");
+        }
+    }
+    if (static_cast<int64_t>(col_.size()) * 2 >= (int64_t{1} << 31))
+        throw std::invalid_argument("matrix too large for int32 device indices");
+}
+
+double SparseSym::diagonal(int i) const {
+    for (int64_t p = rp_[i + 1] - 1; p >= rp_[i]; --p) {
+        if (col_[p] == i) return complex_ ? val_[2 * p] : val_[p];
+        if (col_[p] < i) break;
+    }
+    return 0.0;
+}
+
+namespace {
+
+// reference spmv (kernel.cpp:8-26): lower CSR, mirrored scatter, fixed order
+void host_spmv(const SparseSym& a, const std::vector<double>& x, std::vector<double>& y) {
+    const int n = a.rows();
+    const auto& rp = a.row_ptr();
+    const auto& col = a.col();
+    const auto& val = a.val();
+    y.assign(x.size(), 0.0);
+    if (!a.is_complex()) {
+        for (int r = 0; r < n; ++r) {
+            double acc = 0.0;
+            const double xr = x[r];
+            for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+                const int c = col[p];
+                const double v = val[p];
+                acc += v * x[c];
+                if (c != r) y[c] += v * xr;
+            }
+            y[r] += acc;
+        }
+        return;
+    }
+    for (int r = 0; r < n; ++r) {
+        double ar = 0.0, ai = 0.0;
+        const double xr = x[2 * r], xi = x[2 * r + 1];
+        for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+            const int c = col[p];
+            const double vr = val[2 * p], vi = val[2 * p + 1];
+            ar += vr * x[2 * c] - vi * x[2 * c + 1];
+            ai += vr * x[2 * c + 1] + vi * x[2 * c];
+            if (c != r) {  // conj(v) * x[r]
+                y[2 * c] += vr * xr + vi * xi;
+                y[2 * c + 1] += vr * xi - vi * xr;
+            }
+        }
+        y[2 * r] += ar;
+        y[2 * r + 1] += ai;
+    }
+}
+
+double host_nrm2(const std::vector<double>& v) {
+    double s = 0.0;
+    for (double x : v) s += x * x;
+    return std::sqrt(s);
+}
+
+}  // namespace
+
+// kernel.cpp:174-196 — computed once per handle on the host with the
+// reference's seeded start and loop order, shared by every solve on the
+// handle (and bit-identical to the CPU oracle's value).
+double SparseSym::norm_est() const {
+    const double cached = norm_cache_->load(std::memory_order_relaxed);
+    if (cached >= 0.0) return cached;
+    if (n_ == 0) return 0.0;
+    std::mt19937_64 rng(0x9e3779b97f4a7c15ULL);
+    std::normal_distribution<double> dist(0.0, 1.0);
+    std::vector<double> v(static_cast<size_t>(n_) * (complex_ ? 2 : 1));
+    for (auto& x : v) x = dist(rng);
+    double nrm = host_nrm2(v);
+    if (nrm == 0.0) return 0.0;
+    for (auto& x : v) x /= nrm;
+    std::vector<double> w, t;
+    for (int it = 0; it < 30; ++it) {
+        host_spmv(*this, v, t);
+        host_spmv(*this, t, w);
+        nrm = host_nrm2(w);
+        if (nrm == 0.0) {
+            norm_cache_->store(0.0, std::memory_order_relaxed);
+            return 0.0;
+        }
+        for (size_t i = 0; i < v.size(); ++i) v[i] = w[i] / nrm;
+    }
+    host_spmv(*this, v, t);
+    const double est = host_nrm2(t);
+    norm_cache_->store(est, std::memory_order_relaxed);
+    return est;
+}
+
+// Expand the lower triangle to full CSR (int32) and upload once per
+// (device, sign); the upper entries are the mirrored (conjugated) lower ones.
+const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
+    std::lock_guard<std::mutex> lk(dev_->mu);
+    for (auto& e : dev_->entries)
+        if (e->device == device && e->negated == negate) return *e;
+    const int per = complex_ ? 2 : 1;
+    std::vector<int32_t> cnt(static_cast<size_t>(n_) + 1, 0);
+    for (int r = 0; r < n_; ++r)
+        for (int64_t p = rp_[r]; p < rp_[r + 1]; ++p) {
+            cnt[r + 1]++;
+            if (col_[p] != r) cnt[col_[p] + 1]++;
+        }
+    for (int r = 0; r < n_; ++r) cnt[r + 1] += cnt[r];
+    const int64_t nnz = cnt[n_];
+    std::vector<int32_t> frp(cnt), fcol(static_cast<size_t>(nnz));
+    std::vector<double> fval(static_cast<size_t>(nnz) * per);
+    std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+    const double sgn = negate ? -1.0 : 1.0;
+    // rows in order: upper-part entries (c > r) come from later rows' lower
+    // entries, so fill by scanning rows and appending both mirror images;
+    // columns end up sorted because both scans are in increasing order.
+    std::vector<std::vector<std::pair<int, int64_t>>> upper(static_cast<size_t>(n_));
+    for (int r = 0; r < n_; ++r)
+        for (int64_t p = rp_[r]; p < rp_[r + 1]; ++p)
+            if (col_[p] != r) upper[col_[p]].push_back({r, p});
+    for (int r = 0; r < n_; ++r) {
+        int32_t q = pos[r];
+        for (int64_t p = rp_[r]; p < rp_[r + 1]; ++p) {
+            fcol[q] = col_[p];
+            for (int t = 0; t < per; ++t) fval[static_cast<size_t>(q) * per + t] = sgn * val_[p * per + t];
+            ++q;
+        }
+        for (const auto& [c, p] : upper[r]) {  // entry (r, c) = conj(A(c, r)), c > r
+            fcol[q] = c;
+            fval[static_cast<size_t>(q) * per] = sgn * val_[p * per];
+            if (complex_) fval[static_cast<size_t>(q) * per + 1] = -sgn * val_[p * per + 1];
+            ++q;
+        }
+    }
+    auto e = std::make_unique<DeviceCsr>();
+    e->device = device;
+    e->n = n_;
+    e->nnz_full = nnz;
+    e->negated = negate;
+    int prev = 0;
+    cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    e->row_ptr.alloc(sizeof(int32_t) * frp.size());
+    e->col.alloc(sizeof(int32_t) * std::max<size_t>(fcol.size(), 1));
+    e->val.alloc(sizeof(double) * std::max<size_t>(fval.size(), 1));
+    cuda_check(cudaMemcpy(e->row_ptr.as<void>(), frp.data(), sizeof(int32_t) * frp.size(), cudaMemcpyHostToDevice), "upload");
+    if (nnz) {
+        cuda_check(cudaMemcpy(e->col.as<void>(), fcol.data(), sizeof(int32_t) * fcol.size(), cudaMemcpyHostToDevice), "upload");
+        cuda_check(cudaMemcpy(e->val.as<void>(), fval.data(), sizeof(double) * fval.size(), cudaMemcpyHostToDevice), "upload");
+    }
+    cudaSetDevice(prev);
+    dev_->entries.push_back(std::move(e));
+    return *dev_->entries.back();
+}
+
+// ---------------------------------------------------------------- generators
+
+namespace {
+struct Entry {
+    int r, c;
+    double v;
+};
+SparseSym from_entries(int n, std::vector<Entry>& es) {
+    std::sort(es.begin(), es.end(), [](const Entry& a, const Entry& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
+    std::vector<int64_t> rp(static_cast<size_t>(n) + 1, 0);
+    std::vector<int> col(es.size());
+    std::vector<double> val(es.size());
+    for (size_t i = 0; i < es.size(); ++i) {
+        rp[es[i].r + 1]++;
+        col[i] = es[i].c;
+        val[i] = es[i].v;
+    }
+    for (int r = 0; r < n; ++r) rp[r + 1] += rp[r];
+    return SparseSym(n, std::move(rp), std::move(col), std::move(val));
+}
+
+std::vector<std::string> split_commas(const std::string& s) {
+    std::vector<std::string> out(1);
+    for (char ch : s) {
+        if (ch == ',') out.emplace_back();
+        else out.back() += ch;
+    }
+    return out;
+}
+
+int to_int(const std::string& s) {
+    size_t pos = 0;
+    const int v = std::stoi(s, &pos);
+    if (pos != s.size()) throw std::invalid_argument("bad integer '" + s + "' in spec");
+    return v;
+}
+double to_double(const std::string& s) {
+    size_t pos = 0;
+    const double v = std::stod(s, &pos);
+    if (pos != s.size()) throw std::invalid_argument("bad number '" + s + "' in spec");
+    return v;
+}
+
+SparseSym diag_from(const std::vector<double>& v) {
+    const int n = static_cast<int>(v.size());
+    std::vector<int64_t> rp(static_cast<size_t>(n) + 1);
+    std::vector<int> col(static_cast<size_t>(n));
+    for (int i = 0; i <= n; ++i) rp[i] = i;
+    for (int i = 0; i < n; ++i) col[i] = i;
+    return SparseSym(n, std::move(rp), std::move(col), v);
+}
+}  // namespace
+
+// matio.cpp:246-290: "laplacian1d:N", "diag:v1,...", "diag-geom:N,RATIO"
+SparseSym gen_from_spec(const std::string& spec) {
+    const size_t colon = spec.find(':');
+    if (colon == std::string::npos)
+        throw std::invalid_argument("generator spec needs 'name:args', got '" + spec + "'");
+    const std::string name = spec.substr(0, colon), args = spec.substr(colon + 1);
+    if (name == "laplacian1d") {
+        const int n = to_int(args);
+        if (n < 1) throw std::invalid_argument("gen_laplacian_1d: n must be positive");
+        std::vector<Entry> es;
+        for (int i = 0; i < n; ++i) {
+            if (i > 0) es.push_back({i, i - 1, -1.0});
+            es.push_back({i, i, 2.0});
+        }
+        return from_entries(n, es);
+    }
+    if (name == "diag") {
+        std::vector<double> v;
+        for (const auto& t : split_commas(args)) v.push_back(to_double(t));
+        return diag_from(v);
+    }
+    if (name == "diag-geom") {
+        const auto parts = split_commas(args);
+        if (parts.size() != 2) throw std::invalid_argument("diag-geom needs 'diag-geom:n,ratio'");
+        const int n = to_int(parts[0]);
+        const double ratio = to_double(parts[1]);
+        if (n < 1) throw std::invalid_argument("gen_diag_geometric: n must be positive");
+        if (!(ratio > 0)) throw std::invalid_argument("gen_diag_geometric: ratio must be positive");
+        std::vector<double> v(static_cast<size_t>(n));
+        double x = 1.0;
+        for (int i = 0; i < n; ++i, x *= ratio) v[i] = x;
+        return diag_from(v);
+    }
+    throw std::invalid_argument("unknown generator '" + name + "'");
+}
+
+double spd_shift_value(double lambda1) { return lambda1 <= 0.0 ? 1.05 * lambda1 : 0.0; }
+
+SparseSym apply_spd_shift(const SparseSym& a, double lambda1) {
+    if (a.is_complex()) throw std::invalid_argument("spd_shift: real matrices only");
+    const double shift = spd_shift_value(lambda1);
+    if (shift == 0.0) return a;
+    std::vector<Entry> es;
+    for (int r = 0; r < a.rows(); ++r) {
+        bool has = false;
+        for (int64_t p = a.row_ptr()[r]; p < a.row_ptr()[r + 1]; ++p) {
+            double v = a.val()[p];
+            if (a.col()[p] == r) {
+                v -= shift;
+                has = true;
+            }
+            es.push_back({r, a.col()[p], v});
+        }
+        if (!has) es.push_back({r, r, -shift});
+    }
+    return from_entries(a.rows(), es);
+}
+
+// ---------------------------------------------------------------- Matrix Market
+// Same acceptance rules as proj/src/matio.cpp:89-184: 'matrix coordinate',
+// real|integer, symmetric (lower triangle) | general (numerically symmetric
+// within 1e-12 relative); ParseError carries the offending line.
+
+namespace {
+std::string lowered(std::string s) {
+    for (char& c : s) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    return s;
+}
+bool content_line(std::istream& in, std::string& line, long& no) {
+    while (std::getline(in, line)) {
+        ++no;
+        const size_t i = line.find_first_not_of(" \t\r\n");
+        if (i == std::string::npos || line[i] == '%') continue;
+        return true;
+    }
+    return false;
+}
+}  // namespace
+
+SparseSym parse_matrix_market_file(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw IoError("cannot open '" + path + "'");
+    std::string line;
+    long no = 0;
+    if (!std::getline(in, line)) throw ParseError("empty input", 1);
+    ++no;
+    std::istringstream hs(line);
+    std::string banner, object, format, field, sym;
+    hs >> banner >> object >> format >> field >> sym;
+    if (banner != "%%MatrixMarket") throw ParseError("missing %%MatrixMarket banner", no);
+    if (lowered(object) != "matrix" || lowered(format) != "coordinate")
+        throw ParseError("only 'matrix coordinate' inputs are supported", no);
+    field = lowered(field);
+    sym = lowered(sym);
+    if (field != "real" && field != "integer") throw ParseError("unsupported field '" + field + "'", no);
+    if (sym != "symmetric" && sym != "general") throw ParseError("unsupported symmetry '" + sym + "'", no);
+    const bool general = sym == "general";
+    if (!content_line(in, line, no)) throw ParseError("missing size line", no + 1);
+    long rows = 0, cols = 0, nnz = 0;
+    {
+        std::istringstream ss(line);
+        std::string rest;
+        if (!(ss >> rows >> cols >> nnz)) throw ParseError("malformed size line", no);
+        if (ss >> rest) throw ParseError("trailing tokens on size line", no);
+    }
+    if (rows != cols) throw ParseError("matrix is not square", no);
+    if (rows < 0 || nnz < 0) throw ParseError("negative dimensions", no);
+    struct Pair {
+        double lo = 0, up = 0;
+        bool has_lo = false, has_up = false;
+        long ln_lo = 0, ln_up = 0;
+    };
+    std::unordered_map<int64_t, Pair> slots;
+    std::vector<int64_t> order;
+    for (long e = 0; e < nnz; ++e) {
+        if (!content_line(in, line, no))
+            throw ParseError("unexpected end of input, expected " + std::to_string(nnz) + " entries, got " +
+                                 std::to_string(e),
+                             no + 1);
+        std::istringstream ss(line);
+        long i, j;
+        double v;
+        std::string rest;
+        if (!(ss >> i >> j >> v)) throw ParseError("malformed entry (need 'i j value')", no);
+        if (ss >> rest) throw ParseError("trailing tokens on entry line", no);
+        if (i < 1 || i > rows || j < 1 || j > cols) throw ParseError("index out of range", no);
+        if (!std::isfinite(v)) throw ParseError("non-finite value", no);
+        const bool low = i >= j;
+        if (!general && !low) throw ParseError("symmetric input must store the lower triangle", no);
+        const int64_t r = (low ? i : j) - 1, c = (low ? j : i) - 1;
+        const int64_t key = r * rows + c;
+        auto it = slots.find(key);
+        if (it == slots.end()) {
+            it = slots.emplace(key, Pair{}).first;
+            order.push_back(key);
+        }
+        Pair& s = it->second;
+        if (low) {
+            if (s.has_lo) throw ParseError("duplicate entry", no);
+            s.lo = v, s.has_lo = true, s.ln_lo = no;
+        } else {
+            if (s.has_up) throw ParseError("duplicate entry", no);
+            s.up = v, s.has_up = true, s.ln_up = no;
+        }
+    }
+    std::sort(order.begin(), order.end());
+    std::vector<Entry> es;
+    es.reserve(order.size());
+    for (int64_t key : order) {
+        const Pair& s = slots[key];
+        const int r = static_cast<int>(key / rows), c = static_cast<int>(key % rows);
+        if (r != c && general) {
+            const std::string where = "(" + std::to_string(r + 1) + "," + std::to_string(c + 1) + ")";
+            if (!s.has_lo || !s.has_up)
+                throw ParseError("general input is not symmetric: entry " + where + " lacks its mirror",
+                                 s.has_lo ? s.ln_lo : s.ln_up);
+            const double scale = std::max({std::fabs(s.lo), std::fabs(s.up), 1e-300});
+            if (std::fabs(s.lo - s.up) > 1e-12 * scale)
+                throw ParseError("general input is not symmetric: entry " + where + " mismatches its mirror", s.ln_up);
+        }
+        es.push_back({r, c, s.lo});
+    }
+    return from_entries(static_cast<int>(rows), es);
+}
+
+void write_matrix_market_file(const SparseSym& a, const std::string& path) {
+    if (a.is_complex()) throw std::invalid_argument("Matrix Market export: real matrices only");
+    std::ofstream out(path);
+    if (!out) throw IoError("cannot open '" + path + "' for writing");
+    out << "%%MatrixMarket matrix coordinate real symmetric\n";
+    out << a.rows() << " " << a.rows() << " " << a.nnz_lower() << "\n";
+    char buf[80];
+    for (int r = 0; r < a.rows(); ++r)
+        for (int64_t p = a.row_ptr()[r]; p < a.row_ptr()[r + 1]; ++p) {
+            std::snprintf(buf, sizeof buf, "%d %d %.17g\n", r + 1, a.col()[p] + 1, a.val()[p]);
+            out << buf;
+        }
+    if (!out.flush()) throw IoError("write failed for '" + path + "'");
+}
+
+}  // namespace b2
