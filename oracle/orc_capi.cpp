@@ -184,6 +184,7 @@ void beig_solve_ext_default(beig_solve_ext* ext) {
     ext->op_shift = 0.0;
     ext->which = BEIG_WHICH_SMALLEST;
     ext->device = 0;
+    ext->profile = 0;
 }
 
 int beig_solve_ex(beig_result** out, const beig_matrix* a, int solver, const beig_solver_config* cfg,
@@ -373,6 +374,21 @@ int beig_zmatrix_from_csr(beig_matrix** out, int n, const int64_t* row_ptr, cons
 }
 
 int beig_matrix_is_complex(const beig_matrix* a) { return a && a->is_complex ? 1 : 0; }
+
+// CPU oracle: no device kernels, so no per-kernel statistics
+int beig_result_kernel_stats(const beig_result* r, int kernel, beig_kernel_stat* out) {
+    if (!r || !out) return invalid("beig_result_kernel_stats: null argument");
+    if (kernel < 0 || kernel >= BEIG_KERNEL_CLASSES) return invalid("beig_result_kernel_stats: unknown kernel class");
+    *out = beig_kernel_stat{0, 0.0, 0.0, 0.0};
+    return BEIG_OK;
+}
+
+int beig_result_diagnostics(const beig_result* r, int* cgs2_fallbacks, int* max_jacobi_sweeps) {
+    if (!r) return invalid("beig_result_diagnostics: null argument");
+    if (cgs2_fallbacks) *cgs2_fallbacks = 0;
+    if (max_jacobi_sweeps) *max_jacobi_sweeps = 0;
+    return BEIG_OK;
+}
 
 // ---- analysis checks: outside the hot path; not restated by the oracle ----
 int beig_theory_example3x3(beig_example3x3* out) {

@@ -45,7 +45,7 @@ class StrategyConfig(C.Structure):
 
 class SolveExt(C.Structure):
     _fields_ = [("op_mode", C.c_int), ("op_shift", C.c_double), ("which", C.c_int),
-                ("device", C.c_int)]
+                ("device", C.c_int), ("profile", C.c_int)]
 
 
 class IterRecord(C.Structure):
@@ -57,6 +57,14 @@ class IterRecord(C.Structure):
 class WorkSummary(C.Structure):
     _fields_ = [("spmv_cols", C.c_int64), ("solve_cols", C.c_int64), ("ortho_flops", C.c_int64),
                 ("rr_flops", C.c_int64), ("combined", C.c_double)]
+
+
+class KernelStat(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("ms", C.c_double), ("bytes", C.c_double),
+                ("flops", C.c_double)]
+
+
+KERNEL_CLASSES = ["spmm", "gram", "gemm", "syev", "chol", "residual", "other"]
 
 
 class Example3x3(C.Structure):
@@ -123,10 +131,13 @@ SYMBOLS = {
                                 C.POINTER(StrategyConfig), _DP, C.c_int, C.POINTER(SolveExt)]),
     "beig_result_vectors_z": (C.c_int64, [_P, _DP, C.c_int64]),
     "beig_result_seconds": (C.c_double, [_P]),
+    "beig_result_kernel_stats": (C.c_int, [_P, C.c_int, C.POINTER(KernelStat)]),
+    "beig_result_diagnostics": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
 }
 REFERENCE_SYMBOLS = [s for s in SYMBOLS if s not in (
     "beig_matrix_from_csr", "beig_zmatrix_from_csr", "beig_matrix_is_complex",
-    "beig_solve_ext_default", "beig_solve_ex", "beig_result_vectors_z", "beig_result_seconds")]
+    "beig_solve_ext_default", "beig_solve_ex", "beig_result_vectors_z", "beig_result_seconds",
+    "beig_result_kernel_stats", "beig_result_diagnostics")]
 
 
 class BlockeigError(RuntimeError):
@@ -345,6 +356,20 @@ class Result:
         arr = (IterRecord * max(ln, 1))()
         got = self.L.lib.beig_result_history(self.h, arr, ln)
         return [{f: getattr(arr[i], f) for f, _ in IterRecord._fields_} for i in range(got)]
+
+    def kernel_stats(self) -> dict:
+        out = {}
+        for i, name in enumerate(KERNEL_CLASSES):
+            k = KernelStat()
+            self.L.check(self.L.lib.beig_result_kernel_stats(self.h, i, C.byref(k)))
+            out[name] = {"launches": k.launches, "ms": k.ms, "bytes": k.bytes, "flops": k.flops}
+        return out
+
+    @property
+    def diagnostics(self) -> dict:
+        fb, sw = C.c_int(), C.c_int()
+        self.L.check(self.L.lib.beig_result_diagnostics(self.h, C.byref(fb), C.byref(sw)))
+        return {"cgs2_fallbacks": fb.value, "max_jacobi_sweeps": sw.value}
 
     @property
     def work(self) -> Work:

@@ -138,6 +138,11 @@ public:
             cudaStreamSynchronize(stream_);
             cudaStreamDestroy(stream_);
         }
+        for (auto& p : pending_) {
+            cudaEventDestroy(p.a);
+            cudaEventDestroy(p.b);
+        }
+        for (auto e : ev_pool_) cudaEventDestroy(e);
     }
 
     SolveOutput run(const double* x0, int x0_cols);
@@ -152,12 +157,77 @@ private:
     Blk T1() const { return {T1_.d(), ldT_}; }
     Blk T2() const { return {T2_.d(), ldT_}; }
 
-    void sync() { BKC(cudaStreamSynchronize(stream_)); }
+    void sync() {
+        BKC(cudaStreamSynchronize(stream_));
+        prof_resolve();
+    }
 
+    // ---- optional per-kernel-class CUDA-event timing (ext->profile)
+    struct Pending {
+        int cls;
+        cudaEvent_t a, b;
+        double bytes, flops;
+    };
+    std::vector<cudaEvent_t> ev_pool_;
+    std::vector<Pending> pending_;
+    KernelStat kstats_[K_CLASSES];
+    cudaEvent_t take_event() {
+        if (!ev_pool_.empty()) {
+            cudaEvent_t e = ev_pool_.back();
+            ev_pool_.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        BKC(cudaEventCreate(&e));
+        return e;
+    }
+    cudaEvent_t prof_begin() {
+        if (!cfg_.profile) return nullptr;
+        cudaEvent_t e = take_event();
+        BKC(cudaEventRecord(e, stream_));
+        return e;
+    }
+    void prof_end(cudaEvent_t a, int cls, double bytes, double flops) {
+        if (!a) return;
+        cudaEvent_t b = take_event();
+        BKC(cudaEventRecord(b, stream_));
+        pending_.push_back({cls, a, b, bytes, flops});
+    }
+    void prof_resolve() {
+        for (auto& p : pending_) {
+            float ms = 0.f;
+            BKC(cudaEventElapsedTime(&ms, p.a, p.b));
+            auto& k = kstats_[p.cls];
+            k.launches += 1;
+            k.ms += ms;
+            k.bytes += p.bytes;
+            k.flops += p.flops;
+            ev_pool_.push_back(p.a);
+            ev_pool_.push_back(p.b);
+        }
+        pending_.clear();
+    }
+
+    // K1: algorithmic bytes nnz*12 + (n+1)*4 + 2*n*k*8
     void spmm(Blk x, int k, Blk y) {
         if (k <= 0) return;
+        auto t = prof_begin();
         BKC(bk_spmm_d(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
                       y.ld, st()));
+        prof_end(t, K_SPMM, 12.0 * csr_->nnz_full + 4.0 * (n_ + 1) + 16.0 * n_ * k, 2.0 * csr_->nnz_full * k);
+    }
+    // K2: flops 2*rows*a*b; bytes 8*rows*(a+b)
+    void gram(int rows, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc) {
+        auto t = prof_begin();
+        BKC(bk_gram_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), st()));
+        prof_end(t, K_GRAM, 8.0 * rows * (a + b), 2.0 * rows * a * b);
+    }
+    // K3: flops 2*rows*d*k; bytes 8*rows*(d + k (+k when beta != 0))
+    void gemm(int rows, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
+              double* y, int ldy) {
+        auto t = prof_begin();
+        BKC(bk_gemm_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, st()));
+        prof_end(t, K_GEMM, 8.0 * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * rows * d * k);
     }
     void copy(int rows, Blk src, int k, Blk dst) {
         if (k > 0 && rows > 0) BKC(bk_copy_cols_d(rows, src.p, src.ld, k, dst.p, dst.ld, st()));
@@ -190,12 +260,14 @@ private:
         BKC(bk_colnorm2_d(rows, w.p, w.ld, a, ref2, WORK_.p(), st()));
         if (m > 0)
             for (int pass = 0; pass < 2; ++pass) {
-                BKC(bk_gram_d(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a, WORK_.p(), st()));
-                BKC(bk_gemm_d(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld, st()));
+                gram(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a);
+                gemm(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld);
             }
-        BKC(bk_gram_d(rows, w.p, w.ld, a, w.p, w.ld, a, GB_.d(), a, WORK_.p(), st()));
+        gram(rows, w.p, w.ld, a, w.p, w.ld, a, GB_.d(), a);
         int* info = INFO_.as<int>();
+        auto tc = prof_begin();
         BKC(bk_chol_drop_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
+        prof_end(tc, K_CHOL, 8.0 * a * a, a * a * a / 3.0);
         BKC(cudaMemcpyAsync(pin_.info, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         sync();
         if (debug_) debug_pivots(a, ref2);
@@ -204,12 +276,14 @@ private:
         const int kept = pin_.info[0];
         if (kept == 0) return 0;
         Blk pt{PT_.d(), ldT_};
-        BKC(bk_gemm_d(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld, st()));
+        gemm(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld);
         // second CholQR pass (no dropping: every pivot is ~1 after pass one)
-        BKC(bk_gram_d(rows, pt.p, pt.ld, kept, pt.p, pt.ld, kept, GB_.d(), kept, WORK_.p(), st()));
+        gram(rows, pt.p, pt.ld, kept, pt.p, pt.ld, kept, GB_.d(), kept);
+        auto tc2 = prof_begin();
         BKC(bk_chol_drop_d(kept, GB_.d(), kept, nullptr, 0.0, M2_.d(), kept, info, WORK_.p(), st()));
+        prof_end(tc2, K_CHOL, 8.0 * kept * kept, kept * kept * kept / 3.0);
         BKC(cudaMemcpyAsync(pin_.info, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
-        BKC(bk_gemm_d(rows, pt.p, pt.ld, kept, M2_.d(), kept, kept, 1.0, 0.0, out.p, out.ld, st()));
+        gemm(rows, pt.p, pt.ld, kept, M2_.d(), kept, kept, 1.0, 0.0, out.p, out.ld);
         sync();
         if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
         if (pin_.info[1] || pin_.info[0] != kept) return cgs2_fallback(rows, w, a, q, m, out);
@@ -257,12 +331,12 @@ private:
             copy(rows, w.at(j), 1, v);
             for (int pass = 0; pass < 2; ++pass) {
                 if (m > 0) {
-                    BKC(bk_gram_d(rows, q.p, q.ld, m, v.p, 1, 1, c, 1, WORK_.p(), st()));
-                    BKC(bk_gemm_d(rows, q.p, q.ld, m, c, 1, 1, -1.0, 1.0, v.p, 1, st()));
+                    gram(rows, q.p, q.ld, m, v.p, 1, 1, c, 1);
+                    gemm(rows, q.p, q.ld, m, c, 1, 1, -1.0, 1.0, v.p, 1);
                 }
                 if (kept > 0) {
-                    BKC(bk_gram_d(rows, out.p, out.ld, kept, v.p, 1, 1, c, 1, WORK_.p(), st()));
-                    BKC(bk_gemm_d(rows, out.p, out.ld, kept, c, 1, 1, -1.0, 1.0, v.p, 1, st()));
+                    gram(rows, out.p, out.ld, kept, v.p, 1, 1, c, 1);
+                    gemm(rows, out.p, out.ld, kept, c, 1, 1, -1.0, 1.0, v.p, 1);
                 }
             }
             BKC(bk_colnorm2_d(rows, v.p, 1, 1, nrm2, WORK_.p(), st()));
@@ -298,9 +372,11 @@ private:
     void rayleigh_ritz(Blk s, int d, int as_from) {
         meter_.rr(n_, d);
         spmm(s.at(as_from), d - as_from, AS().at(as_from));
-        BKC(bk_gram_d(n_, s.p, s.ld, d, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
+        gram(n_, s.p, s.ld, d, AS_.d(), ldS_, d, H_.d(), ldH_);
         int* info = INFO_.as<int>() + 8;
+        auto ts = prof_begin();
         BKC(bk_syev_d(d, H_.d(), ldH_, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
+        prof_end(ts, K_SYEV, 16.0 * d * d, 0.0);
         BKC(cudaMemcpyAsync(pin_.info + 8, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         syev_pending_ = true;
     }
@@ -313,7 +389,7 @@ private:
 
     // out[:, 0:k] = s[:, 0:d] Z[:, 0:k]
     void lift(Blk s, int d, const double* z, int ldz, int k, Blk out) {
-        BKC(bk_gemm_d(n_, s.p, s.ld, d, z, ldz, k, 1.0, 0.0, out.p, out.ld, st()));
+        gemm(n_, s.p, s.ld, d, z, ldz, k, 1.0, 0.0, out.p, out.ld);
     }
 
     struct Rep {
@@ -328,10 +404,12 @@ private:
         spmm(v, k, AS());
         double* rn2 = SMALL_.d();
         double* vn2 = SMALL_.d() + dcap_ + tcap_;
+        auto tr = prof_begin();
         BKC(bk_residual_d(n_, v.p, v.ld, AS_.d(), ldS_, VALS_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0, rn2,
                           vn2, WORK_.p(), st()));
         double* rec = SMALL_.d() + 2 * (dcap_ + tcap_);
         BKC(bk_convergence_d(k, rn2, vn2, VALS_.d(), norm_a_, n_ev, cfg_.tol, nullptr, rec, st()));
+        prof_end(tr, K_RESID, 24.0 * n_ * k, 6.0 * n_ * k);
         BKC(cudaMemcpyAsync(pin_.rec, rec, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         sync();
         check_syev();
@@ -352,8 +430,8 @@ private:
             return;
         }
         // (A - zeta I)^{-1} = M M^T with M = R^{-1} from the dense Cholesky
-        BKC(bk_gram_d(n_, INV_.d(), n_, n_, x.p, x.ld, k, PT_.d(), ldT_, WORK_.p(), st()));
-        BKC(bk_gemm_d(n_, INV_.d(), n_, n_, PT_.d(), ldT_, k, 1.0, 0.0, y.p, y.ld, st()));
+        gram(n_, INV_.d(), n_, n_, x.p, x.ld, k, PT_.d(), ldT_);
+        gemm(n_, INV_.d(), n_, n_, PT_.d(), ldT_, k, 1.0, 0.0, y.p, y.ld);
     }
     void factor_shift_invert();
 
@@ -381,6 +459,7 @@ private:
         out_.rr_flops = meter_.rr_flops;
         out_.cgs2_fallbacks = fallbacks_;
         out_.max_jacobi_sweeps = max_sweeps_;
+        for (int c = 0; c < K_CLASSES; ++c) out_.kstats[c] = kstats_[c];
     }
 
     int initial_block(const double* x0, int x0_cols, Blk dst);
@@ -728,8 +807,8 @@ void Engine::solve_tracemin() {
         const int k = n_now;
         // project(u) = u - V (V^T u), in place
         auto project = [&](Blk u) {
-            BKC(bk_gram_d(n_, v.p, v.ld, k, u.p, u.ld, k, COEF_.d(), k, WORK_.p(), st()));
-            BKC(bk_gemm_d(n_, v.p, v.ld, k, COEF_.d(), k, k, -1.0, 1.0, u.p, u.ld, st()));
+            gram(n_, v.p, v.ld, k, u.p, u.ld, k, COEF_.d(), k);
+            gemm(n_, v.p, v.ld, k, COEF_.d(), k, k, -1.0, 1.0, u.p, u.ld);
         };
         // rhs = P_V R; x = 0; p = r = rhs
         copy(n_, {R_.d(), ldT_}, k, cr);

@@ -162,6 +162,13 @@ struct SolverConfig {
     double op_c = 0.0;
     bool largest = false;
     int device = 0;
+    bool profile = false;
+};
+
+enum KernelClass { K_SPMM = 0, K_GRAM, K_GEMM, K_SYEV, K_CHOL, K_RESID, K_OTHER, K_CLASSES };
+struct KernelStat {
+    int64_t launches = 0;
+    double ms = 0.0, bytes = 0.0, flops = 0.0;
 };
 
 struct Work {
@@ -189,6 +196,7 @@ struct SolveOutput {
     // device-side diagnostics (not part of the reference record)
     int cgs2_fallbacks = 0;
     int max_jacobi_sweeps = 0;
+    KernelStat kstats[K_CLASSES];
 };
 
 SolverConfig resolve_config(SolverConfig cfg, SolverKind kind, const StrategyConfig& s, int n);
