@@ -93,13 +93,22 @@ BK_API int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref2, d
                           double* m, int ldm, int* info, void* work, void* stream);
 
 /* ---- K5 symmetric eigensolver (replaces sym_eig_small, proj/src/kernel.cpp:95-100) ----
- * Eigendecomposition of 0.5(H + H^T) (d x d row-major, ldh; destroyed) by
- * parallel cyclic Jacobi.  values ascending (stable among ties), z (ldz)
- * row-major with eigenvector j in column j.  info[0] = sweeps used,
- * info[1] = 1 if not converged. */
+ * Eigendecomposition of 0.5(H + H^T) (d x d row-major, ldh): values ascending
+ * (the n_need smallest; n_need <= 0 means all), z (ldz) row-major with
+ * eigenvector j in column j.  info[0] = Jacobi sweeps used (0 for the
+ * tridiagonal path), info[1] = 1 if not converged.  d <= 2048.
+ * bk_syev_d dispatches: d <= 48 one-CTA cyclic Jacobi (bk_syev_jacobi_d, H is
+ * destroyed), else Householder tridiagonalisation + multisection bisection +
+ * inverse iteration + CholQR2 + back-transformation (bk_syev_tri_d, H kept). */
 BK_API size_t bk_syev_work_bytes(int d);
-BK_API int bk_syev_d(int d, double* h, int ldh, double* values, double* z, int ldz, void* work,
-                     int* info, void* stream);
+BK_API int bk_syev_d(int d, double* h, int ldh, int n_need, double* values, double* z, int ldz,
+                     void* work, int* info, void* stream);
+BK_API size_t bk_syev_jacobi_work_bytes(int d);
+BK_API int bk_syev_jacobi_d(int d, double* h, int ldh, double* values, double* z, int ldz,
+                            void* work, int* info, void* stream);
+BK_API size_t bk_syev_tri_work_bytes(int d);
+BK_API int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double* values, double* z,
+                         int ldz, void* work, int* info, void* stream);
 
 /* ---- K7 column movement / elementwise ---- */
 /* dst[:, 0:k] = src[:, 0:k] (row-major; src and dst may overlap in the same rows) */

@@ -305,12 +305,12 @@ extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref
     BK_LAUNCHED();
 }
 
-extern "C" size_t bk_syev_work_bytes(int d) {
+extern "C" size_t bk_syev_jacobi_work_bytes(int d) {
     const size_t dd = static_cast<size_t>(d > 0 ? d : 1);
     return 2 * dd * dd * sizeof(double);
 }
 
-extern "C" int bk_syev_d(int d, double* h, int ldh, double* values, double* z, int ldz, void* work,
+extern "C" int bk_syev_jacobi_d(int d, double* h, int ldh, double* values, double* z, int ldz, void* work,
                          int* info, void* stream) {
     if (d <= 0) return 0;
     if (d > kMaxPairs * 2) return static_cast<int>(cudaErrorInvalidValue);

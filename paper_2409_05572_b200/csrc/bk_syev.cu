@@ -1,0 +1,477 @@
+// K5 — symmetric eigensolver for the projected (Rayleigh-Ritz) problem, on device.
+//
+// Replaces sym_eig_small (proj/src/kernel.cpp:95-100: Eigen's
+// SelfAdjointEigenSolver = Householder tridiagonalisation + implicit QR) with the
+// same first stage and a parallel second stage:
+//   1. tridiag_kernel   Householder reduction of 0.5(H + H^T) to tridiagonal
+//                       T = Q^T H Q (one CTA; trailing block in shared memory
+//                       once it fits, L2 before).
+//   2. bisect_kernel    the wanted eigenvalues of T by Sturm-count multisection,
+//                       one warp per eigenvalue (32 probe points per round).
+//   3. group_kernel +   eigenvectors of T by inverse iteration, one warp per
+//      invit_kernel     group of (near-)degenerate eigenvalues (relative gap
+//                       < 1e-7 ||T||): members are orthogonalised against the
+//                       group (modified Gram-Schmidt) every step, so exact
+//                       multiplets come out orthonormal.
+//   4. CholQR2 of U     (K2 Gram + K4 Cholesky + K3 update): vectors of distinct
+//                       eigenvalues are orthogonal to O(eps ||T|| / gap); the
+//                       re-orthonormalisation mixes them by the same amount,
+//                       which moves residuals by only O(eps ||T||).
+//   5. backtr_kernel    Z = Q U, one warp per eigenvector applying the stored
+//                       reflectors.
+// Why not Jacobi for d > 64: a cyclic Jacobi sweep is d-1 dependent rounds and
+// ~10 sweeps are needed, so it is latency-bound (96 ms at d = 288 on one CTA,
+// profiles/r01_bench_first.log); this path has O(d) dependent steps in total.
+#include <cfloat>
+
+#include "bk_common.cuh"
+
+namespace bk {
+namespace {
+
+constexpr int kTriThreads = 1024;
+constexpr int kTriSmemMaxM = 150;  // trailing block m x m in shared memory when m <= 150
+constexpr int kSyevMaxD = 2048;
+constexpr int kSyevJacobiMaxD = 48;
+
+// ------------------------------------------------------------------ 1. tridiagonalisation
+// a: d x d working copy (row-major, lda = d), symmetric, both triangles kept.
+// On exit: diag[k], off[k] (T(k+1,k)), reflector k stored in vref[k*d + i]
+// for i < d-k-1 (v[0] = 1), tau[k].
+__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(int d, const double* __restrict__ h, int ldh,
+                                                               double* __restrict__ a, double* __restrict__ vref,
+                                                               double* __restrict__ tau, double* __restrict__ diag,
+                                                               double* __restrict__ off) {
+    extern __shared__ double sm[];
+    __shared__ double red[kTriThreads / 32];
+    __shared__ double s_scal[4];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    double* v = sm;          // d
+    double* p = sm + d;      // d
+    double* tri = sm + 2 * d;  // trailing block once it fits
+    for (int e = tid; e < d * d; e += nt) {
+        const int i = e / d, j = e % d;
+        a[e] = 0.5 * (h[static_cast<size_t>(i) * ldh + j] + h[static_cast<size_t>(j) * ldh + i]);
+    }
+    __syncthreads();
+    bool in_smem = false;
+    int base = 0;  // row/col offset of `tri` inside a
+    auto A = [&](int i, int j) -> double& {  // trailing-block accessor, i, j >= base
+        return in_smem ? tri[(i - base) * (d - base) + (j - base)] : a[static_cast<size_t>(i) * d + j];
+    };
+    auto block_sum = [&](double x) {
+        x = warp_sum(x);
+        if (lane == 0) red[wid] = x;
+        __syncthreads();
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += red[w];
+        __syncthreads();
+        return s;
+    };
+    for (int k = 0; k + 2 < d; ++k) {
+        const int m = d - k - 1;
+        if (!in_smem && m <= kTriSmemMaxM) {
+            // move the trailing (m+1) x (m+1) block (rows/cols >= k) into shared memory
+            base = k;
+            const int mm = d - base;
+            for (int e = tid; e < mm * mm; e += nt) tri[e] = a[static_cast<size_t>(base + e / mm) * d + base + e % mm];
+            __syncthreads();
+            in_smem = true;
+        }
+        // (a) reflector from x = A(k+1:, k)
+        double xs = 0.0;
+        for (int i = 1 + tid; i < m; i += nt) {
+            const double x = A(k + 1 + i, k);
+            xs = fma(x, x, xs);
+        }
+        const double xnorm2 = block_sum(xs);
+        if (tid == 0) {
+            const double alpha = A(k + 1, k);
+            diag[k] = A(k, k);
+            double t = 0.0, beta = alpha, scal = 0.0;
+            if (xnorm2 > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+                t = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            off[k] = beta;
+            tau[k] = t;
+            s_scal[0] = t;
+            s_scal[1] = scal;
+        }
+        __syncthreads();
+        const double t = s_scal[0], scal = s_scal[1];
+        for (int i = tid; i < m; i += nt) {
+            const double vi = i == 0 ? 1.0 : A(k + 1 + i, k) * scal;
+            v[i] = vi;
+            vref[static_cast<size_t>(k) * d + i] = vi;
+        }
+        __syncthreads();
+        if (t == 0.0) continue;  // H = I: nothing to update (uniform branch)
+        // (b) p = t * A22 v   (warp per row, lanes across the row)
+        for (int i = wid; i < m; i += nw) {
+            double s = 0.0;
+            for (int j = lane; j < m; j += 32) s = fma(A(k + 1 + i, k + 1 + j), v[j], s);
+            s = warp_sum(s);
+            if (lane == 0) p[i] = t * s;
+        }
+        __syncthreads();
+        // (c) w = p - (t/2)(p^T v) v
+        double pv = 0.0;
+        for (int i = tid; i < m; i += nt) pv = fma(p[i], v[i], pv);
+        const double kk = -0.5 * t * block_sum(pv);
+        for (int i = tid; i < m; i += nt) p[i] = fma(kk, v[i], p[i]);
+        __syncthreads();
+        // (d) A22 -= v w^T + w v^T
+        for (int e = tid; e < m * m; e += nt) {
+            const int i = e / m, j = e % m;
+            double& x = A(k + 1 + i, k + 1 + j);
+            x -= v[i] * p[j] + p[i] * v[j];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (d >= 2) {
+            diag[d - 2] = A(d - 2, d - 2);
+            off[d - 2] = A(d - 1, d - 2);
+            tau[d - 2] = 0.0;
+        }
+        diag[d - 1] = A(d - 1, d - 1);
+        off[d - 1] = 0.0;
+        if (d >= 1) tau[d - 1] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------ 2. bisection
+__device__ __forceinline__ int sturm_count(int d, const double* __restrict__ dg, const double* __restrict__ off,
+                                           double x, double pivmin) {
+    int cnt = 0;
+    double q = dg[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    for (int i = 1; i < d; ++i) {
+        const double e = off[i - 1];
+        q = dg[i] - x - (e * e) / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+    }
+    return cnt;
+}
+
+// one warp per eigenvalue index j < n_need; 32-way multisection
+__global__ void __launch_bounds__(256) bisect_kernel(int d, const double* __restrict__ dg,
+                                                      const double* __restrict__ off, int n_need,
+                                                      double* __restrict__ lam, double* __restrict__ e2buf) {
+    const int lane = threadIdx.x & 31;
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    (void)e2buf;
+    if (j >= n_need) return;
+    // Gershgorin interval and pivmin (every warp, O(d))
+    double lo = INFINITY, hi = -INFINITY, emax2 = 0.0;
+    for (int i = lane; i < d; i += 32) {
+        const double r = (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0);
+        lo = fmin(lo, dg[i] - r);
+        hi = fmax(hi, dg[i] + r);
+        if (i + 1 < d) emax2 = fmax(emax2, off[i] * off[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+    }
+    const double tnorm = fmax(fabs(lo), fabs(hi));
+    const double pivmin = DBL_MIN * fmax(1.0, emax2);
+    const double slack = 2.0 * DBL_EPSILON * tnorm + pivmin;
+    lo -= slack;
+    hi += slack;
+    const double* e2 = off;
+    // invariant: count(lo) <= j < count(hi)
+    for (int it = 0; it < 40; ++it) {
+        const double width = hi - lo;
+        if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
+        const double x = lo + width * (lane + 1) / 33.0;
+        const int c = sturm_count(d, dg, e2, x, pivmin);
+        // first lane whose probe has more than j eigenvalues below it
+        const unsigned above = __ballot_sync(0xffffffffu, c > j);
+        const int first = above ? __ffs(above) - 1 : 32;
+        const double new_lo = first == 0 ? lo : __shfl_sync(0xffffffffu, x, max(first - 1, 0));
+        const double new_hi = first == 32 ? hi : __shfl_sync(0xffffffffu, x, min(first, 31));
+        if (new_lo == lo && new_hi == hi) break;
+        lo = new_lo;
+        hi = new_hi;
+    }
+    if (lane == 0) lam[j] = 0.5 * (lo + hi);
+}
+
+// ------------------------------------------------------------------ 3. inverse iteration
+// groups of consecutive eigenvalues closer than gap_rel * ||T||; gstart[g], ngroups
+__global__ void group_kernel(int n_need, const double* __restrict__ lam, const double* __restrict__ dg,
+                             const double* __restrict__ off, int d, int* __restrict__ gstart,
+                             int* __restrict__ ngroups) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double tnorm = 0.0;
+    for (int i = 0; i < d; ++i)
+        tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0));
+    const double thr = 1e-7 * fmax(tnorm, DBL_MIN);
+    int g = 0;
+    for (int j = 0; j < n_need; ++j)
+        if (j == 0 || lam[j] - lam[j - 1] > thr) gstart[g++] = j;
+    gstart[g] = n_need;
+    *ngroups = g;
+}
+
+// Solve (T - lam I) y = b in place (b -> y) by Gaussian elimination with partial
+// pivoting on the tridiagonal (rows i, i+1 may swap; fill in u2).  Tiny pivots are
+// replaced by +-eps*||T|| (inverse iteration on an intentionally singular shift).
+__device__ void tri_solve_shifted(int d, const double* __restrict__ dg, const double* __restrict__ off, double lam,
+                                  double tiny, double* __restrict__ b, double* __restrict__ u0,
+                                  double* __restrict__ u1, double* __restrict__ u2, int* __restrict__ piv) {
+    // rows: a_i = off[i-1] (sub), b_i = dg[i]-lam (diag), c_i = off[i] (super)
+    double diag_cur = dg[0] - lam;
+    double sup_cur = d > 1 ? off[0] : 0.0;
+    double sup2_cur = 0.0;
+    for (int i = 0; i + 1 < d; ++i) {
+        const double sub = off[i];  // A(i+1, i)
+        const double nd = dg[i + 1] - lam;
+        const double ns = i + 2 < d ? off[i + 1] : 0.0;
+        if (fabs(sub) > fabs(diag_cur)) {
+            // swap rows i and i+1
+            piv[i] = 1;
+            const double mult = diag_cur / sub;
+            u0[i] = sub;
+            u1[i] = nd;
+            u2[i] = ns;
+            const double bi = b[i];
+            b[i] = b[i + 1];
+            b[i + 1] = bi - mult * b[i];
+            diag_cur = sup_cur - mult * nd;
+            sup_cur = sup2_cur - mult * ns;
+            sup2_cur = 0.0;
+        } else {
+            piv[i] = 0;
+            const double p0 = fabs(diag_cur) < tiny ? copysign(tiny, diag_cur == 0.0 ? 1.0 : diag_cur) : diag_cur;
+            const double mult = sub / p0;
+            u0[i] = p0;
+            u1[i] = sup_cur;
+            u2[i] = sup2_cur;
+            b[i + 1] -= mult * b[i];
+            diag_cur = nd - mult * sup_cur;
+            sup_cur = ns;
+            sup2_cur = 0.0;
+        }
+    }
+    u0[d - 1] = fabs(diag_cur) < tiny ? copysign(tiny, diag_cur == 0.0 ? 1.0 : diag_cur) : diag_cur;
+    // back substitution with the upper band (u0 diag, u1 first, u2 second super-diagonal)
+    for (int i = d - 1; i >= 0; --i) {
+        double s = b[i];
+        if (i + 1 < d) s -= u1[i] * b[i + 1];
+        if (i + 2 < d) s -= u2[i] * b[i + 2];
+        const double p0 = fabs(u0[i]) < tiny ? copysign(tiny, u0[i] == 0.0 ? 1.0 : u0[i]) : u0[i];
+        b[i] = s / p0;
+    }
+    (void)piv;
+}
+
+// one warp per group; u column-major (ldu = d): column j = eigenvector j of T.
+// scratch: per warp 5*d doubles + d ints
+__global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restrict__ dg,
+                                                     const double* __restrict__ off,
+                                                     const double* __restrict__ lam, const int* __restrict__ gstart,
+                                                     const int* __restrict__ ngroups, double* __restrict__ u,
+                                                     double* __restrict__ scratch) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= *ngroups) return;
+    double* b = scratch + static_cast<size_t>(gw) * 5 * d;
+    double* u0 = b + d;
+    double* u1 = u0 + d;
+    double* u2 = u1 + d;
+    int* piv = reinterpret_cast<int*>(u2 + d);
+    double tnorm = 0.0;
+    for (int i = lane; i < d; i += 32)
+        tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0));
+    for (int o = 16; o > 0; o >>= 1) tnorm = fmax(tnorm, __shfl_xor_sync(0xffffffffu, tnorm, o));
+    const double tiny = DBL_EPSILON * fmax(tnorm, DBL_MIN);
+    const int g0 = gstart[gw], g1 = gstart[gw + 1];
+    for (int j = g0; j < g1; ++j) {
+        // deterministic pseudo-random start (splitmix64 of (j, i))
+        for (int i = lane; i < d; i += 32) {
+            unsigned long long z = (static_cast<unsigned long long>(j) << 32) + static_cast<unsigned long long>(i) +
+                                   0x9e3779b97f4a7c15ULL;
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+            z ^= z >> 31;
+            b[i] = static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+        }
+        __syncwarp();
+        const double shift = lam[j];
+        for (int it = 0; it < 3; ++it) {
+            if (lane == 0) tri_solve_shifted(d, dg, off, shift, tiny, b, u0, u1, u2, piv);
+            __syncwarp();
+            // orthogonalise against the group's earlier members (twice)
+            for (int pass = 0; pass < 2; ++pass)
+                for (int q = g0; q < j; ++q) {
+                    const double* uq = u + static_cast<size_t>(q) * d;
+                    double s = 0.0;
+                    for (int i = lane; i < d; i += 32) s = fma(uq[i], b[i], s);
+                    s = warp_sum(s);
+                    for (int i = lane; i < d; i += 32) b[i] -= s * uq[i];
+                    __syncwarp();
+                }
+            double nn = 0.0;
+            for (int i = lane; i < d; i += 32) nn = fma(b[i], b[i], nn);
+            nn = warp_sum(nn);
+            const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+            for (int i = lane; i < d; i += 32) b[i] *= inv;
+            __syncwarp();
+        }
+        double* uj = u + static_cast<size_t>(j) * d;
+        for (int i = lane; i < d; i += 32) uj[i] = b[i];
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ 5. back-transformation
+// z (row-major, ldz): z[:, c] = H_0 H_1 ... H_{d-3} u[:, c]; one warp per column.
+__global__ void __launch_bounds__(128) backtr_kernel(int d, int n_need, const double* __restrict__ vref,
+                                                      const double* __restrict__ tau, double* __restrict__ u,
+                                                      double* __restrict__ z, int ldz) {
+    const int lane = threadIdx.x & 31;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (c >= n_need) return;
+    double* x = u + static_cast<size_t>(c) * d;
+    for (int k = d - 3; k >= 0; --k) {
+        const double t = tau[k];
+        if (t == 0.0) continue;
+        const int m = d - k - 1;
+        const double* vk = vref + static_cast<size_t>(k) * d;
+        double s = 0.0;
+        for (int i = lane; i < m; i += 32) s = fma(vk[i], x[k + 1 + i], s);
+        s = warp_sum(s) * t;
+        for (int i = lane; i < m; i += 32) x[k + 1 + i] -= s * vk[i];
+        __syncwarp();
+    }
+    for (int i = lane; i < d; i += 32) z[static_cast<size_t>(i) * ldz + c] = x[i];
+}
+
+// u (column-major d x k) -> row-major scratch, and back
+__global__ void cm_to_rm_small(int d, int k, const double* __restrict__ cm, double* __restrict__ rm, int ldr) {
+    const int64_t total = static_cast<int64_t>(d) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(e / d), i = static_cast<int>(e % d);
+        rm[static_cast<size_t>(i) * ldr + c] = cm[e];
+    }
+}
+__global__ void rm_to_cm_small(int d, int k, const double* __restrict__ rm, int ldr, double* __restrict__ cm) {
+    const int64_t total = static_cast<int64_t>(d) * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(e / d), i = static_cast<int>(e % d);
+        cm[e] = rm[static_cast<size_t>(i) * ldr + c];
+    }
+}
+
+struct SyevWs {
+    double *a, *vref, *tau, *dg, *off, *e2, *u, *urm, *u2rm, *gram, *m, *chol, *scratch;
+    int *gstart, *ngroups, *cinfo;
+};
+
+size_t carve(SyevWs* w, void* base, int d) {
+    const size_t dd = static_cast<size_t>(d) * d;
+    char* p = static_cast<char*>(base);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char* r = p ? p + off : nullptr;
+        off += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    SyevWs t{};
+    t.a = reinterpret_cast<double*>(take(dd * 8));
+    t.vref = reinterpret_cast<double*>(take(dd * 8));
+    t.tau = reinterpret_cast<double*>(take(d * 8 + 8));
+    t.dg = reinterpret_cast<double*>(take(d * 8 + 8));
+    t.off = reinterpret_cast<double*>(take(d * 8 + 8));
+    t.e2 = reinterpret_cast<double*>(take(d * 8 + 8));
+    t.u = reinterpret_cast<double*>(take(dd * 8));
+    t.urm = reinterpret_cast<double*>(take(dd * 8));
+    t.u2rm = reinterpret_cast<double*>(take(dd * 8));
+    t.gram = reinterpret_cast<double*>(take(dd * 8));
+    t.m = reinterpret_cast<double*>(take(dd * 8));
+    t.chol = reinterpret_cast<double*>(take(bk_chol_work_bytes(d)));
+    t.scratch = reinterpret_cast<double*>(take(static_cast<size_t>(d) * (6 * d + 8) * 8));
+    t.gstart = reinterpret_cast<int*>(take((d + 2) * 4));
+    t.ngroups = reinterpret_cast<int*>(take(64));
+    t.cinfo = reinterpret_cast<int*>(take(64));
+    const size_t gram_ws = bk_gram_work_bytes(d, d, d);
+    double* gw = reinterpret_cast<double*>(take(gram_ws));
+    (void)gw;
+    if (w) *w = t;
+    return off;
+}
+
+}  // namespace
+}  // namespace bk
+
+using namespace bk;
+
+extern "C" size_t bk_syev_tri_work_bytes(int d) { return carve(nullptr, nullptr, d > 0 ? d : 1); }
+
+extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double* values, double* z, int ldz,
+                             void* work, int* info, void* stream) {
+    if (d <= 0) return 0;
+    if (n_need <= 0 || n_need > d) n_need = d;
+    const cudaStream_t s = as_stream(stream);
+    SyevWs w;
+    const size_t total = carve(&w, work, d);
+    void* gram_work = static_cast<char*>(work) + total - ((bk_gram_work_bytes(d, d, d) + 255) & ~size_t(255));
+    const int mm = d < kTriSmemMaxM + 1 ? d : kTriSmemMaxM + 1;
+    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(d) + static_cast<size_t>(mm) * mm);
+    static const cudaError_t attr = cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         static_cast<int>(sizeof(double) * (2 * kSyevMaxD + (kTriSmemMaxM + 1) * (kTriSmemMaxM + 1))));
+    BK_RET(attr);
+    if (d > kSyevMaxD) return static_cast<int>(cudaErrorInvalidValue);
+    if (d == 1) {
+        // 1x1: value and unit vector
+        BK_RET(cudaMemcpyAsync(values, h, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        const double one = 1.0;
+        BK_RET(cudaMemcpyAsync(z, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+        BK_RET(cudaMemsetAsync(info, 0, 2 * sizeof(int), s));
+        return 0;
+    }
+    tridiag_kernel<<<1, kTriThreads, smem, s>>>(d, h, ldh, w.a, w.vref, w.tau, w.dg, w.off);
+    bisect_kernel<<<ceil_div(n_need * 32, 256), 256, 0, s>>>(d, w.dg, w.off, n_need, values, w.e2);
+    group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
+    invit_kernel<<<ceil_div(n_need * 32, 128), 128, 0, s>>>(d, w.dg, w.off, values, w.gstart, w.ngroups, w.u,
+                                                           w.scratch);
+    // CholQR2 of U (d x n_need): row-major copy, Gram, Cholesky (no dropping), update
+    cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need);
+    for (int pass = 0; pass < 2; ++pass) {
+        double* src = pass == 0 ? w.urm : w.u2rm;
+        double* dst = pass == 0 ? w.u2rm : w.urm;
+        int rc = bk_gram_d(d, src, n_need, n_need, src, n_need, n_need, w.gram, n_need, gram_work, stream);
+        if (rc) return rc;
+        rc = bk_chol_drop_d(n_need, w.gram, n_need, nullptr, 0.0, w.m, n_need, w.cinfo, w.chol, stream);
+        if (rc) return rc;
+        rc = bk_gemm_d(d, src, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, dst, n_need, stream);
+        if (rc) return rc;
+    }
+    rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.urm, n_need, w.u);
+    backtr_kernel<<<ceil_div(n_need * 32, 128), 128, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+    BK_RET(cudaMemsetAsync(info, 0, 2 * sizeof(int), s));
+    BK_LAUNCHED();
+}
+
+// Dispatch: the one-CTA cyclic Jacobi (bk_small.cu) for small projected
+// problems, where its d-1 rounds per sweep are cheap and it gives the most
+// accurate vectors; tridiagonalisation + bisection + inverse iteration above.
+extern "C" size_t bk_syev_work_bytes(int d) {
+    const size_t a = bk_syev_jacobi_work_bytes(d), b = bk_syev_tri_work_bytes(d);
+    return a > b ? a : b;
+}
+
+extern "C" int bk_syev_d(int d, double* h, int ldh, int n_need, double* values, double* z, int ldz, void* work,
+                         int* info, void* stream) {
+    if (d <= kSyevJacobiMaxD) return bk_syev_jacobi_d(d, h, ldh, values, z, ldz, work, info, stream);
+    return bk_syev_tri_d(d, h, ldh, n_need, values, z, ldz, work, info, stream);
+}

@@ -51,7 +51,7 @@ int beig_matrix_lambda_min(const beig_matrix* a, double* out) {
         b2::DevMem h(nn * sizeof(double)), z(nn * sizeof(double)), vals(n * sizeof(double)),
             work(bk_syev_work_bytes(n)), info(4 * sizeof(int));
         b2::cuda_check(cudaMemcpy(h.p(), dense.data(), nn * sizeof(double), cudaMemcpyHostToDevice), "upload");
-        b2::cuda_check(bk_syev_d(n, h.d(), n, vals.d(), z.d(), n, work.p(), info.as<int>(), nullptr), "bk_syev_d");
+        b2::cuda_check(bk_syev_d(n, h.d(), n, 1, vals.d(), z.d(), n, work.p(), info.as<int>(), nullptr), "bk_syev_d");
         int hinfo[2] = {0, 0};
         double v0 = 0.0;
         b2::cuda_check(cudaMemcpy(hinfo, info.p(), 2 * sizeof(int), cudaMemcpyDeviceToHost), "download");

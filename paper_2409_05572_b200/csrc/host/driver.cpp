@@ -369,13 +369,15 @@ private:
 
     // Rayleigh-Ritz on s[:, 0:d]; columns [0, as_from) of AS already hold A s.
     // values -> VALS (ascending), coefficients -> Z (ldH)  (rr.cpp:8-14)
-    void rayleigh_ritz(Blk s, int d, int as_from) {
+    // n_need: leading Ritz pairs the caller uses (values/vectors beyond it are
+    // not computed on the tridiagonal path)
+    void rayleigh_ritz(Blk s, int d, int as_from, int n_need = 0) {
         meter_.rr(n_, d);
         spmm(s.at(as_from), d - as_from, AS().at(as_from));
         gram(n_, s.p, s.ld, d, AS_.d(), ldS_, d, H_.d(), ldH_);
         int* info = INFO_.as<int>() + 8;
         auto ts = prof_begin();
-        BKC(bk_syev_d(d, H_.d(), ldH_, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
+        BKC(bk_syev_d(d, H_.d(), ldH_, n_need > 0 ? n_need : d, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
         prof_end(ts, K_SYEV, 16.0 * d * d, 0.0);
         BKC(cudaMemcpyAsync(pin_.info + 8, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         syev_pending_ = true;
@@ -643,7 +645,7 @@ void Engine::solve_sd() {
             return finish(Status::stagnated, v, n_ev);
         }
         const int ds = xb + kw;
-        rayleigh_ritz(v, ds, n_old);
+        rayleigh_ritz(v, ds, n_old, n_now);
         lift(v, ds, Z_.d(), ldH_, n_now, S(1 - cur_));
         cur_ ^= 1;
         if (d == Decision::shrink) {
@@ -743,7 +745,7 @@ void Engine::solve_lobpcg() {
             }
         }
         // Rayleigh-Ritz on S = [X, P, W]; A X is still in AS(:, 0:n_old)
-        rayleigh_ritz(s, ds, n_old);
+        rayleigh_ritz(s, ds, n_old, n_now);
         // HL trick (solvers.cpp:187-196) in coefficient space:
         // ZC = [Z(:, :n_now) | orth(Zp)], Zp = Z(:, lock:n_now) with rows < n_now zeroed
         const int ahl = n_now - lock;  // n_now is post-expansion here

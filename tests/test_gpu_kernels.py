@@ -1,0 +1,195 @@
+"""Kernel-level parity on the B200: every bk_* kernel called through the thin C
+ABI on torch-allocated device memory, checked against the CPU oracle (SpMM,
+eigensolver) or an fp64 numpy reference (dense contractions).  Tolerances are
+written in each test."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from tests.helpers import dense_from_lower, random_sym_lower
+from tests.oracle_api import OracleKernels
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+_D = C.c_void_p
+
+
+@pytest.fixture(scope="module")
+def bk(product):
+    f = product.lib
+    f.bk_spmm_d.argtypes = [C.c_int, _D, _D, _D, _D, C.c_int, C.c_int, _D, C.c_int, _D]
+    f.bk_gram_work_bytes.restype = C.c_size_t
+    f.bk_gram_work_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+    f.bk_gram_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, _D, _D]
+    f.bk_gemm_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int, C.c_double, C.c_double, _D,
+                            C.c_int, _D]
+    f.bk_syev_work_bytes.restype = C.c_size_t
+    f.bk_syev_work_bytes.argtypes = [C.c_int]
+    f.bk_syev_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, _D, C.c_int, _D, _D, _D]
+    f.bk_syev_jacobi_d.argtypes = [C.c_int, _D, C.c_int, _D, _D, C.c_int, _D, _D, _D]
+    f.bk_syev_tri_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, _D, C.c_int, _D, _D, _D]
+    f.bk_chol_work_bytes.restype = C.c_size_t
+    f.bk_chol_work_bytes.argtypes = [C.c_int]
+    f.bk_chol_drop_d.argtypes = [C.c_int, _D, C.c_int, _D, C.c_double, _D, C.c_int, _D, _D, _D]
+    f.bk_colnorm2_work_bytes.restype = C.c_size_t
+    f.bk_colnorm2_work_bytes.argtypes = [C.c_int, C.c_int]
+    f.bk_colnorm2_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, _D, _D]
+    return f
+
+
+def dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x), device="cuda")
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def full_csr(rp, col, val, n):
+    a = dense_from_lower(rp, col, val, n)
+    r, c = np.nonzero(a)
+    frp = np.zeros(n + 1, dtype=np.int32)
+    np.add.at(frp, r + 1, 1)
+    return np.cumsum(frp).astype(np.int32), c.astype(np.int32), a[r, c], a
+
+
+@pytest.mark.parametrize("k", [1, 7, 32, 50, 96, 150])
+def test_spmm_vs_oracle(bk, oracle, k):
+    # K1 vs the oracle's reference-order spmv_block: 1e-13 relative (test_kernel.cpp:39-55)
+    n = 300
+    rp, col, val = random_sym_lower(n, 7, density=0.05)
+    frp, fcol, fval, _ = full_csr(rp, col, val, n)
+    x = np.random.default_rng(k).standard_normal((n, k))
+    ld = k + 3
+    xd = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    xd[:, :k] = dev(x)
+    yd = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    t_rp, t_c, t_v = dev(frp), dev(fcol), dev(fval)
+    assert bk.bk_spmm_d(n, ptr(t_rp), ptr(t_c), ptr(t_v), ptr(xd), ld, k, ptr(yd), ld, stream()) == 0
+    torch.cuda.synchronize()
+    a = oracle.from_csr(n, rp, col, val)
+    want = OracleKernels(oracle).spmv_block(a, x)
+    got = yd[:, :k].cpu().numpy()
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+    # determinism: bit-identical across calls
+    y2 = torch.zeros_like(yd)
+    bk.bk_spmm_d(n, ptr(t_rp), ptr(t_c), ptr(t_v), ptr(xd), ld, k, ptr(y2), ld, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(y2[:, :k], yd[:, :k])
+
+
+@pytest.mark.parametrize("n,a,b", [(1000, 13, 70), (262144, 96, 96), (5000, 288, 288), (77, 1, 1)])
+def test_gram_vs_numpy(bk, n, a, b):
+    rng = np.random.default_rng(n + a)
+    x, y = rng.standard_normal((n, a)), rng.standard_normal((n, b))
+    xd, yd = dev(x), dev(y)
+    c = torch.zeros((a, b), dtype=torch.float64, device="cuda")
+    ws = torch.empty(bk.bk_gram_work_bytes(n, a, b) // 8 + 1, dtype=torch.float64, device="cuda")
+    assert bk.bk_gram_d(n, ptr(xd), a, a, ptr(yd), b, b, ptr(c), b, ptr(ws), stream()) == 0
+    torch.cuda.synchronize()
+    want = x.T @ y
+    # fp64: |err| <= 1e-13 * n-scaled magnitude
+    assert np.abs(c.cpu().numpy() - want).max() <= 1e-13 * np.sqrt(n) * np.abs(want).max() + 1e-12
+
+
+@pytest.mark.parametrize("n,d,k,beta", [(1000, 40, 40, 0.0), (262144, 288, 96, 0.0), (5000, 96, 7, 1.0), (33, 5, 3, -1.0)])
+def test_gemm_vs_numpy(bk, n, d, k, beta):
+    rng = np.random.default_rng(d + k)
+    x, cm, y0 = rng.standard_normal((n, d)), rng.standard_normal((d, k)), rng.standard_normal((n, k))
+    xd, cd, yd = dev(x), dev(cm), dev(y0)
+    assert bk.bk_gemm_d(n, ptr(xd), d, d, ptr(cd), k, k, -1.0, beta, ptr(yd), k, stream()) == 0
+    torch.cuda.synchronize()
+    want = -x @ cm + beta * y0
+    assert np.abs(yd.cpu().numpy() - want).max() <= 1e-13 * d * np.abs(want).max()
+
+
+def clustered_sym(d, seed, cluster=(3, 0.5)):
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    nc = min(cluster[0], d - 1)
+    lam = np.sort(np.r_[np.full(nc, cluster[1]), rng.uniform(-3, 3, d - nc)])
+    return (q * lam) @ q.T, lam
+
+
+@pytest.mark.parametrize("path", ["jacobi", "tri", "dispatch"])
+@pytest.mark.parametrize("d", [2, 5, 40, 97, 288])
+def test_syev_vs_reference(bk, oracle, path, d):
+    if path == "jacobi" and d > 160:
+        pytest.skip("one-CTA Jacobi is used for small d only")
+    h, lam = clustered_sym(d, d)
+    hd = dev(h)
+    vals = torch.zeros(d, dtype=torch.float64, device="cuda")
+    z = torch.zeros((d, d), dtype=torch.float64, device="cuda")
+    ws = torch.empty(bk.bk_syev_work_bytes(d) // 8 + 1, dtype=torch.float64, device="cuda")
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    if path == "jacobi":
+        rc = bk.bk_syev_jacobi_d(d, ptr(hd), d, ptr(vals), ptr(z), d, ptr(ws), ptr(info), stream())
+    elif path == "tri":
+        rc = bk.bk_syev_tri_d(d, ptr(hd), d, d, ptr(vals), ptr(z), d, ptr(ws), ptr(info), stream())
+    else:
+        rc = bk.bk_syev_d(d, ptr(hd), d, d, ptr(vals), ptr(z), d, ptr(ws), ptr(info), stream())
+    torch.cuda.synchronize()
+    assert rc == 0 and int(info[1]) == 0
+    v, zz = vals.cpu().numpy(), z.cpu().numpy()
+    ov, _ = OracleKernels(oracle).sym_eig(h)
+    scale = np.abs(lam).max()
+    np.testing.assert_allclose(v, ov, atol=1e-13 * scale * max(1, d / 50))
+    np.testing.assert_allclose(v, lam, atol=1e-12 * scale)
+    assert np.all(np.diff(v) >= 0)
+    assert np.abs(zz.T @ zz - np.eye(d)).max() < 1e-12
+    assert np.linalg.norm(h @ zz - zz * v, axis=0).max() < 1e-12 * scale * max(1, d / 50)
+
+
+def test_syev_partial_and_degenerate(bk):
+    # n_need < d (the LOBPCG use) and an exact 6-fold multiplet
+    d, k = 200, 70
+    h, lam = clustered_sym(d, 3, cluster=(6, -1.25))
+    hd = dev(h)
+    vals = torch.zeros(d, dtype=torch.float64, device="cuda")
+    z = torch.zeros((d, d), dtype=torch.float64, device="cuda")
+    ws = torch.empty(bk.bk_syev_work_bytes(d) // 8 + 1, dtype=torch.float64, device="cuda")
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    assert bk.bk_syev_d(d, ptr(hd), d, k, ptr(vals), ptr(z), d, ptr(ws), ptr(info), stream()) == 0
+    torch.cuda.synchronize()
+    v = vals.cpu().numpy()[:k]
+    zz = z.cpu().numpy()[:, :k]
+    np.testing.assert_allclose(v, lam[:k], atol=1e-12 * 3)
+    assert np.abs(zz.T @ zz - np.eye(k)).max() < 1e-12
+    assert np.linalg.norm(h @ zz - zz * v, axis=0).max() < 1e-12 * 3
+
+
+def _chol(bk, w):
+    a = w.shape[1]
+    g = w.T @ w
+    ref2 = np.sum(w * w, axis=0)
+    gd, rd = dev(g), dev(ref2)
+    m = torch.zeros((a, a), dtype=torch.float64, device="cuda")
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    ws = torch.empty(bk.bk_chol_work_bytes(a) // 8 + 1, dtype=torch.float64, device="cuda")
+    assert bk.bk_chol_drop_d(a, ptr(gd), a, ptr(rd), 1e-8, ptr(m), a, ptr(info), ptr(ws), stream()) == 0
+    torch.cuda.synchronize()
+    return int(info[0]), int(info[1]), m.cpu().numpy()
+
+
+def test_chol_drop_rule(bk):
+    # K4 keep/drop (kernel.cpp:83-85 rule): a certainly independent block is
+    # orthonormalised by W*m; an exactly dependent column (and a zero column)
+    # is dropped; a column whose remaining norm sits inside the cancellation
+    # band is reported as uncertain (the driver then redoes it with exact CGS2)
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((15, 3))
+    w = np.c_[x, 2 * x[:, 0] + 1e-3 * rng.standard_normal(15), np.zeros(15)]
+    kept, unsure, m = _chol(bk, w)
+    assert (kept, unsure) == (4, 0)
+    q = w @ m[:, :kept]
+    assert np.abs(q.T @ q - np.eye(kept)).max() < 1e-9
+    w2 = np.c_[x, x[:, 1] - x[:, 2] + 1e-10 * rng.standard_normal(15)]
+    kept2, unsure2, _ = _chol(bk, w2)
+    assert unsure2 == 1
