@@ -7,17 +7,19 @@
 //   K2 Gram    C = X^T Y   (X n x a, Y n x b, reduce over the long n axis)
 //      replaces s.transpose()*as (proj/src/rr.cpp:11) and q.transpose()*v
 //      inside CGS2 (proj/src/kernel.cpp:76,79).  Split-K over n so ~2 CTAs per
-//      SM are busy even when a x b is only a few 64x64 tiles; partial tiles go
-//      to a workspace and are summed in a fixed split order (deterministic).
+//      SM are busy even when a x b is a handful of tiles; partial tiles go to a
+//      workspace and are summed in a fixed split order (deterministic).
 //   K3 update  Y = alpha X C + beta Y   (X n x d, C d x k)
 //      replaces s*e.vectors (rr.cpp:13), s*z1 / s*o.q (solvers.cpp:195) and
 //      q*(q^T v) (kernel.cpp:76,79).
 //
-// Both: 64x64 output tile per CTA, 8 warps each owning a 32x16 sub-tile
-// (4 x 2 DMMA fragments), 16-deep K stages streamed global->shared with
-// cp.async in a 3-stage ring.  Shared-memory pitches are 4 (mod 16) doubles so
-// the fragment loads (lanes g=0..3, t=0..3 of a half-warp) hit 16 distinct
-// 8-byte banks.
+// Tiles are sized to the block widths of the solver (multiples of 96 at the
+// reference defaults n_ex = 1.5 n_ev): Gram 96 x 96 per CTA with 8 warps of
+// 48 x 24 (18 DMMA per 4-deep k step against 9 fragment loads); update 128 rows
+// x 96 columns with 8 warps of 32 x 48 (24 DMMA per k step).  Operands stream
+// global -> shared with cp.async (16-byte when the view is 16-byte aligned,
+// tails zero-filled) through a multi-stage ring; shared pitches are 4 (mod 16)
+// doubles so fragment loads of a half-warp hit 16 distinct 8-byte banks.
 #include <algorithm>
 
 #include "bk_common.cuh"
@@ -25,49 +27,61 @@
 namespace bk {
 namespace {
 
-constexpr int TM = 64, TN = 64, TK = 16, STAGES = 3;
-constexpr int PITCH_T = TM + 4;  // [TK][PITCH_T] tiles (row = k)
-constexpr int PITCH_X = TK + 4;  // [TM][PITCH_X] tile of X rows in the update
+template <bool V16>
+__device__ __forceinline__ void load_rows(double* dst, int pitch, const double* __restrict__ src, int ld, int r0,
+                                          int r_end, int c0, int c_end, int rows, int cols, int tid, int nthreads) {
+    // copy src[r0 + r][c0 + c] for r < rows, c < cols into dst[r*pitch + c], zero outside
+    if constexpr (V16) {
+        const int cpr = cols / 2;  // 16-byte chunks per row (cols even)
+        for (int e = tid; e < rows * cpr; e += nthreads) {
+            const int r = e / cpr, c = 2 * (e - r * cpr);
+            const int row = r0 + r, col = c0 + c;
+            int bytes = 0;
+            if (row < r_end && col < c_end) bytes = col + 1 < c_end ? 16 : 8;
+            const double* g = bytes ? src + static_cast<size_t>(row) * ld + col : src;
+            cp_async16(dst + r * pitch + c, g, bytes);
+        }
+    } else {
+        for (int e = tid; e < rows * cols; e += nthreads) {
+            const int r = e / cols, c = e - r * cols;
+            const int row = r0 + r, col = c0 + c;
+            const bool ok = row < r_end && col < c_end;
+            cp_async8(dst + r * pitch + c, ok ? src + static_cast<size_t>(row) * ld + col : src, ok);
+        }
+    }
+}
 
 // ------------------------------------------------------------------ Gram
-// smem per stage: Xs[TK][PITCH_T], Ys[TK][PITCH_T]
-__global__ void __launch_bounds__(256) gram_kernel(int n, const double* __restrict__ x, int ldx, int a,
-                                                    const double* __restrict__ y, int ldy, int b,
-                                                    double* __restrict__ out, int ldo, int rows_per_split) {
-    extern __shared__ double smem[];
-    double* xs = smem;                         // STAGES * TK * PITCH_T
-    double* ys = smem + STAGES * TK * PITCH_T;  // STAGES * TK * PITCH_T
+template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16>
+__global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double* __restrict__ x, int ldx, int a,
+                                                             const double* __restrict__ y, int ldy, int b,
+                                                             double* __restrict__ out, int ldo, int rows_per_split) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int PX = TM + 4, PY = TN + 4;
+    constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
+    extern __shared__ __align__(16) double smem[];
+    double* xs = smem;                      // STAGES x TK x PX
+    double* ys = smem + STAGES * TK * PX;   // STAGES x TK x PY
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int i0 = blockIdx.x * TM, j0 = blockIdx.y * TN;
     const int split = blockIdx.z;
     const int r_begin = split * rows_per_split;
     const int r_end = min(n, r_begin + rows_per_split);
-    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+    const int wm = (warp / WN) * (TM / WM), wn = (warp % WN) * (TN / WN);
 
-    double acc[4][2][2];
+    double acc[FM][FN][2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int ni = 0; ni < FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
     const int nk = ceil_div(max(r_end - r_begin, 0), TK);
     auto load_stage = [&](int kt, int st) {
         const int r0 = r_begin + kt * TK;
-        double* xd = xs + st * TK * PITCH_T;
-        double* yd = ys + st * TK * PITCH_T;
-#pragma unroll
-        for (int e = 0; e < (TK * TM) / 256; ++e) {
-            const int idx = tid + 256 * e;
-            const int rr = idx / TM, cc = idx % TM;
-            const int row = r0 + rr;
-            const bool okx = row < r_end && i0 + cc < a;
-            const bool oky = row < r_end && j0 + cc < b;
-            cp_async8(xd + rr * PITCH_T + cc, okx ? x + static_cast<size_t>(row) * ldx + i0 + cc : x, okx);
-            cp_async8(yd + rr * PITCH_T + cc, oky ? y + static_cast<size_t>(row) * ldy + j0 + cc : y, oky);
-        }
+        load_rows<V16>(xs + st * TK * PX, PX, x, ldx, r0, r_end, i0, a, TK, TM, tid, NT);
+        load_rows<V16>(ys + st * TK * PY, PY, y, ldy, r0, r_end, j0, b, TK, TN, tid, NT);
     };
-
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
         if (st < nk) load_stage(st, st);
@@ -79,28 +93,28 @@ __global__ void __launch_bounds__(256) gram_kernel(int n, const double* __restri
         const int nxt = kt + STAGES - 1;
         if (nxt < nk) load_stage(nxt, nxt % STAGES);
         cp_async_commit();
-        const double* xd = xs + (kt % STAGES) * TK * PITCH_T;
-        const double* yd = ys + (kt % STAGES) * TK * PITCH_T;
+        const double* xd = xs + (kt % STAGES) * TK * PX;
+        const double* yd = ys + (kt % STAGES) * TK * PY;
 #pragma unroll
         for (int k4 = 0; k4 < TK; k4 += 4) {
-            double af[4], bf[2];
+            double af[FM], bf[FN];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) af[mi] = xd[(k4 + t) * PITCH_T + wm + mi * 8 + g];
+            for (int mi = 0; mi < FM; ++mi) af[mi] = xd[(k4 + t) * PX + wm + mi * 8 + g];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) bf[ni] = yd[(k4 + t) * PITCH_T + wn + ni * 8 + g];
+            for (int ni = 0; ni < FN; ++ni) bf[ni] = yd[(k4 + t) * PY + wn + ni * 8 + g];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                for (int ni = 0; ni < FN; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
     }
     cp_async_wait<0>();
 
     double* o = out + static_cast<size_t>(split) * a * ldo;
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
+        for (int ni = 0; ni < FN; ++ni) {
             const int i = i0 + wm + mi * 8 + g;
             const int j = j0 + wn + ni * 8 + 2 * t;
             if (i < a) {
@@ -111,8 +125,8 @@ __global__ void __launch_bounds__(256) gram_kernel(int n, const double* __restri
 }
 
 // C[i][j] = sum_s work[s][i][j] in split order
-__global__ void gram_reduce(int splits, int a, int b, const double* __restrict__ work,
-                            double* __restrict__ c, int ldc) {
+__global__ void gram_reduce(int splits, int a, int b, const double* __restrict__ work, double* __restrict__ c,
+                            int ldc) {
     const int64_t total = static_cast<int64_t>(a) * b;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -123,62 +137,53 @@ __global__ void gram_reduce(int splits, int a, int b, const double* __restrict__
     }
 }
 
+constexpr int GTM = 96, GTN = 96, GTK = 16, GWM = 2, GWN = 4, GST = 4;
+constexpr size_t kGramSmem = sizeof(double) * GST * GTK * ((GTM + 4) + (GTN + 4));
+
 struct GramPlan {
     int splits, rows_per_split;
 };
 
 GramPlan gram_plan(int n, int a, int b) {
-    const int tiles = ceil_div(a, TM) * ceil_div(b, TN);
+    const int tiles = ceil_div(a, GTM) * ceil_div(b, GTN);
     int splits = ceil_div(2 * kSMs, tiles);
-    splits = max(1, min(splits, ceil_div(n, 4 * TK * 8)));  // >= 512 rows per split
-    splits = min(splits, 64);
+    splits = max(1, min(splits, ceil_div(n, 256)));  // >= 256 rows per split
+    splits = min(splits, 96);
     int rps = ceil_div(n, splits);
-    rps = ceil_div(rps, TK) * TK;
+    rps = ceil_div(rps, GTK) * GTK;
     splits = max(1, ceil_div(n, rps));
     return {splits, rps};
 }
 
 // ------------------------------------------------------------------ update
-// smem per stage: Xs[TM][PITCH_X], Cs[TK][PITCH_T]
-__global__ void __launch_bounds__(256) gemm_kernel(int n, const double* __restrict__ x, int ldx, int d,
-                                                    const double* __restrict__ cm, int ldc, int k,
-                                                    double alpha, double beta, double* __restrict__ y,
-                                                    int ldy) {
-    extern __shared__ double smem[];
-    double* xs = smem;                            // STAGES * TM * PITCH_X
-    double* cs = smem + STAGES * TM * PITCH_X;    // STAGES * TK * PITCH_T
+template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16>
+__global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(int n, const double* __restrict__ x, int ldx, int d,
+                                                             const double* __restrict__ cm, int ldc, int k,
+                                                             double alpha, double beta, double* __restrict__ y,
+                                                             int ldy) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int PX = TK + 4, PC = TN + 4;
+    constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
+    extern __shared__ __align__(16) double smem[];
+    double* xs = smem;                     // STAGES x TM x PX
+    double* cs = smem + STAGES * TM * PX;  // STAGES x TK x PC
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int r0 = blockIdx.x * TM, c0 = blockIdx.y * TN;
-    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+    const int wm = (warp / WN) * (TM / WM), wn = (warp % WN) * (TN / WN);
 
-    double acc[4][2][2];
+    double acc[FM][FN][2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int ni = 0; ni < FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
     const int nk = ceil_div(d, TK);
     auto load_stage = [&](int kt, int st) {
         const int k0 = kt * TK;
-        double* xd = xs + st * TM * PITCH_X;
-        double* cd = cs + st * TK * PITCH_T;
-#pragma unroll
-        for (int e = 0; e < (TM * TK) / 256; ++e) {
-            const int idx = tid + 256 * e;
-            const int rr = idx / TK, kk = idx % TK;
-            const bool ok = r0 + rr < n && k0 + kk < d;
-            cp_async8(xd + rr * PITCH_X + kk, ok ? x + static_cast<size_t>(r0 + rr) * ldx + k0 + kk : x, ok);
-        }
-#pragma unroll
-        for (int e = 0; e < (TK * TN) / 256; ++e) {
-            const int idx = tid + 256 * e;
-            const int kk = idx / TN, cc = idx % TN;
-            const bool ok = k0 + kk < d && c0 + cc < k;
-            cp_async8(cd + kk * PITCH_T + cc, ok ? cm + static_cast<size_t>(k0 + kk) * ldc + c0 + cc : cm, ok);
-        }
+        load_rows<V16>(xs + st * TM * PX, PX, x, ldx, r0, n, k0, d, TM, TK, tid, NT);
+        load_rows<false>(cs + st * TK * PC, PC, cm, ldc, k0, d, c0, k, TK, TN, tid, NT);
     };
-
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
         if (st < nk) load_stage(st, st);
@@ -190,27 +195,27 @@ __global__ void __launch_bounds__(256) gemm_kernel(int n, const double* __restri
         const int nxt = kt + STAGES - 1;
         if (nxt < nk) load_stage(nxt, nxt % STAGES);
         cp_async_commit();
-        const double* xd = xs + (kt % STAGES) * TM * PITCH_X;
-        const double* cd = cs + (kt % STAGES) * TK * PITCH_T;
+        const double* xd = xs + (kt % STAGES) * TM * PX;
+        const double* cd = cs + (kt % STAGES) * TK * PC;
 #pragma unroll
         for (int k4 = 0; k4 < TK; k4 += 4) {
-            double af[4], bf[2];
+            double af[FM], bf[FN];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) af[mi] = xd[(wm + mi * 8 + g) * PITCH_X + k4 + t];
+            for (int mi = 0; mi < FM; ++mi) af[mi] = xd[(wm + mi * 8 + g) * PX + k4 + t];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) bf[ni] = cd[(k4 + t) * PITCH_T + wn + ni * 8 + g];
+            for (int ni = 0; ni < FN; ++ni) bf[ni] = cd[(k4 + t) * PC + wn + ni * 8 + g];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                for (int ni = 0; ni < FN; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
     }
     cp_async_wait<0>();
 
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
+        for (int ni = 0; ni < FN; ++ni) {
             const int i = r0 + wm + mi * 8 + g;
             const int j = c0 + wn + ni * 8 + 2 * t;
             if (i < n) {
@@ -222,8 +227,15 @@ __global__ void __launch_bounds__(256) gemm_kernel(int n, const double* __restri
         }
 }
 
-constexpr size_t kGramSmem = sizeof(double) * 2 * STAGES * TK * PITCH_T;
-constexpr size_t kGemmSmem = sizeof(double) * (STAGES * TM * PITCH_X + STAGES * TK * PITCH_T);
+constexpr int UTM = 128, UTN = 96, UTK = 16, UWM = 4, UWN = 2, UST = 3;
+constexpr size_t kGemmSmem = sizeof(double) * UST * (UTM * (UTK + 4) + UTK * (UTN + 4));
+
+bool aligned16(const double* p, int ld) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld & 1) == 0; }
+
+template <class K>
+cudaError_t prep(K kernel, size_t smem) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+}
 
 }  // namespace
 }  // namespace bk
@@ -235,39 +247,56 @@ extern "C" size_t bk_gram_work_bytes(int n, int a, int b) {
     return static_cast<size_t>(p.splits) * max(a, 1) * max(b, 1) * sizeof(double);
 }
 
-extern "C" int bk_gram_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b,
-                         double* c, int ldc, void* work, void* stream) {
+extern "C" int bk_gram_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
+                         int ldc, void* work, void* stream) {
     if (a <= 0 || b <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
     if (n <= 0) {
         for (int i = 0; i < a; ++i) BK_RET(cudaMemsetAsync(c + static_cast<size_t>(i) * ldc, 0, sizeof(double) * b, s));
         return 0;
     }
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGramSmem));
-    BK_RET(attr);
+    auto k16 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, true>;
+    auto k8 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, false>;
+    static const cudaError_t a1 = prep(k16, kGramSmem);
+    static const cudaError_t a2 = prep(k8, kGramSmem);
+    BK_RET(a1);
+    BK_RET(a2);
     const GramPlan p = gram_plan(n, a, b);
-    const dim3 grid(ceil_div(a, TM), ceil_div(b, TN), p.splits);
+    const dim3 grid(ceil_div(a, GTM), ceil_div(b, GTN), p.splits);
     auto w = static_cast<double*>(work);
-    gram_kernel<<<grid, 256, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, w, b, p.rows_per_split);
-    const int64_t total = static_cast<int64_t>(a) * b;
-    gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
-        p.splits, a, b, w, c, ldc);
+    // a single split writes C directly
+    double* dst = p.splits == 1 ? c : w;
+    const int ldo = p.splits == 1 ? ldc : b;
+    if (aligned16(x, ldx) && aligned16(y, ldy))
+        k16<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
+    else
+        k8<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
+    if (p.splits > 1) {
+        const int64_t total = static_cast<int64_t>(a) * b;
+        gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
+            p.splits, a, b, w, c, ldc);
+    }
     BK_LAUNCHED();
 }
 
-extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k,
-                         double alpha, double beta, double* y, int ldy, void* stream) {
+extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                         double beta, double* y, int ldy, void* stream) {
     if (n <= 0 || k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
     if (d <= 0) {
         if (beta == 1.0) return 0;
         return bk_axpby_d(n, k, 0.0, y, ldy, beta, y, ldy, stream);
     }
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGemmSmem));
-    BK_RET(attr);
-    const dim3 grid(ceil_div(n, TM), ceil_div(k, TN));
-    gemm_kernel<<<grid, 256, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy);
+    auto k16 = gemm_kernel<UTM, UTN, UTK, UWM, UWN, UST, true>;
+    auto k8 = gemm_kernel<UTM, UTN, UTK, UWM, UWN, UST, false>;
+    static const cudaError_t a1 = prep(k16, kGemmSmem);
+    static const cudaError_t a2 = prep(k8, kGemmSmem);
+    BK_RET(a1);
+    BK_RET(a2);
+    const dim3 grid(ceil_div(n, UTM), ceil_div(k, UTN));
+    if (aligned16(x, ldx))
+        k16<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy);
+    else
+        k8<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy);
     BK_LAUNCHED();
 }

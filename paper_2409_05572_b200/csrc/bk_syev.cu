@@ -22,6 +22,8 @@
 // Why not Jacobi for d > 64: a cyclic Jacobi sweep is d-1 dependent rounds and
 // ~10 sweeps are needed, so it is latency-bound (96 ms at d = 288 on one CTA,
 // profiles/r01_bench_first.log); this path has O(d) dependent steps in total.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "bk_common.cuh"
@@ -31,7 +33,7 @@ namespace {
 
 constexpr int kTriThreads = 1024;
 constexpr int kTriSmemMaxM = 150;  // trailing block m x m in shared memory when m <= 150
-constexpr int kSyevMaxD = 2048;
+constexpr int kSyevMaxD = 1200;  // 4d + 151^2 doubles of shared memory <= 227 KB
 constexpr int kSyevJacobiMaxD = 48;
 
 // ------------------------------------------------------------------ 1. tridiagonalisation
@@ -140,6 +142,291 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(int d, const doubl
         off[d - 1] = 0.0;
         if (d >= 1) tau[d - 1] = 0.0;
     }
+}
+
+// Fused variant (the one launched): the rank-2 update of step k-1 is applied
+// lazily inside step k's single pass over the trailing block, which also
+// accumulates p = A v for step k — one read + one write of the trailing block
+// per step instead of two reads + one write.
+__global__ void __launch_bounds__(kTriThreads) tridiag_fused_kernel(int d, const double* __restrict__ h, int ldh,
+                                                                     double* __restrict__ a,
+                                                                     double* __restrict__ vref,
+                                                                     double* __restrict__ tau,
+                                                                     double* __restrict__ diag,
+                                                                     double* __restrict__ off) {
+    extern __shared__ double sm[];
+    __shared__ double red[kTriThreads / 32];
+    __shared__ double s_scal[2];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    double* v = sm;           // current reflector (absolute row index)
+    double* vp = sm + d;      // pending update: previous reflector
+    double* wp = sm + 2 * d;  // pending update: previous w
+    double* col = sm + 3 * d; // column k after the pending update; reused for p / w
+    double* tri = sm + 4 * d; // trailing block once it fits
+    for (int e = tid; e < d * d; e += nt) {
+        const int i = e / d, j = e - i * d;
+        a[e] = 0.5 * (h[static_cast<size_t>(i) * ldh + j] + h[static_cast<size_t>(j) * ldh + i]);
+    }
+    for (int i = tid; i < d; i += nt) {
+        vp[i] = 0.0;
+        wp[i] = 0.0;
+    }
+    __syncthreads();
+    bool in_smem = false;
+    int base = 0, ld = d;
+    double* st = a;  // storage of rows/cols >= base
+    auto block_sum = [&](double x) {
+        x = warp_sum(x);
+        if (lane == 0) red[wid] = x;
+        __syncthreads();
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += red[w];
+        __syncthreads();
+        return s;
+    };
+    for (int k = 0; k + 2 < d; ++k) {
+        const int m = d - k - 1;
+        if (!in_smem && m + 1 <= kTriSmemMaxM + 1) {
+            const int mm = d - k;
+            for (int e = tid; e < mm * mm; e += nt) {
+                const int i = e / mm, j = e - i * mm;
+                tri[e] = a[static_cast<size_t>(k + i) * d + k + j];
+            }
+            __syncthreads();
+            in_smem = true;
+            base = k;
+            ld = mm;
+            st = tri;
+        }
+        // (1) column k with the pending update applied
+        const double vpk = vp[k], wpk = wp[k];
+        double xs = 0.0;
+        for (int r = k + tid; r < d; r += nt) {
+            const double x = st[static_cast<size_t>(r - base) * ld + (k - base)] - (vp[r] * wpk + wp[r] * vpk);
+            col[r] = x;
+            if (r >= k + 2) xs = fma(x, x, xs);
+        }
+        const double xnorm2 = block_sum(xs);  // includes a __syncthreads: col[] visible
+        // (2) reflector
+        if (tid == 0) {
+            const double alpha = col[k + 1];
+            diag[k] = col[k];
+            double t = 0.0, beta = alpha, scal = 0.0;
+            if (xnorm2 > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+                t = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            off[k] = beta;
+            tau[k] = t;
+            s_scal[0] = t;
+            s_scal[1] = scal;
+        }
+        __syncthreads();
+        const double t = s_scal[0], scal = s_scal[1];
+        for (int r = k + 1 + tid; r < d; r += nt) {
+            const double vr = r == k + 1 ? 1.0 : col[r] * scal;
+            v[r] = vr;
+            vref[static_cast<size_t>(k) * d + (r - k - 1)] = vr;
+        }
+        __syncthreads();
+        // (3) fused pass: apply the pending update to the trailing block and
+        //     accumulate p = t * A22 v (warp per row, lanes across the row)
+        // 8 independent loads per lane in flight: one CTA must cover L2 latency
+        constexpr int U = 8;
+        for (int i = k + 1 + wid; i < d; i += nw) {
+            double* row = st + static_cast<size_t>(i - base) * ld - base;
+            const double vpi = vp[i], wpi = wp[i];
+            double s = 0.0;
+            for (int j0 = k + 1 + lane; j0 < d; j0 += 32 * U) {
+                double x[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + 32 * u;
+                    x[u] = j < d ? row[j] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + 32 * u;
+                    if (j < d) {
+                        const double y = x[u] - (vpi * wp[j] + wpi * vp[j]);
+                        row[j] = y;
+                        s = fma(y, v[j], s);
+                    }
+                }
+            }
+            s = warp_sum(s);
+            if (lane == 0) col[i] = t * s;  // p_i (column k no longer needed)
+        }
+        __syncthreads();
+        // (4) w = p - (t/2)(p^T v) v becomes the pending update
+        double pv = 0.0;
+        for (int i = k + 1 + tid; i < d; i += nt) pv = fma(col[i], v[i], pv);
+        const double kk = -0.5 * t * block_sum(pv);
+        for (int i = k + 1 + tid; i < d; i += nt) {
+            wp[i] = fma(kk, v[i], col[i]);
+            vp[i] = v[i];
+        }
+        __syncthreads();
+    }
+    // last 2 x 2 block with the final pending update
+    if (tid == 0) {
+        const int k = d - 2;
+        auto at = [&](int i, int j) { return st[static_cast<size_t>(i - base) * ld + (j - base)] - (vp[i] * wp[j] + wp[i] * vp[j]); };
+        diag[k] = at(k, k);
+        off[k] = at(k + 1, k);
+        diag[k + 1] = at(k + 1, k + 1);
+        off[k + 1] = 0.0;
+        tau[k] = 0.0;
+        tau[k + 1] = 0.0;
+    }
+}
+
+// Cluster variant (used whenever the matrix fits in the cluster's shared
+// memory): a thread-block cluster of C CTAs (C = 1..16) keeps the whole
+// symmetric matrix resident in distributed shared memory, rows distributed
+// cyclically (row i on rank i % C).  Per step: every rank updates its part of
+// column k and scatters it to all ranks through DSMEM; after one cluster
+// barrier each rank computes the (identical) reflector redundantly; the fused
+// update + matvec runs on local rows; the p slices are all-gathered through
+// DSMEM and, after a second barrier, every rank forms w redundantly.
+// Reductions run in the same fixed order on every rank, so the replicated
+// scalars are bit-identical.
+constexpr int kClThreads = 512;
+
+__global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, const double* __restrict__ h, int ldh,
+                                                                      double* __restrict__ vref,
+                                                                      double* __restrict__ tau,
+                                                                      double* __restrict__ diag,
+                                                                      double* __restrict__ off) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = static_cast<int>(cl.num_blocks());
+    const int rank = static_cast<int>(cl.block_rank());
+    extern __shared__ double sm[];
+    __shared__ double red[kClThreads / 32];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    const int nloc = (d + C - 1) / C;
+    double* A = sm;                       // local rows: A[t*d + j] is row rank + C*t
+    double* v = A + static_cast<size_t>(nloc) * d;
+    double* vp = v + d;
+    double* wp = vp + d;
+    double* col = wp + d;
+    double* p = col + d;
+    for (int e = tid; e < nloc * d; e += nt) {
+        const int t = e / d, j = e - t * d;
+        const int i = rank + C * t;
+        if (i < d) A[e] = 0.5 * (h[static_cast<size_t>(i) * ldh + j] + h[static_cast<size_t>(j) * ldh + i]);
+    }
+    for (int i = tid; i < d; i += nt) {
+        vp[i] = 0.0;
+        wp[i] = 0.0;
+    }
+    auto block_sum = [&](double x) {
+        x = warp_sum(x);
+        if (lane == 0) red[wid] = x;
+        __syncthreads();
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += red[w];
+        __syncthreads();
+        return s;
+    };
+    cl.sync();
+    for (int k = 0; k + 2 < d; ++k) {
+        // phase 1: own rows r >= k of column k (pending update applied), scattered to every rank
+        const int t0 = k <= rank ? 0 : (k - rank + C - 1) / C;
+        const double vpk = vp[k], wpk = wp[k];
+        for (int t = t0 + tid; t < nloc; t += nt) {
+            const int r = rank + C * t;
+            if (r >= d) break;
+            const double x = A[static_cast<size_t>(t) * d + k] - (vp[r] * wpk + wp[r] * vpk);
+            for (int q = 0; q < C; ++q) cl.map_shared_rank(col, q)[r] = x;
+        }
+        cl.sync();
+        // phase 1b (replicated): reflector from col[k+1:]
+        double xs = 0.0;
+        for (int r = k + 2 + tid; r < d; r += nt) xs = fma(col[r], col[r], xs);
+        const double xnorm2 = block_sum(xs);
+        const double alpha = col[k + 1];
+        double t = 0.0, beta = alpha, scal = 0.0;
+        if (xnorm2 > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+            t = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int r = k + 1 + tid; r < d; r += nt) {
+            const double vr = r == k + 1 ? 1.0 : col[r] * scal;
+            v[r] = vr;
+            if (rank == 0) vref[static_cast<size_t>(k) * d + (r - k - 1)] = vr;
+        }
+        if (rank == 0 && tid == 0) {
+            diag[k] = col[k];
+            off[k] = beta;
+            tau[k] = t;
+        }
+        __syncthreads();
+        // phase 2: fused pending update + p = t A22 v on local rows i >= k+1
+        const int t1 = k + 1 <= rank ? 0 : (k + 1 - rank + C - 1) / C;
+        for (int tt = t1 + wid; tt < nloc; tt += nw) {
+            const int i = rank + C * tt;
+            if (i >= d) break;
+            double* row = A + static_cast<size_t>(tt) * d;
+            const double vpi = vp[i], wpi = wp[i];
+            double s = 0.0;
+            for (int j = k + 1 + lane; j < d; j += 32) {
+                const double x = row[j] - (vpi * wp[j] + wpi * vp[j]);
+                row[j] = x;
+                s = fma(x, v[j], s);
+            }
+            s = warp_sum(s) * t;
+            if (lane < C) cl.map_shared_rank(p, lane)[i] = s;
+        }
+        cl.sync();
+        // phase 3 (replicated): w = p - (t/2)(p^T v) v becomes the pending update
+        double pv = 0.0;
+        for (int i = k + 1 + tid; i < d; i += nt) pv = fma(p[i], v[i], pv);
+        const double kk = -0.5 * t * block_sum(pv);
+        for (int i = k + 1 + tid; i < d; i += nt) {
+            wp[i] = fma(kk, v[i], p[i]);
+            vp[i] = v[i];
+        }
+        __syncthreads();
+    }
+    // last 2 x 2 block: owners of rows d-2, d-1 publish their entries to rank 0
+    if (d >= 2) {
+        const int k = d - 2;
+        for (int r = k + tid; r < d; r += nt) {
+            if (r % C != rank) continue;
+            const int t = r / C;
+            const double* row = A + static_cast<size_t>(t) * d;
+            double* c0 = cl.map_shared_rank(col, 0);
+            c0[r] = row[k] - (vp[r] * wp[k] + wp[r] * vp[k]);                               // A(r, d-2)
+            if (r == d - 1) c0[d] = row[d - 1] - (vp[r] * wp[d - 1] + wp[r] * vp[d - 1]);  // A(d-1, d-1)
+        }
+    }
+    cl.sync();
+    if (rank == 0 && tid == 0) {
+        const int k = d - 2;
+        diag[k] = col[k];
+        off[k] = col[k + 1];
+        diag[k + 1] = col[d];
+        off[k + 1] = 0.0;
+        tau[k] = 0.0;
+        tau[k + 1] = 0.0;
+    }
+}
+
+// cluster size for the distributed tridiagonalisation, 0 when it does not fit
+int tridiag_cluster_size(int d, size_t* smem) {
+    for (int c = 1; c <= 16; c *= 2) {
+        const size_t nloc = static_cast<size_t>((d + c - 1) / c);
+        const size_t bytes = sizeof(double) * (nloc * d + 5 * static_cast<size_t>(d) + 8);
+        if (bytes <= 200 * 1024) {
+            *smem = bytes;
+            return c;
+        }
+    }
+    return 0;
 }
 
 // ------------------------------------------------------------------ 2. bisection
@@ -426,9 +713,10 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     const size_t total = carve(&w, work, d);
     void* gram_work = static_cast<char*>(work) + total - ((bk_gram_work_bytes(d, d, d) + 255) & ~size_t(255));
     const int mm = d < kTriSmemMaxM + 1 ? d : kTriSmemMaxM + 1;
-    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(d) + static_cast<size_t>(mm) * mm);
-    static const cudaError_t attr = cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         static_cast<int>(sizeof(double) * (2 * kSyevMaxD + (kTriSmemMaxM + 1) * (kTriSmemMaxM + 1))));
+    const size_t smem = sizeof(double) * (4 * static_cast<size_t>(d) + static_cast<size_t>(mm) * mm);
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        tridiag_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(sizeof(double) * (4 * kSyevMaxD + (kTriSmemMaxM + 1) * (kTriSmemMaxM + 1))));
     BK_RET(attr);
     if (d > kSyevMaxD) return static_cast<int>(cudaErrorInvalidValue);
     if (d == 1) {
@@ -439,7 +727,33 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         BK_RET(cudaMemsetAsync(info, 0, 2 * sizeof(int), s));
         return 0;
     }
-    tridiag_kernel<<<1, kTriThreads, smem, s>>>(d, h, ldh, w.a, w.vref, w.tau, w.dg, w.off);
+    size_t csmem = 0;
+    const int C = tridiag_cluster_size(d, &csmem);
+    bool launched = false;
+    if (C > 0) {
+        static const cudaError_t a1 = cudaFuncSetAttribute(tridiag_cluster_kernel,
+                                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 8192);
+        static const cudaError_t a2 =
+            cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        BK_RET(a1);
+        BK_RET(a2);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(C, 1, 1);
+        cfg.blockDim = dim3(kClThreads, 1, 1);
+        cfg.dynamicSmemBytes = csmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr_c[1];
+        attr_c[0].id = cudaLaunchAttributeClusterDimension;
+        attr_c[0].val.clusterDim.x = C;
+        attr_c[0].val.clusterDim.y = 1;
+        attr_c[0].val.clusterDim.z = 1;
+        cfg.attrs = attr_c;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, d, h, ldh, w.vref, w.tau, w.dg, w.off);
+        if (e == cudaSuccess) launched = true;
+        else (void)cudaGetLastError();  // cluster not schedulable: fall back below
+    }
+    if (!launched) tridiag_fused_kernel<<<1, kTriThreads, smem, s>>>(d, h, ldh, w.a, w.vref, w.tau, w.dg, w.off);
     bisect_kernel<<<ceil_div(n_need * 32, 256), 256, 0, s>>>(d, w.dg, w.off, n_need, values, w.e2);
     group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
     invit_kernel<<<ceil_div(n_need * 32, 128), 128, 0, s>>>(d, w.dg, w.off, values, w.gstart, w.ngroups, w.u,

@@ -37,6 +37,13 @@ struct Blk {
 };
 
 #define BKC(call) cuda_check((call), #call)
+// launch + (when profiling) time it as an "other" kernel class
+#define BKO(call)                                \
+    do {                                         \
+        auto _t = prof_begin();                  \
+        BKC(call);                               \
+        prof_end(_t, K_OTHER, 0.0, 0.0);         \
+    } while (0)
 
 // pinned host staging for the per-iteration record and small infos
 struct Pinned {
@@ -230,7 +237,7 @@ private:
         prof_end(t, K_GEMM, 8.0 * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * rows * d * k);
     }
     void copy(int rows, Blk src, int k, Blk dst) {
-        if (k > 0 && rows > 0) BKC(bk_copy_cols_d(rows, src.p, src.ld, k, dst.p, dst.ld, st()));
+        if (k > 0 && rows > 0) BKO(bk_copy_cols_d(rows, src.p, src.ld, k, dst.p, dst.ld, st()));
     }
 
     // host std::mt19937_64 / normal_distribution block (random_block,
@@ -257,7 +264,7 @@ private:
     int proj_ortho(int rows, Blk w, int a, Blk q, int m, Blk out) {
         if (a <= 0) return 0;
         double* ref2 = SMALL_.d();  // a doubles
-        BKC(bk_colnorm2_d(rows, w.p, w.ld, a, ref2, WORK_.p(), st()));
+        BKO(bk_colnorm2_d(rows, w.p, w.ld, a, ref2, WORK_.p(), st()));
         if (m > 0)
             for (int pass = 0; pass < 2; ++pass) {
                 gram(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a);
@@ -339,7 +346,7 @@ private:
                     gemm(rows, out.p, out.ld, kept, c, 1, 1, -1.0, 1.0, v.p, 1);
                 }
             }
-            BKC(bk_colnorm2_d(rows, v.p, 1, 1, nrm2, WORK_.p(), st()));
+            BKO(bk_colnorm2_d(rows, v.p, 1, 1, nrm2, WORK_.p(), st()));
             double h = 0.0;
             BKC(cudaMemcpyAsync(&pin_.rec[3], nrm2, sizeof(double), cudaMemcpyDeviceToHost, stream_));
             sync();
@@ -347,7 +354,7 @@ private:
             const double nrm = std::sqrt(h);
             if (!std::isfinite(nrm)) throw std::runtime_error("orthonormalization: non-finite values");
             if (nrm < kDropTol * std::sqrt(ref2[j])) continue;
-            BKC(bk_axpby_d(rows, 1, 1.0 / nrm, v.p, 1, 0.0, out.at(kept).p, out.ld, st()));
+            BKO(bk_axpby_d(rows, 1, 1.0 / nrm, v.p, 1, 0.0, out.at(kept).p, out.ld, st()));
             ++kept;
         }
         return kept;
@@ -428,7 +435,7 @@ private:
                 spmm(x, k, T2());
                 ax_known = T2();
             }
-            BKC(bk_lincomb_d(n_, k, cfg_.op_c, x.p, x.ld, -1.0, ax_known.p, ax_known.ld, y.p, y.ld, st()));
+            BKO(bk_lincomb_d(n_, k, cfg_.op_c, x.p, x.ld, -1.0, ax_known.p, ax_known.ld, y.p, y.ld, st()));
             return;
         }
         // (A - zeta I)^{-1} = M M^T with M = R^{-1} from the dense Cholesky
@@ -637,7 +644,7 @@ void Engine::solve_sd() {
                 ev = Event::expand;
             }
         }
-        BKC(bk_scale_rows_d(n_, n_old, td, R_.d(), ldT_, T1().p, ldT_, st()));
+        BKO(bk_scale_rows_d(n_, n_old, td, R_.d(), ldT_, T1().p, ldT_, st()));
         meter_.proj_ortho(n_, n_old, xb);
         const int kw = proj_ortho(n_, T1(), n_old, v, xb, v.at(xb));
         if (kw == 0) {
@@ -690,7 +697,7 @@ void Engine::solve_lobpcg() {
             np -= drop;
         }
         // W = T R(:, lock:) orthonormalised against [X, P]
-        BKC(bk_scale_rows_d(n_, active, td, R_.d() + lock, ldT_, T1().p, ldT_, st()));
+        BKO(bk_scale_rows_d(n_, active, td, R_.d() + lock, ldT_, T1().p, ldT_, st()));
         int m = n_now + np;
         meter_.proj_ortho(n_, active, m);
         const int kw = proj_ortho(n_, T1(), active, s, m, s.at(m));
@@ -751,7 +758,7 @@ void Engine::solve_lobpcg() {
         const int ahl = n_now - lock;  // n_now is post-expansion here
         copy(ds, z, n_now, zc);
         copy(ds, z.at(lock), ahl, cz);
-        BKC(bk_zero_rows_d(cz.p, cz.ld, ahl, 0, n_now, st()));
+        BKO(bk_zero_rows_d(cz.p, cz.ld, ahl, 0, n_now, st()));
         const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now));
         meter_.w.ortho_flops += static_cast<int64_t>(ds) * (n_now - lock) * (2 * n_now + (n_now - lock));
         // [X, P] = S ZC
@@ -815,9 +822,9 @@ void Engine::solve_tracemin() {
         // rhs = P_V R; x = 0; p = r = rhs
         copy(n_, {R_.d(), ldT_}, k, cr);
         project(cr);
-        BKC(bk_axpby_d(n_, k, 0.0, cr.p, cr.ld, 0.0, cx.p, cx.ld, st()));
+        BKO(bk_axpby_d(n_, k, 0.0, cr.p, cr.ld, 0.0, cx.p, cx.ld, st()));
         copy(n_, cr, k, cp);
-        BKC(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs, WORK_.p(), st()));
+        BKO(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs, WORK_.p(), st()));
         std::vector<double> h_rs(k);
         BKC(cudaMemcpyAsync(h_rs.data(), rs, k * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         sync();
@@ -844,11 +851,11 @@ void Engine::solve_tracemin() {
             project(cap);
             BKC(bk_coldot_d(n_, cp.p, cp.ld, cap.p, cap.ld, k, pap, WORK_.p(), st()));
             BKC(bk_cg_step1_d(n_, k, rs, pap, act, cx.p, cx.ld, cr.p, cr.ld, cp.p, cp.ld, cap.p, cap.ld, st()));
-            BKC(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs_new, WORK_.p(), st()));
+            BKO(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs_new, WORK_.p(), st()));
             BKC(bk_cg_step2_d(n_, k, rs, rs_new, act, cr.p, cr.ld, cp.p, cp.ld, st()));
         }
         // y = V - delta
-        BKC(bk_lincomb_d(n_, k, 1.0, v.p, v.ld, -1.0, cx.p, cx.ld, T1().p, ldT_, st()));
+        BKO(bk_lincomb_d(n_, k, 1.0, v.p, v.ld, -1.0, cx.p, cx.ld, T1().p, ldT_, st()));
         Event ev = Event::none;
         int ycols = n_now;
         if (d == Decision::expand) {

@@ -1,0 +1,108 @@
+"""Micro-benchmark of the bk_* kernels at config-2 sizes (CUDA events, warm L2
+noted).  Not part of the product; used to iterate on kernel performance."""
+import ctypes as C
+import json
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+
+from paper_2409_05572_b200 import load, workloads as W
+
+L = load()
+f = L.lib
+_D = C.c_void_p
+f.bk_spmm_d.argtypes = [C.c_int, _D, _D, _D, _D, C.c_int, C.c_int, _D, C.c_int, _D]
+f.bk_gram_work_bytes.restype = C.c_size_t
+f.bk_gram_work_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+f.bk_gram_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, _D, _D]
+f.bk_gemm_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int, C.c_double, C.c_double, _D, C.c_int, _D]
+f.bk_syev_work_bytes.restype = C.c_size_t
+f.bk_syev_work_bytes.argtypes = [C.c_int]
+f.bk_syev_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, _D, C.c_int, _D, _D, _D]
+f.bk_chol_work_bytes.restype = C.c_size_t
+f.bk_chol_work_bytes.argtypes = [C.c_int]
+f.bk_chol_drop_d.argtypes = [C.c_int, _D, C.c_int, _D, C.c_double, _D, C.c_int, _D, _D, _D]
+
+p = lambda t: C.c_void_p(t.data_ptr())
+S = lambda: C.c_void_p(torch.cuda.current_stream().cuda_stream)
+only = sys.argv[1:] if len(sys.argv) > 1 else None
+
+
+def timeit(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+out = {}
+n = 262144
+if not only or "gram" in only:
+    for a, b in [(288, 288), (192, 96), (96, 96), (96, 1)]:
+        x = torch.randn(n, 344, dtype=torch.float64, device="cuda")
+        y = torch.randn(n, 344, dtype=torch.float64, device="cuda")
+        c = torch.zeros(a, b, dtype=torch.float64, device="cuda")
+        ws = torch.empty(f.bk_gram_work_bytes(n, a, b) // 8 + 1, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: f.bk_gram_d(n, p(x), 344, a, p(y), 344, b, p(c), b, p(ws), S()))
+        out[f"gram_{a}x{b}"] = {"ms": ms, "tflops": 2 * n * a * b / ms / 1e9}
+        ref = torch.matmul(x[:, :a].t(), y[:, :b])
+        ms2 = timeit(lambda: torch.matmul(x[:, :a].t(), y[:, :b]))
+        out[f"gram_{a}x{b}"]["cublas_tflops"] = 2 * n * a * b / ms2 / 1e9
+        out[f"gram_{a}x{b}"]["maxerr"] = float((c - ref).abs().max())
+if not only or "gemm" in only:
+    for d, k in [(288, 192), (288, 96), (192, 96), (96, 96)]:
+        x = torch.randn(n, 344, dtype=torch.float64, device="cuda")
+        cm = torch.randn(d, k, dtype=torch.float64, device="cuda")
+        y = torch.zeros(n, 344, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: f.bk_gemm_d(n, p(x), 344, d, p(cm), k, k, 1.0, 0.0, p(y), 344, S()))
+        ms2 = timeit(lambda: torch.matmul(x[:, :d], cm))
+        out[f"gemm_{d}x{k}"] = {"ms": ms, "tflops": 2 * n * d * k / ms / 1e9, "cublas_tflops": 2 * n * d * k / ms2 / 1e9}
+if not only or "syev" in only:
+    for d, need in [(288, 96), (192, 96), (288, 288), (40, 40), (83, 69)]:
+        rng = np.random.default_rng(d)
+        q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+        lam = np.sort(rng.uniform(0, 12, d))
+        h = torch.as_tensor((q * lam) @ q.T, device="cuda")
+        vals = torch.zeros(d, dtype=torch.float64, device="cuda")
+        z = torch.zeros(d, d, dtype=torch.float64, device="cuda")
+        ws = torch.empty(f.bk_syev_work_bytes(d) // 8 + 1, dtype=torch.float64, device="cuda")
+        info = torch.zeros(4, dtype=torch.int32, device="cuda")
+        hh = h.clone()
+        ms = timeit(lambda: (hh.copy_(h), f.bk_syev_d(d, p(hh), d, need, p(vals), p(z), d, p(ws), p(info), S())), reps=10)
+        out[f"syev_{d}_{need}"] = {"ms": ms}
+if not only or "chol" in only:
+    for a in [96, 192, 288]:
+        w = torch.randn(4096, a, dtype=torch.float64, device="cuda")
+        g = w.t() @ w
+        r2 = (w * w).sum(0)
+        m = torch.zeros(a, a, dtype=torch.float64, device="cuda")
+        info = torch.zeros(4, dtype=torch.int32, device="cuda")
+        ws = torch.empty(f.bk_chol_work_bytes(a) // 8 + 1, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: f.bk_chol_drop_d(a, p(g), a, p(r2), 1e-8, p(m), a, p(info), p(ws), S()))
+        out[f"chol_{a}"] = {"ms": ms}
+if not only or "spmm" in only:
+    wl = W.config2("fix", x0=False)
+    a = L.from_csr(wl.n, wl.row_ptr, wl.col, wl.val)
+    # full CSR on device via the library's own upload path is internal; rebuild here
+    import scipy.sparse as sp
+    lo = sp.csr_matrix((wl.val, wl.col, wl.row_ptr), shape=(wl.n, wl.n))
+    full = (lo + lo.T - sp.diags(lo.diagonal())).tocsr()
+    full.sort_indices()
+    rp = torch.as_tensor(full.indptr.astype(np.int32), device="cuda")
+    ci = torch.as_tensor(full.indices.astype(np.int32), device="cuda")
+    vv = torch.as_tensor(full.data, device="cuda")
+    for k in [69, 96, 192, 288]:
+        x = torch.randn(wl.n, 344, dtype=torch.float64, device="cuda")
+        y = torch.zeros(wl.n, 344, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: f.bk_spmm_d(wl.n, p(rp), p(ci), p(vv), p(x), 344, k, p(y), 344, S()))
+        bytes_ = 12 * full.nnz + 4 * (wl.n + 1) + 16 * wl.n * k
+        out[f"spmm_k{k}"] = {"ms": ms, "gbs": bytes_ / ms / 1e6}
+print(json.dumps(out, indent=1))
