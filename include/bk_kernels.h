@@ -148,6 +148,18 @@ BK_API int bk_cg_step1_d(int n, int k, const double* rs, const double* pap, int*
 BK_API int bk_cg_step2_d(int n, int k, double* rs, const double* rs_new, const int* active,
                          const double* r, int ldr, double* p, int ldp, void* stream);
 
+/* device-side CGS2 column step (the exact fallback of K4, kernel.cpp:83-87):
+ * given nrm2 = ||v||^2 after the projections and ref2 = ||w_j||^2 before them,
+ * keep v when sqrt(nrm2) >= drop * sqrt(ref2) (and ref2 > 0): write v / ||v||
+ * into column counter[0] of out and increment counter[0].  No host sync. */
+BK_API int bk_cgs2_commit_d(int n, const double* v, const double* nrm2, const double* ref2, double drop,
+                            double* out, int ldo, int* counter, void* stream);
+
+/* host-only hook: nblocks consecutive random blocks (sizes[i] values each) from
+ * the solver's per-solve normal stream; bit-identical to drawing each block
+ * with a fresh std::normal_distribution over one std::mt19937_64(seed) */
+BK_API int bk_host_normal_blocks(uint64_t seed, const int* sizes, int nblocks, double* out);
+
 /* host-only hook (no device use): the product's strategy state machine driven
  * over a residual sequence, for CPU tests of decide() parity */
 BK_API int bk_host_decide_sequence(int kind, int j_e, int j_s, double mu, int j_p, int j_warm,

@@ -570,6 +570,17 @@ BEIG_API int orc_resolve_config(const beig_solver_config* cfg, int solver, const
     });
 }
 
+// consecutive random blocks from one engine, a fresh distribution per block
+BEIG_API void orc_random_blocks(uint64_t seed, const int* sizes, int nblocks, double* out) {
+    std::mt19937_64 rng(seed);
+    size_t off = 0;
+    for (int b = 0; b < nblocks; ++b) {
+        auto m = orc::random_block<double>(sizes[b], 1, rng);
+        std::memcpy(out + off, m.a.data(), m.a.size() * sizeof(double));
+        off += m.a.size();
+    }
+}
+
 // std::mt19937_64 + std::normal_distribution block (reference random_block)
 BEIG_API void orc_random_block(int rows, int cols, uint64_t seed, double* out) {
     std::mt19937_64 rng(seed);

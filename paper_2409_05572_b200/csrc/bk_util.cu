@@ -467,3 +467,33 @@ extern "C" int bk_cg_step2_d(int n, int k, double* rs, const double* rs_new, con
     cg_commit_rs<<<ceil_div(k, 256), 256, 0, s>>>(k, rs, rs_new, active);
     BK_LAUNCHED();
 }
+
+namespace bk {
+namespace {
+__global__ void cgs2_commit_kernel(int n, const double* __restrict__ v, const double* __restrict__ nrm2,
+                                   const double* __restrict__ ref2, double drop, double* __restrict__ out, int ldo,
+                                   int* __restrict__ counter) {
+    // every block evaluates the (identical) decision; block 0 bumps the counter
+    const double r2 = *ref2, v2 = *nrm2;
+    const bool keep = r2 > 0.0 && isfinite(v2) && sqrt(v2) >= drop * sqrt(r2);
+    if (!keep) return;
+    const int col = *counter;
+    const double inv = 1.0 / sqrt(v2);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[static_cast<size_t>(i) * ldo + col] = v[i] * inv;
+}
+__global__ void counter_bump(const double* __restrict__ nrm2, const double* __restrict__ ref2, double drop,
+                             int* __restrict__ counter) {
+    const double r2 = *ref2, v2 = *nrm2;
+    if (r2 > 0.0 && isfinite(v2) && sqrt(v2) >= drop * sqrt(r2)) *counter += 1;
+}
+}  // namespace
+}  // namespace bk
+
+extern "C" int bk_cgs2_commit_d(int n, const double* v, const double* nrm2, const double* ref2, double drop,
+                                double* out, int ldo, int* counter, void* stream) {
+    const cudaStream_t s = as_stream(stream);
+    cgs2_commit_kernel<<<elem_grid(n), 256, 0, s>>>(n, v, nrm2, ref2, drop, out, ldo, counter);
+    counter_bump<<<1, 1, 0, s>>>(nrm2, ref2, drop, counter);
+    BK_LAUNCHED();
+}

@@ -21,6 +21,7 @@
 #include <limits>
 
 #include "host.hpp"
+#include "rng.hpp"
 
 namespace b2 {
 
@@ -36,7 +37,13 @@ struct Blk {
     Blk at(int c) const { return {p + c, ld}; }
 };
 
-#define BKC(call) cuda_check((call), #call)
+thread_local double g_host_call_s = 0.0;  // BLOCKEIG_TIMING: host time inside CUDA / bk_* calls
+#define BKC(call)                                                                                          \
+    do {                                                                                                   \
+        const auto _h0 = std::chrono::steady_clock::now();                                                 \
+        cuda_check((call), #call);                                                                         \
+        g_host_call_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - _h0).count(); \
+    } while (0)
 // launch + (when profiling) time it as an "other" kernel class
 #define BKO(call)                                \
     do {                                         \
@@ -165,8 +172,38 @@ private:
     Blk T2() const { return {T2_.d(), ldT_}; }
 
     void sync() {
+        const auto t0 = std::chrono::steady_clock::now();
         BKC(cudaStreamSynchronize(stream_));
+        sync_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        ++syncs_;
+        if (cfg_.profile) {
+            // device-side view of the host round trip: from the previous segment's
+            // resume marker to this segment's first kernel (host think + launch time)
+            cudaEvent_t resume = take_event();
+            BKC(cudaEventRecord(resume, stream_));
+            if (resume_ev_ && !pending_.empty()) {
+                float ms = 0.f;
+                BKC(cudaEventElapsedTime(&ms, resume_ev_, pending_.front().a));
+                bubble_ms_ += ms;
+            }
+            prof_resolve();
+            if (resume_ev_) ev_pool_.push_back(resume_ev_);
+            resume_ev_ = resume;
+            return;
+        }
         prof_resolve();
+    }
+    cudaEvent_t resume_ev_ = nullptr;
+    double bubble_ms_ = 0.0;
+    double sync_wait_s_ = 0.0;
+    int64_t syncs_ = 0;
+    // BLOCKEIG_TIMING: wall time per loop phase (host view, includes waits)
+    double phase_s_[8] = {};
+    std::chrono::steady_clock::time_point phase_t_ = std::chrono::steady_clock::now();
+    void mark(int ph) {
+        const auto now = std::chrono::steady_clock::now();
+        phase_s_[ph] += std::chrono::duration<double>(now - phase_t_).count();
+        phase_t_ = now;
     }
 
     // ---- optional per-kernel-class CUDA-event timing (ext->profile)
@@ -201,7 +238,8 @@ private:
         pending_.push_back({cls, a, b, bytes, flops});
     }
     void prof_resolve() {
-        for (auto& p : pending_) {
+        for (size_t i = 0; i < pending_.size(); ++i) {
+            auto& p = pending_[i];
             float ms = 0.f;
             BKC(cudaEventElapsedTime(&ms, p.a, p.b));
             auto& k = kstats_[p.cls];
@@ -209,11 +247,19 @@ private:
             k.ms += ms;
             k.bytes += p.bytes;
             k.flops += p.flops;
+            if (i + 1 < pending_.size()) {  // device idle / unprofiled time before the next class
+                float gap = 0.f;
+                BKC(cudaEventElapsedTime(&gap, p.b, pending_[i + 1].a));
+                gap_ms_[pending_[i + 1].cls] += gap;
+            }
+        }
+        for (auto& p : pending_) {
             ev_pool_.push_back(p.a);
             ev_pool_.push_back(p.b);
         }
         pending_.clear();
     }
+    double gap_ms_[K_CLASSES] = {};
 
     // K1: algorithmic bytes nnz*12 + (n+1)*4 + 2*n*k*8
     void spmm(Blk x, int k, Blk y) {
@@ -245,11 +291,15 @@ private:
     // uploaded into dst (row-major)
     void random_block(int cols, Blk dst) {
         if (cols <= 0) return;
-        std::normal_distribution<double> dist(0.0, 1.0);
+        const auto t0 = std::chrono::steady_clock::now();
         std::vector<double> h(static_cast<size_t>(n_) * cols);
-        for (auto& x : h) x = dist(rng_);
+        rng_.take(h.data(), h.size());
         upload_colmajor(h.data(), cols, dst);
+        rng_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        rng_cols_ += cols;
     }
+    double rng_s_ = 0.0;
+    int64_t rng_cols_ = 0;
     void upload_colmajor(const double* h, int cols, Blk dst) {
         const size_t bytes = static_cast<size_t>(n_) * cols * sizeof(double);
         if (stage_.bytes() < bytes) stage_.alloc(bytes);
@@ -324,40 +374,36 @@ private:
 
     // exact column CGS2 (kernel.cpp:71-86) for blocks whose Cholesky pivots
     // were not decisive; w already carries the external projection
+    // The external projection (two block passes against q) is already applied
+    // to w, so only the in-block Gram-Schmidt remains: two passes against the
+    // columns accepted so far, then the drop test against the ORIGINAL norm —
+    // decided on the device (bk_cgs2_commit_d), one host sync at the end.
+    // `out` is zeroed first, so projecting against its first j columns (kept <= j)
+    // is exact without knowing the kept count on the host.
     int cgs2_fallback(int rows, Blk w, int a, Blk q, int m, Blk out) {
+        (void)q;
+        (void)m;
         ++fallbacks_;
-        std::vector<double> ref2(a);
-        BKC(cudaMemcpyAsync(ref2.data(), SMALL_.d(), a * sizeof(double), cudaMemcpyDeviceToHost, stream_));
-        sync();
+        const double* ref2 = SMALL_.d();  // set by proj_ortho
         Blk v{VEC_.d(), 1};
         double* c = COEF_.d();
         double* nrm2 = SMALL_.d() + tcap_;
-        int kept = 0;
+        int* counter = INFO_.as<int>() + 32;
+        BKO(bk_zero_rows_d(out.p, out.ld, a, 0, rows, st()));
+        BKC(cudaMemsetAsync(counter, 0, sizeof(int), stream_));
         for (int j = 0; j < a; ++j) {
-            if (ref2[j] == 0.0) continue;
             copy(rows, w.at(j), 1, v);
-            for (int pass = 0; pass < 2; ++pass) {
-                if (m > 0) {
-                    gram(rows, q.p, q.ld, m, v.p, 1, 1, c, 1);
-                    gemm(rows, q.p, q.ld, m, c, 1, 1, -1.0, 1.0, v.p, 1);
+            if (j > 0)
+                for (int pass = 0; pass < 2; ++pass) {
+                    gram(rows, out.p, out.ld, j, v.p, 1, 1, c, 1);
+                    gemm(rows, out.p, out.ld, j, c, 1, 1, -1.0, 1.0, v.p, 1);
                 }
-                if (kept > 0) {
-                    gram(rows, out.p, out.ld, kept, v.p, 1, 1, c, 1);
-                    gemm(rows, out.p, out.ld, kept, c, 1, 1, -1.0, 1.0, v.p, 1);
-                }
-            }
             BKO(bk_colnorm2_d(rows, v.p, 1, 1, nrm2, WORK_.p(), st()));
-            double h = 0.0;
-            BKC(cudaMemcpyAsync(&pin_.rec[3], nrm2, sizeof(double), cudaMemcpyDeviceToHost, stream_));
-            sync();
-            h = pin_.rec[3];
-            const double nrm = std::sqrt(h);
-            if (!std::isfinite(nrm)) throw std::runtime_error("orthonormalization: non-finite values");
-            if (nrm < kDropTol * std::sqrt(ref2[j])) continue;
-            BKO(bk_axpby_d(rows, 1, 1.0 / nrm, v.p, 1, 0.0, out.at(kept).p, out.ld, st()));
-            ++kept;
+            BKO(bk_cgs2_commit_d(rows, v.p, nrm2, ref2 + j, kDropTol, out.p, out.ld, counter, st()));
         }
-        return kept;
+        BKC(cudaMemcpyAsync(pin_.info + 13, counter, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        sync();
+        return pin_.info[13];
     }
 
     // count fresh orthonormal random columns orthogonal to q = [vs | acc],
@@ -468,6 +514,17 @@ private:
         out_.rr_flops = meter_.rr_flops;
         out_.cgs2_fallbacks = fallbacks_;
         out_.max_jacobi_sweeps = max_sweeps_;
+        if (std::getenv("BLOCKEIG_TIMING"))
+            std::fprintf(stderr,
+                         "[blockeig] syncs=%lld host_wait_in_sync=%.3fs host_in_calls=%.3fs phases: other=%.3f "
+                         "resid=%.3f W=%.3f rr=%.3f hl=%.3f lift=%.3f tail=%.3f expand=%.3f\n",
+                         static_cast<long long>(syncs_), sync_wait_s_, g_host_call_s, phase_s_[0], phase_s_[1],
+                         phase_s_[2], phase_s_[3], phase_s_[4], phase_s_[5], phase_s_[6], phase_s_[7]);
+        if (std::getenv("BLOCKEIG_TIMING"))
+            std::fprintf(stderr, "[blockeig] device gaps before class (ms): spmm=%.1f gram=%.1f gemm=%.1f syev=%.1f "
+                         "chol=%.1f resid=%.1f other=%.1f; post-sync bubbles %.1f ms; host rng %.3fs for %lld cols\n",
+                         gap_ms_[0], gap_ms_[1], gap_ms_[2], gap_ms_[3], gap_ms_[4], gap_ms_[5], gap_ms_[6],
+                         bubble_ms_, rng_s_, static_cast<long long>(rng_cols_));
         for (int c = 0; c < K_CLASSES; ++c) out_.kstats[c] = kstats_[c];
     }
 
@@ -481,7 +538,7 @@ private:
     SolverConfig cfg_;
     SolverKind kind_;
     int n_;
-    std::mt19937_64 rng_;
+    NormalPairStream rng_;  // the reference's per-solve mt19937_64 normal stream, produced ahead
     const DeviceCsr* csr_ = nullptr;
     cudaStream_t stream_ = nullptr;
     int tcap_ = 0, dcap_ = 0, ldS_ = 0, ldT_ = 0, ldH_ = 0;
@@ -682,7 +739,9 @@ void Engine::solve_lobpcg() {
     for (int j = 1; j <= cfg_.max_iters; ++j) {
         meter_.begin_iteration();
         Blk s = S(cur_);
+        mark(0);
         const Rep rep = residual(s, n_now, n_ev);
+        mark(1);
         const int lock = std::min(rep.converged, n_now - 1);
         if (rep.converged >= n_ev) {
             push(j, rep.overall, n_now, Event::none, lock);
@@ -700,7 +759,9 @@ void Engine::solve_lobpcg() {
         BKO(bk_scale_rows_d(n_, active, td, R_.d() + lock, ldT_, T1().p, ldT_, st()));
         int m = n_now + np;
         meter_.proj_ortho(n_, active, m);
+        mark(0);
         const int kw = proj_ortho(n_, T1(), active, s, m, s.at(m));
+        mark(2);
         if (kw == 0) {
             push(j, rep.overall, n_now, Event::none, lock);
             return finish(Status::stagnated, s, n_ev);
@@ -751,18 +812,24 @@ void Engine::solve_lobpcg() {
                 ds = m + kw;
             }
         }
+        mark(7);
         // Rayleigh-Ritz on S = [X, P, W]; A X is still in AS(:, 0:n_old)
+        mark(0);
         rayleigh_ritz(s, ds, n_old, n_now);
+        mark(3);
         // HL trick (solvers.cpp:187-196) in coefficient space:
         // ZC = [Z(:, :n_now) | orth(Zp)], Zp = Z(:, lock:n_now) with rows < n_now zeroed
         const int ahl = n_now - lock;  // n_now is post-expansion here
         copy(ds, z, n_now, zc);
         copy(ds, z.at(lock), ahl, cz);
         BKO(bk_zero_rows_d(cz.p, cz.ld, ahl, 0, n_now, st()));
+        mark(0);
         const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now));
+        mark(4);
         meter_.w.ortho_flops += static_cast<int64_t>(ds) * (n_now - lock) * (2 * n_now + (n_now - lock));
         // [X, P] = S ZC
         lift(s, ds, zc.p, zc.ld, n_now + pk, S(1 - cur_));
+        mark(5);
         cur_ ^= 1;
         np = pk;
         if (d == Decision::shrink) {
@@ -779,6 +846,7 @@ void Engine::solve_lobpcg() {
         }
         if (ev == Event::none && lock > prev_lock) ev = Event::lock;
         push(j, rep.overall, n_now, ev, lock);
+        mark(6);
         prev_lock = lock;
     }
     finish(Status::max_iters, S(cur_), n_ev);

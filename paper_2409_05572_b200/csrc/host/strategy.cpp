@@ -108,3 +108,25 @@ extern "C" int bk_host_decide_sequence(int kind, int j_e, int j_s, double mu, in
         return 1;
     }
 }
+
+#include <cstring>
+
+#include "rng.hpp"
+
+// host-only hook: consecutive random blocks (sizes[i] values each) from one
+// per-solve normal stream, as the solver draws them — CPU test of bit parity
+// with std::normal_distribution over std::mt19937_64 (the reference's
+// random_block, proj/src/kernel.cpp:166-172)
+extern "C" int bk_host_normal_blocks(uint64_t seed, const int* sizes, int nblocks, double* out) {
+    try {
+        b2::NormalPairStream s(seed, 1024);
+        size_t off = 0;
+        for (int b = 0; b < nblocks; ++b) {
+            s.take(out + off, static_cast<size_t>(sizes[b]));
+            off += static_cast<size_t>(sizes[b]);
+        }
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}

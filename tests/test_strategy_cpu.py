@@ -122,3 +122,20 @@ def test_product_matches_oracle_random(oracle, both, seed):
                   j_p=int(rng.integers(1, 12)), j_warm=int(rng.integers(0, 8)), r_warm=float(10 ** rng.uniform(-6, 0)))
         outs = [run(s, r, 10, 20, 20, 0) for _, run in runners]
         assert outs[0] == outs[1], kind
+
+
+def test_normal_stream_bit_identical(oracle, product_path):
+    # the product's background normal stream == std::normal_distribution per
+    # block over one std::mt19937_64 (reference random_block, kernel.cpp:166-172),
+    # including the discarded cached value after odd-sized blocks
+    sizes = np.array([7, 1, 64, 33, 2, 5000, 3], dtype=np.int32)
+    total = int(sizes.sum())
+    got = np.zeros(total)
+    want = np.zeros(total)
+    pf = C.CDLL(product_path).bk_host_normal_blocks
+    pf.argtypes = [C.c_uint64, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double)]
+    assert pf(11, sizes.ctypes.data_as(C.POINTER(C.c_int)), len(sizes), got.ctypes.data_as(C.POINTER(C.c_double))) == 0
+    of = oracle.lib.orc_random_blocks
+    of.argtypes = [C.c_uint64, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double)]
+    of(11, sizes.ctypes.data_as(C.POINTER(C.c_int)), len(sizes), want.ctypes.data_as(C.POINTER(C.c_double)))
+    assert np.array_equal(got, want)
