@@ -45,6 +45,11 @@ BK_API int bk_spmm_z(int n, const int32_t* row_ptr, const int32_t* col, const do
 BK_API size_t bk_gram_work_bytes(int n, int a, int b);
 BK_API int bk_gram_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b,
                      double* c, int ldc, void* work, void* stream);
+/* symmetric-result variant for the Rayleigh-Ritz matrix H = S^T (A S) (d x d):
+ * only the 96 x 96 tiles on and above the diagonal are computed; the strictly
+ * lower tiles are mirrored (the reference symmetrises, kernel.cpp:97) */
+BK_API int bk_gram_sym_d(int n, const double* x, int ldx, const double* y, int ldy, int d, double* c,
+                         int ldc, void* work, void* stream);
 
 /* ---- K3 update: Y = alpha X C + beta Y, X n x d, C d x k (row-major, ldc) ----
  * (replaces s*e.vectors, proj/src/rr.cpp:13; s*z1 / s*o.q, proj/src/solvers.cpp:195;

@@ -52,7 +52,7 @@ __device__ __forceinline__ void load_rows(double* dst, int pitch, const double* 
 }
 
 // ------------------------------------------------------------------ Gram
-template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16>
+template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16, bool SYM = false>
 __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double* __restrict__ x, int ldx, int a,
                                                              const double* __restrict__ y, int ldy, int b,
                                                              double* __restrict__ out, int ldo, int rows_per_split) {
@@ -64,7 +64,18 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
     double* ys = smem + STAGES * TK * PX;   // STAGES x TK x PY
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int i0 = blockIdx.x * TM, j0 = blockIdx.y * TN;
+    int ti = blockIdx.x, tj = blockIdx.y;
+    if constexpr (SYM) {  // blockIdx.x enumerates the upper-triangular tile pairs ti <= tj
+        const int nt = ceil_div(a, TM);
+        int rem = blockIdx.x;
+        ti = 0;
+        while (rem >= nt - ti) {
+            rem -= nt - ti;
+            ++ti;
+        }
+        tj = ti + rem;
+    }
+    const int i0 = ti * TM, j0 = tj * TN;
     const int split = blockIdx.z;
     const int r_begin = split * rows_per_split;
     const int r_end = min(n, r_begin + rows_per_split);
@@ -124,15 +135,17 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
         }
 }
 
-// C[i][j] = sum_s work[s][i][j] in split order
+// C[i][j] = sum_s work[s][i][j] in split order; with `sym`, entries of the
+// strictly-lower tiles (never computed) are mirrored from the upper ones
 __global__ void gram_reduce(int splits, int a, int b, const double* __restrict__ work, double* __restrict__ c,
-                            int ldc) {
+                            int ldc, int sym, int tile) {
     const int64_t total = static_cast<int64_t>(a) * b;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(e / b), j = static_cast<int>(e % b);
+        const int64_t src = sym && i / tile > j / tile ? static_cast<int64_t>(j) * b + i : e;
         double s = 0.0;
-        for (int p = 0; p < splits; ++p) s += work[static_cast<size_t>(p) * total + e];
+        for (int p = 0; p < splits; ++p) s += work[static_cast<size_t>(p) * total + src];
         c[static_cast<size_t>(i) * ldc + j] = s;
     }
 }
@@ -146,7 +159,9 @@ struct GramPlan {
 
 GramPlan gram_plan(int n, int a, int b) {
     const int tiles = ceil_div(a, GTM) * ceil_div(b, GTN);
-    int splits = ceil_div(2 * kSMs, tiles);
+    // one wave: 2 resident CTAs per SM (register / shared-memory limited), so
+    // tiles x splits must not exceed 2 x 148 or a straggler wave doubles the time
+    int splits = max(1, (2 * kSMs) / tiles);
     splits = max(1, min(splits, ceil_div(n, 256)));  // >= 256 rows per split
     splits = min(splits, 96);
     int rps = ceil_div(n, splits);
@@ -243,9 +258,45 @@ cudaError_t prep(K kernel, size_t smem) {
 using namespace bk;
 
 extern "C" size_t bk_gram_work_bytes(int n, int a, int b) {
-    const GramPlan p = gram_plan(max(n, 1), max(a, 1), max(b, 1));
+    // enough for any tile count (the symmetric variant launches fewer tiles and
+    // therefore more splits): the one-tile plan has the most splits
+    const GramPlan p = gram_plan(max(n, 1), 1, 1);
     return static_cast<size_t>(p.splits) * max(a, 1) * max(b, 1) * sizeof(double);
 }
+
+namespace bk {
+namespace {
+template <bool SYM>
+int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
+                void* work, cudaStream_t s) {
+    auto k16 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, true, SYM>;
+    auto k8 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, false, SYM>;
+    static const cudaError_t a1 = prep(k16, kGramSmem);
+    static const cudaError_t a2 = prep(k8, kGramSmem);
+    BK_RET(a1);
+    BK_RET(a2);
+    const int nt = ceil_div(a, GTM);
+    const int tiles = SYM ? nt * (nt + 1) / 2 : nt * ceil_div(b, GTN);
+    // plan with the number of tiles actually launched
+    const GramPlan p = gram_plan(n, SYM ? tiles * GTM : a, SYM ? GTN : b);
+    const dim3 grid(SYM ? tiles : nt, SYM ? 1 : ceil_div(b, GTN), p.splits);
+    auto w = static_cast<double*>(work);
+    const bool direct = p.splits == 1 && !SYM;  // a single split writes C directly
+    double* dst = direct ? c : w;
+    const int ldo = direct ? ldc : b;
+    if (aligned16(x, ldx) && aligned16(y, ldy))
+        k16<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
+    else
+        k8<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
+    if (!direct) {
+        const int64_t total = static_cast<int64_t>(a) * b;
+        gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
+            p.splits, a, b, w, c, ldc, SYM ? 1 : 0, GTM);
+    }
+    BK_LAUNCHED();
+}
+}  // namespace
+}  // namespace bk
 
 extern "C" int bk_gram_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
                          int ldc, void* work, void* stream) {
@@ -255,28 +306,15 @@ extern "C" int bk_gram_d(int n, const double* x, int ldx, int a, const double* y
         for (int i = 0; i < a; ++i) BK_RET(cudaMemsetAsync(c + static_cast<size_t>(i) * ldc, 0, sizeof(double) * b, s));
         return 0;
     }
-    auto k16 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, true>;
-    auto k8 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, false>;
-    static const cudaError_t a1 = prep(k16, kGramSmem);
-    static const cudaError_t a2 = prep(k8, kGramSmem);
-    BK_RET(a1);
-    BK_RET(a2);
-    const GramPlan p = gram_plan(n, a, b);
-    const dim3 grid(ceil_div(a, GTM), ceil_div(b, GTN), p.splits);
-    auto w = static_cast<double*>(work);
-    // a single split writes C directly
-    double* dst = p.splits == 1 ? c : w;
-    const int ldo = p.splits == 1 ? ldc : b;
-    if (aligned16(x, ldx) && aligned16(y, ldy))
-        k16<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
-    else
-        k8<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
-    if (p.splits > 1) {
-        const int64_t total = static_cast<int64_t>(a) * b;
-        gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
-            p.splits, a, b, w, c, ldc);
-    }
-    BK_LAUNCHED();
+    return gram_launch<false>(n, x, ldx, a, y, ldy, b, c, ldc, work, s);
+}
+
+extern "C" int bk_gram_sym_d(int n, const double* x, int ldx, const double* y, int ldy, int d, double* c, int ldc,
+                             void* work, void* stream) {
+    if (d <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    if (n <= 0) return bk_gram_d(n, x, ldx, d, y, ldy, d, c, ldc, work, stream);
+    return gram_launch<true>(n, x, ldx, d, y, ldy, d, c, ldc, work, s);
 }
 
 extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,

@@ -427,7 +427,12 @@ private:
     void rayleigh_ritz(Blk s, int d, int as_from, int n_need = 0) {
         meter_.rr(n_, d);
         spmm(s.at(as_from), d - as_from, AS().at(as_from));
-        gram(n_, s.p, s.ld, d, AS_.d(), ldS_, d, H_.d(), ldH_);
+        {  // H = S^T (A S): upper tiles only, mirrored (symmetrised by the eigensolver anyway)
+            auto tg = prof_begin();
+            BKC(bk_gram_sym_d(n_, s.p, s.ld, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
+            // algorithmic flops of a symmetric Gram: n d (d + 1)
+            prof_end(tg, K_GRAM, 8.0 * n_ * 2 * d, 1.0 * n_ * d * (d + 1.0));
+        }
         int* info = INFO_.as<int>() + 8;
         auto ts = prof_begin();
         BKC(bk_syev_d(d, H_.d(), ldH_, n_need > 0 ? n_need : d, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
