@@ -153,6 +153,11 @@ BK_API int bk_cg_step1_d(int n, int k, const double* rs, const double* pap, int*
 BK_API int bk_cg_step2_d(int n, int k, double* rs, const double* rs_new, const int* active,
                          const double* r, int ldr, double* p, int ldp, void* stream);
 
+/* Newton-Schulz re-orthonormalisation coefficients: m = (3I - g)/2 (a x a), so
+ * that W m is orthonormal to O(||W^T W - I||^2).  Second pass of CholQR2 and
+ * the final polish of the eigenvector block (no sequential factorisation). */
+BK_API int bk_ns_coeff_d(int a, const double* g, int ldg, double* m, int ldm, void* stream);
+
 /* device-side CGS2 column step (the exact fallback of K4, kernel.cpp:83-87):
  * given nrm2 = ||v||^2 after the projections and ref2 = ||w_j||^2 before them,
  * keep v when sqrt(nrm2) >= drop * sqrt(ref2) (and ref2 > 0): write v / ||v||

@@ -24,9 +24,13 @@ __global__ void __launch_bounds__(256) spmm_d_kernel(int n, const int32_t* __res
                                                       const double* __restrict__ val,
                                                       const double* __restrict__ x, int ldx, int k,
                                                       double* __restrict__ y, int ldy) {
-    const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // each CTA sweeps a contiguous chunk of rows, its warps interleaved within
+    // the chunk, so X rows shared by neighbouring rows (stencil offsets +-1,
+    // +-grid line) are re-read from L1 instead of L2
+    const int rpc = ceil_div(n, gridDim.x);
+    const int r_begin = blockIdx.x * rpc, r_end = min(n, r_begin + rpc);
+    for (int row = r_begin + warp; row < r_end; row += nw) {
         const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
         for (int c0 = 0; c0 < k; c0 += 32 * VPL) {
             double acc[VPL];
@@ -41,7 +45,27 @@ __global__ void __launch_bounds__(256) spmm_d_kernel(int n, const int32_t* __res
                     my_v = __ldg(val + p);
                 }
                 const int cnt = min(32, e - pb);
-                for (int t = 0; t < cnt; ++t) {
+                // 4 nonzeros per step: all their X-row gathers are issued before
+                // any is consumed (memory-level parallelism; the kernel is
+                // latency-bound otherwise).  Accumulation order is unchanged.
+                constexpr int G = 4;
+                int t = 0;
+                for (; t + G <= cnt; t += G) {
+                    double xv[G][VPL], vv[G];
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const int c = __shfl_sync(0xffffffffu, my_c, t + q);
+                        vv[q] = __shfl_sync(0xffffffffu, my_v, t + q);
+                        const double* xr = x + static_cast<size_t>(c) * ldx + c0 + lane;
+#pragma unroll
+                        for (int u = 0; u < VPL; ++u) xv[q][u] = c0 + lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < G; ++q)
+#pragma unroll
+                        for (int u = 0; u < VPL; ++u) acc[u] = fma(vv[q], xv[q][u], acc[u]);
+                }
+                for (; t < cnt; ++t) {
                     const int c = __shfl_sync(0xffffffffu, my_c, t);
                     const double v = __shfl_sync(0xffffffffu, my_v, t);
                     const double* xr = x + static_cast<size_t>(c) * ldx + c0 + lane;
@@ -104,6 +128,84 @@ __global__ void __launch_bounds__(256) spmm_z_kernel(int n, const int32_t* __res
     }
 }
 
+// Vectorised variant for even k and 16-byte aligned X / Y rows: each lane owns
+// pairs of columns (double2), and the (col, val) pairs of up to 8 nonzeros are
+// fetched first so all of a row's X-row gathers are in flight together.
+template <int VPL2>
+__global__ void __launch_bounds__(256) spmm_d2_kernel(int n, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ x, int ldx, int k,
+                                                       double* __restrict__ y, int ldy) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int k2 = k >> 1;  // column pairs
+    const int ldx2 = ldx >> 1, ldy2 = ldy >> 1;
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+    double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
+    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
+        for (int c0 = 0; c0 < k2; c0 += 32 * VPL2) {
+            double2 acc[VPL2];
+#pragma unroll
+            for (int u = 0; u < VPL2; ++u) acc[u] = make_double2(0.0, 0.0);
+            for (int pb = s; pb < e; pb += 32) {
+                const int p = pb + lane;
+                int my_c = 0;
+                double my_v = 0.0;
+                if (p < e) {
+                    my_c = __ldg(ci + p);
+                    my_v = __ldg(val + p);
+                }
+                const int cnt = min(32, e - pb);
+                int t = 0;
+                for (; t + 8 <= cnt; t += 8) {
+                    int cc[8];
+                    double vv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        cc[q] = __shfl_sync(0xffffffffu, my_c, t + q);
+                        vv[q] = __shfl_sync(0xffffffffu, my_v, t + q);
+                    }
+                    double2 xv[8][VPL2];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int u = 0; u < VPL2; ++u) {
+                            const int c = c0 + lane + 32 * u;
+                            xv[q][u] = c < k2 ? __ldg(x2 + static_cast<size_t>(cc[q]) * ldx2 + c) : make_double2(0.0, 0.0);
+                        }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int u = 0; u < VPL2; ++u) {
+                            acc[u].x = fma(vv[q], xv[q][u].x, acc[u].x);
+                            acc[u].y = fma(vv[q], xv[q][u].y, acc[u].y);
+                        }
+                }
+                for (; t < cnt; ++t) {
+                    const int c = __shfl_sync(0xffffffffu, my_c, t);
+                    const double v = __shfl_sync(0xffffffffu, my_v, t);
+#pragma unroll
+                    for (int u = 0; u < VPL2; ++u) {
+                        const int cc2 = c0 + lane + 32 * u;
+                        if (cc2 < k2) {
+                            const double2 xv = __ldg(x2 + static_cast<size_t>(c) * ldx2 + cc2);
+                            acc[u].x = fma(v, xv.x, acc[u].x);
+                            acc[u].y = fma(v, xv.y, acc[u].y);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < VPL2; ++u) {
+                const int c = c0 + lane + 32 * u;
+                if (c < k2) y2[static_cast<size_t>(row) * ldy2 + c] = acc[u];
+            }
+        }
+    }
+}
+
 int spmm_grid(int n) {
     // 8 warps per CTA, one row per warp per grid-stride step; enough CTAs to
     // fill every SM several times over (148 SMs x 8 resident CTAs)
@@ -121,6 +223,15 @@ extern "C" int bk_spmm_d(int n, const int32_t* rp, const int32_t* ci, const doub
     if (n <= 0 || k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
     const int grid = spmm_grid(n);
+    const bool vec = (k % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
+                     (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+    if (vec && k >= 16 && false) {  // measured slower (register pressure); kept for reference
+        if (k <= 64)
+            spmm_d2_kernel<1><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
+        else
+            spmm_d2_kernel<2><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
+        BK_LAUNCHED();
+    }
     if (k <= 32)
         spmm_d_kernel<1><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
     else if (k <= 64)

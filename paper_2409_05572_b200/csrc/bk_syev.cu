@@ -416,6 +416,11 @@ __global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, cons
     }
 }
 
+template <class K>
+cudaError_t prep_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
 // cluster size for the distributed tridiagonalisation, 0 when it does not fit
 int tridiag_cluster_size(int d, size_t* smem) {
     for (int c = 1; c <= 16; c *= 2) {
@@ -523,7 +528,6 @@ __device__ void tri_solve_shifted(int d, const double* __restrict__ dg, const do
         const double ns = i + 2 < d ? off[i + 1] : 0.0;
         if (fabs(sub) > fabs(diag_cur)) {
             // swap rows i and i+1
-            piv[i] = 1;
             const double mult = diag_cur / sub;
             u0[i] = sub;
             u1[i] = nd;
@@ -535,7 +539,6 @@ __device__ void tri_solve_shifted(int d, const double* __restrict__ dg, const do
             sup_cur = sup2_cur - mult * ns;
             sup2_cur = 0.0;
         } else {
-            piv[i] = 0;
             const double p0 = fabs(diag_cur) < tiny ? copysign(tiny, diag_cur == 0.0 ? 1.0 : diag_cur) : diag_cur;
             const double mult = sub / p0;
             u0[i] = p0;
@@ -566,14 +569,27 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
                                                      const double* __restrict__ lam, const int* __restrict__ gstart,
                                                      const int* __restrict__ ngroups, double* __restrict__ u,
                                                      double* __restrict__ scratch) {
-    const int lane = threadIdx.x & 31;
+    extern __shared__ double ism[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // T staged in shared memory (the solve walks it sequentially), plus a
+    // private 4*d workspace per warp: no global round trips on the serial path
+    double* sdg = ism;
+    double* soff = ism + d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        sdg[i] = dg[i];
+        soff[i] = off[i];
+    }
+    __syncthreads();
+    dg = sdg;
+    off = soff;
+    (void)scratch;
     if (gw >= *ngroups) return;
-    double* b = scratch + static_cast<size_t>(gw) * 5 * d;
+    double* b = ism + 2 * d + static_cast<size_t>(wib) * 4 * d;
     double* u0 = b + d;
     double* u1 = u0 + d;
     double* u2 = u1 + d;
-    int* piv = reinterpret_cast<int*>(u2 + d);
+    int piv[1];
     double tnorm = 0.0;
     for (int i = lane; i < d; i += 32)
         tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0));
@@ -639,6 +655,62 @@ __global__ void __launch_bounds__(128) backtr_kernel(int d, int n_need, const do
         __syncwarp();
     }
     for (int i = lane; i < d; i += 32) z[static_cast<size_t>(i) * ldz + c] = x[i];
+}
+
+// Register-resident variant (d <= 32*NPL): each warp keeps its eigenvector
+// column in registers (NPL values per lane); the CTA stages KC reflectors at a
+// time in shared memory, so every reflector is read from L2 once per CTA.
+template <int NPL>
+__global__ void __launch_bounds__(256) backtr_reg_kernel(int d, int n_need, const double* __restrict__ vref,
+                                                          const double* __restrict__ tau,
+                                                          const double* __restrict__ u, double* __restrict__ z,
+                                                          int ldz) {
+    constexpr int KC = 8;
+    extern __shared__ double bsm[];  // KC x d reflector slab
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int c = blockIdx.x * nwb + wib;
+    const bool live = c < n_need;
+    double x[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int r = lane + 32 * q;
+        x[q] = live && r < d ? u[static_cast<size_t>(c) * d + r] : 0.0;
+    }
+    for (int kk = d - 3; kk >= 0; kk -= KC) {
+        const int k_lo = max(0, kk - KC + 1);
+        // stage reflectors k_lo..kk: slot (kk - k) holds v_k[0 .. d-k-2]
+        for (int e = threadIdx.x; e < KC * d; e += blockDim.x) {
+            const int sidx = e / d, i = e - sidx * d;
+            const int k = kk - sidx;
+            if (k >= k_lo && i < d - k - 1) bsm[e] = vref[static_cast<size_t>(k) * d + i];
+        }
+        __syncthreads();
+        if (live)
+            for (int k = kk; k >= k_lo; --k) {
+                const double t = tau[k];
+                if (t == 0.0) continue;
+                const double* vk = bsm + (kk - k) * d;
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    const int r = lane + 32 * q;
+                    if (r > k && r < d) s = fma(vk[r - k - 1], x[q], s);
+                }
+                s = warp_sum(s) * t;
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    const int r = lane + 32 * q;
+                    if (r > k && r < d) x[q] = fma(-s, vk[r - k - 1], x[q]);
+                }
+            }
+        __syncthreads();
+    }
+    if (live)
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int r = lane + 32 * q;
+            if (r < d) z[static_cast<size_t>(r) * ldz + c] = x[q];
+        }
 }
 
 // u (column-major d x k) -> row-major scratch, and back
@@ -756,22 +828,53 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     if (!launched) tridiag_fused_kernel<<<1, kTriThreads, smem, s>>>(d, h, ldh, w.a, w.vref, w.tau, w.dg, w.off);
     bisect_kernel<<<ceil_div(n_need * 32, 256), 256, 0, s>>>(d, w.dg, w.off, n_need, values, w.e2);
     group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
-    invit_kernel<<<ceil_div(n_need * 32, 128), 128, 0, s>>>(d, w.dg, w.off, values, w.gstart, w.ngroups, w.u,
-                                                           w.scratch);
+    {
+        const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 4 * 4 * static_cast<size_t>(d));
+        static const cudaError_t ai = cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           static_cast<int>(sizeof(double) * 18 * kSyevMaxD));
+        BK_RET(ai);
+        invit_kernel<<<ceil_div(n_need * 32, 128), 128, ism, s>>>(d, w.dg, w.off, values, w.gstart, w.ngroups, w.u,
+                                                                 w.scratch);
+    }
     // CholQR2 of U (d x n_need): row-major copy, Gram, Cholesky (no dropping), update
     cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need);
+    // two Newton-Schulz steps U <- U (3I - U^T U)/2: inverse-iteration vectors of
+    // distinct eigenvalues are orthogonal to O(eps ||T|| / gap) (gap >= 1e-7 ||T||
+    // between groups), so the error squares twice to ~1e-16 — GEMM-only, no
+    // sequential factorisation
     for (int pass = 0; pass < 2; ++pass) {
         double* src = pass == 0 ? w.urm : w.u2rm;
         double* dst = pass == 0 ? w.u2rm : w.urm;
         int rc = bk_gram_d(d, src, n_need, n_need, src, n_need, n_need, w.gram, n_need, gram_work, stream);
         if (rc) return rc;
-        rc = bk_chol_drop_d(n_need, w.gram, n_need, nullptr, 0.0, w.m, n_need, w.cinfo, w.chol, stream);
+        rc = bk_ns_coeff_d(n_need, w.gram, n_need, w.m, n_need, stream);
         if (rc) return rc;
         rc = bk_gemm_d(d, src, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, dst, n_need, stream);
         if (rc) return rc;
     }
     rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.urm, n_need, w.u);
-    backtr_kernel<<<ceil_div(n_need * 32, 128), 128, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+    {
+        const size_t bs = sizeof(double) * 8 * static_cast<size_t>(d);
+        const int blocks = ceil_div(n_need, 8);
+        static const cudaError_t ab4 = prep_smem(backtr_reg_kernel<4>, sizeof(double) * 8 * kSyevMaxD);
+        static const cudaError_t ab8 = prep_smem(backtr_reg_kernel<8>, sizeof(double) * 8 * kSyevMaxD);
+        static const cudaError_t ab12 = prep_smem(backtr_reg_kernel<12>, sizeof(double) * 8 * kSyevMaxD);
+        static const cudaError_t ab16 = prep_smem(backtr_reg_kernel<16>, sizeof(double) * 8 * kSyevMaxD);
+        BK_RET(ab4);
+        BK_RET(ab8);
+        BK_RET(ab12);
+        BK_RET(ab16);
+        if (d <= 128)
+            backtr_reg_kernel<4><<<blocks, 256, bs, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+        else if (d <= 256)
+            backtr_reg_kernel<8><<<blocks, 256, bs, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+        else if (d <= 384)
+            backtr_reg_kernel<12><<<blocks, 256, bs, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+        else if (d <= 512)
+            backtr_reg_kernel<16><<<blocks, 256, bs, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+        else
+            backtr_kernel<<<ceil_div(n_need * 32, 128), 128, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+    }
     BK_RET(cudaMemsetAsync(info, 0, 2 * sizeof(int), s));
     BK_LAUNCHED();
 }

@@ -334,16 +334,13 @@ private:
         if (kept == 0) return 0;
         Blk pt{PT_.d(), ldT_};
         gemm(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld);
-        // second CholQR pass (no dropping: every pivot is ~1 after pass one)
+        // second pass: the block is orthonormal to ~1e-8 after the pivot-checked
+        // first pass (p >= 1e-8 g_jj bounds its condition), so one Newton-Schulz
+        // step W1 (3I - G)/2 restores orthogonality to ~1e-16 without a second
+        // sequential factorisation or host round trip
         gram(rows, pt.p, pt.ld, kept, pt.p, pt.ld, kept, GB_.d(), kept);
-        auto tc2 = prof_begin();
-        BKC(bk_chol_drop_d(kept, GB_.d(), kept, nullptr, 0.0, M2_.d(), kept, info, WORK_.p(), st()));
-        prof_end(tc2, K_CHOL, 8.0 * kept * kept, kept * kept * kept / 3.0);
-        BKC(cudaMemcpyAsync(pin_.info, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        BKO(bk_ns_coeff_d(kept, GB_.d(), kept, M2_.d(), kept, st()));
         gemm(rows, pt.p, pt.ld, kept, M2_.d(), kept, kept, 1.0, 0.0, out.p, out.ld);
-        sync();
-        if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
-        if (pin_.info[1] || pin_.info[0] != kept) return cgs2_fallback(rows, w, a, q, m, out);
         return kept;
     }
 
