@@ -126,6 +126,130 @@ def config2(strategy="fix", n_ex=96, side=64, x0=True):
                     x0_columns(n, n_ex, 1, "normal") if x0 else None)
 
 
+def matrix_rng(seed):
+    """Matrix randomness uses its own stream (SeedSequence [seed, 0xA]) so it is
+    not the same sequence as the X0 draw of the same config seed."""
+    return np.random.default_rng([seed, 0xA])
+
+
+def clustered(n=1_000_000, clusters=50, width=1e-3, per_row=8, coupling=0.01, seed=2):
+    """Config 3 matrix: A = D + coupling (S + S^T)/2.  D: `clusters`
+    centres U[0,100], each holding n/clusters values U[c, c+width], cluster-major
+    rows; S: per_row draws per row, with replacement, from columns != row, N(0,1)
+    values, duplicates summed.  The lower entry (i, j) is coupling * 0.5 * sum of
+    the draws landing on (i, j) or (j, i)."""
+    rng = matrix_rng(seed)
+    centres = rng.uniform(0.0, 100.0, clusters)
+    per = n // clusters
+    diag = (centres[:, None] + rng.uniform(0.0, width, (clusters, per))).ravel()
+    assert diag.size == n
+    r = np.repeat(np.arange(n, dtype=np.int64), per_row)
+    c = rng.integers(0, n - 1, r.size)
+    c = c + (c >= r)  # columns != row
+    v = rng.standard_normal(r.size)
+    lo, hi = np.minimum(r, c), np.maximum(r, c)
+    rp, col, s = lower_csr_from_coo(n, np.concatenate([hi, np.arange(n)]),
+                                    np.concatenate([lo, np.arange(n)]),
+                                    np.concatenate([v, np.zeros(n)]))
+    # s holds the summed off-diagonal draws (0 on the diagonal): scale, add D
+    val = (s * 0.5) * coupling
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    dpos = np.nonzero(col == rows)[0]
+    val[dpos] = diag
+    return rp, col, val
+
+
+def anderson(side=96, w=16.5, seed=3):
+    """Config 4 base matrix A: 3D periodic lattice, hopping -1 to each neighbour,
+    on-site potential U[-w/2, w/2] per site in site order (x fastest)."""
+    rp, col, val = grid_laplacian((side, side, side), periodic=True)
+    n = side ** 3
+    pot = matrix_rng(seed).uniform(-w / 2, w / 2, n)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    val = val.copy()
+    val[col == rows] = pot
+    return rp, col, val
+
+
+def full_from_lower(n, rp, col, val):
+    import scipy.sparse as sp
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    low = sp.csr_matrix((val, (rows, col)), shape=(n, n))
+    d = sp.diags(low.diagonal())
+    return (low + low.T.conj() - d).tocsr()
+
+
+def lower_from_full(m):
+    import scipy.sparse as sp
+    low = sp.tril(m).tocsr()
+    low.sort_indices()
+    return low.indptr.astype(np.int64), low.indices.astype(np.int32), low.data.copy()
+
+
+def squared(n, rp, col, val):
+    """A^2 formed once on the host in fp64, returned as lower CSR."""
+    a = full_from_lower(n, rp, col, val)
+    return lower_from_full(a @ a)
+
+
+def magnetic(side=1024, phi=1.0 / 64):
+    """Config 5: 2D periodic magnetic Laplacian (complex Hermitian).  Diagonal 4,
+    x-links -1, and the y-link (x, y) -> (x, y+1) carries -exp(i 2 pi phi x), i.e.
+    H[(x, y+1), (x, y)] = -exp(i 2 pi phi x).  Entries are stored in
+    the lower triangle (conjugated where the wrap puts them above the diagonal);
+    phi*side is an integer, so the wrap is consistent."""
+    n = side * side
+    idx = np.arange(n, dtype=np.int64)
+    x, y = idx % side, idx // side
+    up = x + side * ((y + 1) % side)
+    hy = -np.exp(2j * np.pi * phi * x)
+    right = (x + 1) % side + side * y
+    rows = np.concatenate([idx, up, right])
+    cols = np.concatenate([idx, idx, idx])
+    vals = np.concatenate([np.full(n, 4.0 + 0j), hy, np.full(n, -1.0 + 0j)])
+    # entry (r, c) with r < c goes to the lower triangle as conj at (c, r)
+    swap = rows < cols
+    r2 = np.where(swap, cols, rows)
+    c2 = np.where(swap, rows, cols)
+    v2 = np.where(swap, np.conj(vals), vals)
+    return lower_csr_from_coo(n, r2, c2, v2)
+
+
+def config3(solver="lobpcg", n=1_000_000, x0=True):
+    """Clustered spectrum, n = 1e6: the nev = 100 LARGEST eigenpairs (solved as the
+    smallest of M = -A, values negated back).  LOBPCG at n_ex 150 / n_es 105; SI at
+    n_ex 200 with the power operator B = -M = A (op_shift 0).  seed 2, tol 1e-8."""
+    rp, c, v = clustered(n=n)
+    n_ex = 200 if solver == "si" else 150
+    ext = dict(which=1)
+    if solver == "si":
+        ext.update(op_mode=1, op_shift=0.0)
+    return Workload(f"cfg3_clustered_{n}_{solver}", n, rp, c, v, solver,
+                    dict(n_ev=100, n_ex=n_ex, tol=1e-8, max_iters=3000), "fix", ext,
+                    x0_columns(n, n_ex, 2, "normal") if x0 else None)
+
+
+def config4(side=96, x0=True):
+    """Anderson 96^3 (W = 16.5), the nev = 128 eigenpairs nearest 0 via LOBPCG on
+    A^2 (explicit), block 128 + 32 guard vectors, tol 1e-7, seed 3."""
+    rp, c, v = anderson(side)
+    n = side ** 3
+    rp2, c2, v2 = squared(n, rp, c, v)
+    return Workload(f"cfg4_anderson_{side}_lobpcg", n, rp2, c2, v2, "lobpcg",
+                    dict(n_ev=128, n_ex=160, tol=1e-7, max_iters=20000), "fix", {},
+                    x0_columns(n, 160, 3, "normal") if x0 else None)
+
+
+def config5(side=1024, nev=256, n_ex=384, x0=True):
+    """Magnetic Laplacian 1024^2, phi = 1/64, complex128, LOBPCG nev 256, width
+    up to 384, complex N(0,1) X0 seed 4, tol 1e-8."""
+    rp, c, v = magnetic(side)
+    n = side * side
+    return Workload(f"cfg5_magnetic_{side}_lobpcg", n, rp, c, v, "lobpcg",
+                    dict(n_ev=nev, n_ex=n_ex, tol=1e-8, max_iters=5000), "fix", {},
+                    x0_columns(n, n_ex, 4, "complex") if x0 else None)
+
+
 def lap2d_eigs(nx, ny, k):
     a = 2 - 2 * np.cos(np.arange(1, nx + 1) * np.pi / (nx + 1))
     b = 2 - 2 * np.cos(np.arange(1, ny + 1) * np.pi / (ny + 1))
