@@ -18,7 +18,7 @@
 // shared memory up to d = 160 and in global memory (L2-resident) above.
 #include <cfloat>
 
-#include "bk_common.cuh"
+#include "bk_chol.cuh"
 
 namespace bk {
 namespace {
@@ -29,128 +29,9 @@ constexpr int kCholSmemMaxA = 160;
 __global__ void __launch_bounds__(1024) chol_drop_kernel(int a, const double* __restrict__ g, int ldg,
                                                           const double* __restrict__ ref2, double drop,
                                                           double* __restrict__ m, int ldm,
-                                                          int* __restrict__ info, double* __restrict__ s,
-                                                          double* __restrict__ rc, int* __restrict__ slot) {
-    __shared__ int s_keep, s_kept, s_unsure, s_bad;
-    __shared__ double s_rjj;
+                                                          int* __restrict__ info, double* __restrict__ s) {
     extern __shared__ double dyn_s[];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-    // shared layout: gd[a] r2[a] piv[a] slot[a] (ints) | Schur complement s (a <= kCholSmemMaxA)
-    double* gd = dyn_s;
-    double* r2 = dyn_s + a;
-    double* piv = dyn_s + 2 * a;
-    int* gslot = slot;
-    slot = reinterpret_cast<int*>(dyn_s + 3 * a);
-    if (a <= kCholSmemMaxA) s = dyn_s + 3 * a + (a + 1) / 2;  // working Schur complement in shared memory
-    for (int e = tid; e < a * a; e += nt) s[e] = g[static_cast<size_t>(e / a) * ldg + e % a];
-    (void)gslot;
-    for (int j = tid; j < a; j += nt) {
-        gd[j] = g[static_cast<size_t>(j) * ldg + j];
-        r2[j] = ref2 ? ref2[j] : 0.0;
-    }
-    if (tid == 0) {
-        s_unsure = 0;
-        s_bad = 0;
-    }
-    (void)s_keep;
-    (void)s_rjj;
-    __syncthreads();
-    // right-looking skip-pivot Cholesky with ONE barrier per pivot: every thread
-    // evaluates the (identical) keep decision itself; row j stays unscaled
-    // during the step and R is formed in a final pass.
-    int kept = 0;
-    for (int j = 0; j < a; ++j) {
-        const double p = s[j * a + j];
-        const double gjj = gd[j];
-        int keep;
-        bool unsure = false, bad = false;
-        if (!isfinite(p) || !isfinite(gjj)) {
-            bad = true;
-            keep = 0;
-        } else if (ref2 == nullptr) {
-            keep = p > 0.0;
-            unsure = p <= 1e-8 * gjj;  // pass 2 of CholQR2: basis lost rank
-        } else {
-            const double thr = drop * sqrt(r2[j]);
-            if (r2[j] == 0.0 || gjj < thr * thr) {
-                keep = 0;  // certain: the pivot can never exceed the projected norm
-            } else {
-                keep = p >= thr * thr;
-                unsure = p < 1e-8 * gjj || fabs(sqrt(fmax(p, 0.0)) - thr) < 1e-4 * thr;
-            }
-        }
-        if (tid == 0) {
-            if (unsure) s_unsure = 1;
-            if (bad) s_bad = 1;
-            slot[j] = keep ? kept : -1;
-            piv[j] = p;
-        }
-        if (keep) {
-            ++kept;
-            const double invp = 1.0 / p;
-            for (int k = j + 1 + wid; k < a; k += nw) {
-                const double rk = s[j * a + k] * invp;
-                for (int l = k + lane; l < a; l += 32) s[k * a + l] -= rk * s[j * a + l];
-            }
-        }
-        __syncthreads();
-    }
-    // R rows: R[j][l] = s[j][l] / sqrt(p_j), R[j][j] = sqrt(p_j)
-    for (int e = tid; e < a * a; e += nt) {
-        const int j = e / a, l = e % a;
-        if (l < j || slot[j] < 0) continue;
-        const double rj = sqrt(piv[j]);
-        s[e] = l == j ? rj : s[e] / rj;
-    }
-    __syncthreads();
-    (void)rc;
-    // R^{-1} = M (upper triangular over the kept indices), computed row by row
-    // from the bottom: for each kept i (descending, one barrier per row) all
-    // kept c > i in parallel:  M[i][c] = -(sum_{i<l<=c} R[i][l] M[l][c]) / R[i][i].
-    // R lives in the upper triangle of s; M is stored transposed in the strict
-    // lower triangle (M[l][c] at s[c*a + l]) and its diagonal in m's diagonal
-    // slot, so both stay in shared memory.
-    // dropped indices hold no R entries: zero their row of R (upper part) so the
-    // dot products below need no per-element test
-    for (int e = tid; e < a * a; e += nt) {
-        const int j = e / a, l = e % a;
-        if (l > j && (slot[j] < 0 || slot[l] < 0)) s[e] = 0.0;
-    }
-    __syncthreads();
-    // 1/R[i][i] once (piv[] no longer needed)
-    for (int i = tid; i < a; i += nt) piv[i] = slot[i] >= 0 ? 1.0 / s[i * a + i] : 0.0;
-    __syncthreads();
-    // Column c of M depends only on itself: one warp per column walks i
-    // downward (lanes split each dot product), no CTA barrier needed.
-    for (int c = wid; c < a; c += nw) {
-        if (slot[c] < 0) continue;
-        for (int i = c - 1; i >= 0; --i) {
-            if (slot[i] < 0) continue;
-            double acc = 0.0;
-            for (int l = i + 1 + lane; l < c; l += 32) acc = fma(s[i * a + l], s[c * a + l], acc);
-            acc = warp_sum(acc);
-            if (lane == 0) s[c * a + i] = -(acc + s[i * a + c] * piv[c]) * piv[i];  // M[i][c]
-            __syncwarp();
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < a * a; e += nt) {
-        const int j = e / a, c = e % a;  // output row j (original column), column c (slot)
-        m[static_cast<size_t>(j) * ldm + c] = 0.0;
-    }
-    __syncthreads();
-    for (int e = tid; e < a * a; e += nt) {
-        const int i = e / a, c = e % a;  // M[i][c], original indices i <= c
-        if (i > c || slot[i] < 0 || slot[c] < 0) continue;
-        const double val = i == c ? piv[c] : s[c * a + i];
-        m[static_cast<size_t>(i) * ldm + slot[c]] = val;
-    }
-    if (tid == 0) {
-        info[0] = kept;
-        info[1] = s_unsure;
-        info[2] = s_bad;
-    }
+    chol_drop_body(a, g, ldg, ref2, drop, m, ldm, info, s, kCholSmemMaxA, dyn_s);
 }
 
 // ------------------------------------------------------------------ K5
@@ -330,8 +211,6 @@ extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref
         return 0;
     }
     auto s = static_cast<double*>(work);  // a x a (used when a > kCholSmemMaxA)
-    double* rc = s + static_cast<size_t>(a) * a;  // 3a scratch
-    int* slot = reinterpret_cast<int*>(rc + 3 * static_cast<size_t>(a));
     if (a > 4096) return static_cast<int>(cudaErrorInvalidValue);
     static const cudaError_t attr = cudaFuncSetAttribute(
         chol_drop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -342,7 +221,7 @@ extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref
     // small blocks: per-pivot work is tiny, so fewer warps mean fewer redundant
     // decision evaluations and a cheaper barrier on the sequential path
     const int threads = 1024;
-    chol_drop_kernel<<<1, threads, smem, as_stream(stream)>>>(a, g, ldg, ref2, drop, m, ldm, info, s, rc, slot);
+    chol_drop_kernel<<<1, threads, smem, as_stream(stream)>>>(a, g, ldg, ref2, drop, m, ldm, info, s);
     BK_LAUNCHED();
 }
 

@@ -25,8 +25,9 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <utility>
 
-#include "bk_common.cuh"
+#include "bk_chol.cuh"
 
 namespace bk {
 namespace {
@@ -562,16 +563,17 @@ __device__ void tri_solve_shifted(int d, const double* __restrict__ dg, const do
     (void)piv;
 }
 
-// one warp per group; u column-major (ldu = d): column j = eigenvector j of T.
-// scratch: per warp 5*d doubles + d ints
+// one warp per wanted eigenvalue j; u column-major (ldu = d): column j = the
+// inverse-iteration vector of T for lam[j].  Vectors are iterated independently
+// (no Gram-Schmidt inside a cluster: that serialised a whole cluster on one
+// warp); clusters are orthonormalised afterwards as blocks (group_chol_kernel).
 __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restrict__ dg,
                                                      const double* __restrict__ off,
-                                                     const double* __restrict__ lam, const int* __restrict__ gstart,
-                                                     const int* __restrict__ ngroups, double* __restrict__ u,
-                                                     double* __restrict__ scratch) {
+                                                     const double* __restrict__ lam, int n_need,
+                                                     double* __restrict__ u) {
     extern __shared__ double ism[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     // T staged in shared memory (the solve walks it sequentially), plus a
     // private 4*d workspace per warp: no global round trips on the serial path
     double* sdg = ism;
@@ -583,8 +585,7 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
     __syncthreads();
     dg = sdg;
     off = soff;
-    (void)scratch;
-    if (gw >= *ngroups) return;
+    if (j >= n_need) return;
     double* b = ism + 2 * d + static_cast<size_t>(wib) * 4 * d;
     double* u0 = b + d;
     double* u1 = u0 + d;
@@ -595,43 +596,49 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
         tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0));
     for (int o = 16; o > 0; o >>= 1) tnorm = fmax(tnorm, __shfl_xor_sync(0xffffffffu, tnorm, o));
     const double tiny = DBL_EPSILON * fmax(tnorm, DBL_MIN);
-    const int g0 = gstart[gw], g1 = gstart[gw + 1];
-    for (int j = g0; j < g1; ++j) {
-        // deterministic pseudo-random start (splitmix64 of (j, i))
-        for (int i = lane; i < d; i += 32) {
-            unsigned long long z = (static_cast<unsigned long long>(j) << 32) + static_cast<unsigned long long>(i) +
-                                   0x9e3779b97f4a7c15ULL;
-            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-            z ^= z >> 31;
-            b[i] = static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
-        }
+    // deterministic pseudo-random start (splitmix64 of (j, i)): distinct starts
+    // make the vectors of a degenerate cluster independent
+    for (int i = lane; i < d; i += 32) {
+        unsigned long long z = (static_cast<unsigned long long>(j) << 32) + static_cast<unsigned long long>(i) +
+                               0x9e3779b97f4a7c15ULL;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        z ^= z >> 31;
+        b[i] = static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    }
+    __syncwarp();
+    const double shift = lam[j];
+    for (int it = 0; it < 3; ++it) {
+        if (lane == 0) tri_solve_shifted(d, dg, off, shift, tiny, b, u0, u1, u2, piv);
         __syncwarp();
-        const double shift = lam[j];
-        for (int it = 0; it < 3; ++it) {
-            if (lane == 0) tri_solve_shifted(d, dg, off, shift, tiny, b, u0, u1, u2, piv);
-            __syncwarp();
-            // orthogonalise against the group's earlier members (twice)
-            for (int pass = 0; pass < 2; ++pass)
-                for (int q = g0; q < j; ++q) {
-                    const double* uq = u + static_cast<size_t>(q) * d;
-                    double s = 0.0;
-                    for (int i = lane; i < d; i += 32) s = fma(uq[i], b[i], s);
-                    s = warp_sum(s);
-                    for (int i = lane; i < d; i += 32) b[i] -= s * uq[i];
-                    __syncwarp();
-                }
-            double nn = 0.0;
-            for (int i = lane; i < d; i += 32) nn = fma(b[i], b[i], nn);
-            nn = warp_sum(nn);
-            const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-            for (int i = lane; i < d; i += 32) b[i] *= inv;
-            __syncwarp();
-        }
-        double* uj = u + static_cast<size_t>(j) * d;
-        for (int i = lane; i < d; i += 32) uj[i] = b[i];
+        double nn = 0.0;
+        for (int i = lane; i < d; i += 32) nn = fma(b[i], b[i], nn);
+        nn = warp_sum(nn);
+        const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+        for (int i = lane; i < d; i += 32) b[i] *= inv;
         __syncwarp();
     }
+    double* uj = u + static_cast<size_t>(j) * d;
+    for (int i = lane; i < d; i += 32) uj[i] = b[i];
+}
+
+// One CTA per cluster g (gstart[g] .. gstart[g+1]): Cholesky of the cluster's
+// diagonal block of the Gram U^T U (row-major n_need x n_need), written as the
+// block R^{-1} of the block-diagonal m (zeroed by the caller), so U m has each
+// cluster orthonormal; inter-cluster products are O(eps ||T|| / gap) and the
+// Newton-Schulz steps that follow remove them.
+__global__ void __launch_bounds__(1024) group_chol_kernel(int n_need, const double* __restrict__ gram,
+                                                           const int* __restrict__ gstart,
+                                                           const int* __restrict__ ngroups, double* __restrict__ m,
+                                                           double* __restrict__ gwork, int* __restrict__ ginfo,
+                                                           int smem_max_a) {
+    extern __shared__ double dyn_s[];
+    const int b = blockIdx.x;
+    if (b >= *ngroups) return;
+    const int g0 = gstart[b], g = gstart[b + 1] - g0;
+    const size_t o = static_cast<size_t>(g0) * n_need + g0;
+    chol_drop_body(g, gram + o, n_need, nullptr, 0.0, m + o, n_need, ginfo + 4 * b,
+                   gwork + static_cast<size_t>(g0) * n_need, smem_max_a, dyn_s);
 }
 
 // ------------------------------------------------------------------ 5. back-transformation
@@ -733,7 +740,7 @@ __global__ void rm_to_cm_small(int d, int k, const double* __restrict__ rm, int 
 
 struct SyevWs {
     double *a, *vref, *tau, *dg, *off, *e2, *u, *urm, *u2rm, *gram, *m, *chol, *scratch;
-    int *gstart, *ngroups, *cinfo;
+    int *gstart, *ngroups, *cinfo, *ginfo;
 };
 
 size_t carve(SyevWs* w, void* base, int d) {
@@ -762,6 +769,7 @@ size_t carve(SyevWs* w, void* base, int d) {
     t.gstart = reinterpret_cast<int*>(take((d + 2) * 4));
     t.ngroups = reinterpret_cast<int*>(take(64));
     t.cinfo = reinterpret_cast<int*>(take(64));
+    t.ginfo = reinterpret_cast<int*>(take(static_cast<size_t>(d) * 16 + 64));
     const size_t gram_ws = bk_gram_work_bytes(d, d, d);
     double* gw = reinterpret_cast<double*>(take(gram_ws));
     (void)gw;
@@ -833,18 +841,33 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         static const cudaError_t ai = cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            static_cast<int>(sizeof(double) * 18 * kSyevMaxD));
         BK_RET(ai);
-        invit_kernel<<<ceil_div(n_need * 32, 128), 128, ism, s>>>(d, w.dg, w.off, values, w.gstart, w.ngroups, w.u,
-                                                                 w.scratch);
+        invit_kernel<<<ceil_div(n_need * 32, 128), 128, ism, s>>>(d, w.dg, w.off, values, n_need, w.u);
     }
-    // CholQR2 of U (d x n_need): row-major copy, Gram, Cholesky (no dropping), update
     cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need);
-    // two Newton-Schulz steps U <- U (3I - U^T U)/2: inverse-iteration vectors of
-    // distinct eigenvalues are orthogonal to O(eps ||T|| / gap) (gap >= 1e-7 ||T||
-    // between groups), so the error squares twice to ~1e-16 — GEMM-only, no
-    // sequential factorisation
+    // clusters -> orthonormal blocks: Gram, per-cluster Cholesky (block-diagonal
+    // R^{-1}), update
+    {
+        int rc = bk_gram_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work, stream);
+        if (rc) return rc;
+        BK_RET(cudaMemsetAsync(w.m, 0, sizeof(double) * n_need * n_need, s));
+        // Schur complement in shared memory for clusters up to smax columns
+        int smax = n_need < 160 ? n_need : 160;
+        while (smax > 0 && static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8 > 28800) --smax;
+        const size_t gsm = sizeof(double) * (static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8);
+        static const cudaError_t ag = cudaFuncSetAttribute(group_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           226 * 1024);
+        BK_RET(ag);
+        group_chol_kernel<<<n_need, 1024, gsm, s>>>(n_need, w.gram, w.gstart, w.ngroups, w.m, w.scratch,
+                                                    w.ginfo, smax);
+        rc = bk_gemm_d(d, w.urm, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, w.u2rm, n_need, stream);
+        if (rc) return rc;
+    }
+    // two Newton-Schulz steps U <- U (3I - U^T U)/2: after the cluster step the
+    // columns are orthonormal to O(eps ||T|| / gap) (gap >= 1e-7 ||T|| between
+    // clusters), so the error squares twice to ~1e-16 — GEMM-only
     for (int pass = 0; pass < 2; ++pass) {
-        double* src = pass == 0 ? w.urm : w.u2rm;
-        double* dst = pass == 0 ? w.u2rm : w.urm;
+        double* src = pass == 0 ? w.u2rm : w.urm;
+        double* dst = pass == 0 ? w.urm : w.u2rm;
         int rc = bk_gram_d(d, src, n_need, n_need, src, n_need, n_need, w.gram, n_need, gram_work, stream);
         if (rc) return rc;
         rc = bk_ns_coeff_d(n_need, w.gram, n_need, w.m, n_need, stream);
@@ -852,6 +875,7 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         rc = bk_gemm_d(d, src, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, dst, n_need, stream);
         if (rc) return rc;
     }
+    std::swap(w.urm, w.u2rm);  // result in u2rm -> name it urm below
     rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.urm, n_need, w.u);
     {
         const size_t bs = sizeof(double) * 8 * static_cast<size_t>(d);

@@ -65,11 +65,18 @@ if not only or "gemm" in only:
         ms = timeit(lambda: f.bk_gemm_d(n, p(x), 344, d, p(cm), k, k, 1.0, 0.0, p(y), 344, S()))
         ms2 = timeit(lambda: torch.matmul(x[:, :d], cm))
         out[f"gemm_{d}x{k}"] = {"ms": ms, "tflops": 2 * n * d * k / ms / 1e9, "cublas_tflops": 2 * n * d * k / ms2 / 1e9}
-if not only or "syev" in only:
-    for d, need in [(288, 96), (192, 96), (288, 288), (40, 40), (83, 69)]:
+if not only or "syev" in only or "syevbig" in only:
+    cases = [(288, 96, 0), (192, 96, 0), (288, 288, 0), (40, 40, 0), (83, 69, 0), (480, 160, 0),
+             (480, 160, 1), (450, 150, 1)]
+    if "syevbig" in (only or []):
+        cases = [c for c in cases if c[0] >= 450]
+    for d, need, clus in cases:
         rng = np.random.default_rng(d)
         q, _ = np.linalg.qr(rng.standard_normal((d, d)))
         lam = np.sort(rng.uniform(0, 12, d))
+        if clus:  # config-4 like: the wanted values packed within 1e-6 ||H||
+            lam[: need + 40] = np.sort(rng.uniform(0, 1e-4, need + 40))
+            lam[-1] = 130.0
         h = torch.as_tensor((q * lam) @ q.T, device="cuda")
         vals = torch.zeros(d, dtype=torch.float64, device="cuda")
         z = torch.zeros(d, d, dtype=torch.float64, device="cuda")
@@ -77,7 +84,12 @@ if not only or "syev" in only:
         info = torch.zeros(4, dtype=torch.int32, device="cuda")
         hh = h.clone()
         ms = timeit(lambda: (hh.copy_(h), f.bk_syev_d(d, p(hh), d, need, p(vals), p(z), d, p(ws), p(info), S())), reps=10)
-        out[f"syev_{d}_{need}"] = {"ms": ms}
+        hn = h.cpu().numpy()
+        zz = z.cpu().numpy()[:, :need]
+        vv = vals.cpu().numpy()[:need]
+        res = np.abs(hn @ zz - zz * vv).max() / np.abs(lam).max()
+        orth = np.abs(zz.T @ zz - np.eye(need)).max()
+        out[f"syev_{d}_{need}" + ("c" if clus else "")] = {"ms": ms, "res": float(res), "orth": float(orth)}
 if not only or "chol" in only:
     for a in [96, 192, 288]:
         w = torch.randn(4096, a, dtype=torch.float64, device="cuda")
