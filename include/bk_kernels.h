@@ -165,6 +165,46 @@ BK_API int bk_ns_coeff_d(int a, const double* g, int ldg, double* m, int ldm, vo
 BK_API int bk_cgs2_commit_d(int n, const double* v, const double* nrm2, const double* ref2, double drop,
                             double* out, int ldo, int* counter, void* stream);
 
+/* ---- complex128 (Hermitian) variants — config 5 (no reference counterpart:
+ * the reference is real-only).  Complex blocks are interleaved
+ * (re, im) row-major; every ld / column count below is in COMPLEX elements.
+ * Tall-skinny products run on the real views (n x 2k) through the real DMMA
+ * kernels (bk_complex.cu explains the rearrangements).  Same contracts as the
+ * _d functions above; the work sizes differ. */
+BK_API size_t bk_gram_z_work_bytes(int n, int a, int b);
+BK_API int bk_gram_z(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
+                     int ldc, void* work, void* stream);
+BK_API size_t bk_gemm_z_work_bytes(int d, int k);
+BK_API int bk_gemm_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                     double beta, double* y, int ldy, void* work, void* stream);
+BK_API size_t bk_colnorm2_z_work_bytes(int n, int k);
+BK_API int bk_colnorm2_z(int n, const double* x, int ldx, int k, double* out, void* work, void* stream);
+BK_API size_t bk_coldot_z_work_bytes(int n, int k); /* out[c] = Re sum conj(x) y */
+BK_API int bk_coldot_z(int n, const double* x, int ldx, const double* y, int ldy, int k, double* out,
+                       void* work, void* stream);
+BK_API size_t bk_residual_z_work_bytes(int n, int k);
+BK_API int bk_residual_z(int n, const double* v, int ldv, const double* av, int ldav, const double* lambda,
+                         int k, double* r, int ldr, const double* t, double* w, int ldw, int w_from,
+                         double* rn2, double* vn2, void* work, void* stream);
+BK_API int bk_ns_coeff_z(int a, const double* g, int ldg, double* m, int ldm, void* stream);
+BK_API size_t bk_chol_z_work_bytes(int a);
+BK_API int bk_chol_drop_z(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
+                          int ldm, int* info, void* work, void* stream);
+BK_API int bk_cm_to_rm_z(int n, int k, const double* cm, int ldcm, double* rm, int ldrm, void* stream);
+BK_API int bk_rm_to_cm_z(int n, int k, const double* rm, int ldrm, double* cm, int ldcm, void* stream);
+/* Hermitian projected eigenproblem: grid-cooperative Householder reduction to a
+ * REAL tridiagonal (LAPACK zhetd2 conventions), bisection + inverse iteration
+ * as for bk_syev_tri_d, complex back-transformation.  d <= 1200. */
+BK_API size_t bk_syev_z_work_bytes(int d);
+BK_API int bk_syev_z(int d, const double* h, int ldh, int n_need, double* values, double* z, int ldz,
+                     void* work, int* info, void* stream);
+BK_API int bk_cg_step1_z(int n, int k, const double* rs, const double* pap, int* active, double* x, int ldx,
+                         double* r, int ldr, const double* p, int ldp, const double* ap, int ldap, void* stream);
+BK_API int bk_cg_step2_z(int n, int k, double* rs, const double* rs_new, const int* active, const double* r,
+                         int ldr, double* p, int ldp, void* stream);
+BK_API int bk_cgs2_commit_z(int n, const double* v, const double* nrm2, const double* ref2, double drop,
+                            double* out, int ldo, int* counter, void* stream);
+
 /* host-only hook: nblocks consecutive random blocks (sizes[i] values each) from
  * the solver's per-solve normal stream; bit-identical to drawing each block
  * with a fresh std::normal_distribution over one std::mt19937_64(seed) */

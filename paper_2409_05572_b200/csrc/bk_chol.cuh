@@ -4,6 +4,8 @@
 // vectors).  See bk_small.cu for the algorithm and its reference mapping
 // (proj/src/kernel.cpp:65-89).
 //
+// pairs: g is the real 2c x 2c embedding of a complex Hermitian Gram (bk_complex.cu);
+// odd indices follow the decision of their even twin.
 // dyn_s: dynamic shared memory of (3a + (a+1)/2) doubles, plus a*a doubles when
 // a <= smem_max_a (the Schur complement then lives in shared memory; otherwise
 // in the global scratch s, a*a doubles).
@@ -12,10 +14,15 @@
 
 namespace bk {
 
+// one-CTA launch of the routine below (bk_small.cu); pairs: see above
+int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop, double* m, int ldm, int* info,
+                void* work, cudaStream_t st, bool pairs);
+
 __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__ g, int ldg,
                                                const double* __restrict__ ref2, double drop,
                                                double* __restrict__ m, int ldm, int* __restrict__ info,
-                                               double* __restrict__ s, int smem_max_a, double* dyn_s) {
+                                               double* __restrict__ s, int smem_max_a, double* dyn_s,
+                                               bool pairs = false) {
     __shared__ int s_unsure, s_bad;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
@@ -47,6 +54,11 @@ __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__
         if (!isfinite(p) || !isfinite(gjj)) {
             bad = true;
             keep = 0;
+        } else if (pairs && (j & 1)) {
+            // real embedding of a complex Gram: index 2c+1 is the imaginary twin
+            // of 2c (same pivot in exact arithmetic) and follows its decision
+            keep = slot[j - 1] >= 0 && p > 0.0;
+            unsure = (slot[j - 1] >= 0) != (p > 0.0);
         } else if (ref2 == nullptr) {
             keep = p > 0.0;
             unsure = p <= 1e-8 * gjj;  // pass 2 of CholQR2: basis lost rank

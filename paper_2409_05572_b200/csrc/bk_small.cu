@@ -29,9 +29,10 @@ constexpr int kCholSmemMaxA = 160;
 __global__ void __launch_bounds__(1024) chol_drop_kernel(int a, const double* __restrict__ g, int ldg,
                                                           const double* __restrict__ ref2, double drop,
                                                           double* __restrict__ m, int ldm,
-                                                          int* __restrict__ info, double* __restrict__ s) {
+                                                          int* __restrict__ info, double* __restrict__ s,
+                                                          int pairs) {
     extern __shared__ double dyn_s[];
-    chol_drop_body(a, g, ldg, ref2, drop, m, ldm, info, s, kCholSmemMaxA, dyn_s);
+    chol_drop_body(a, g, ldg, ref2, drop, m, ldm, info, s, kCholSmemMaxA, dyn_s, pairs != 0);
 }
 
 // ------------------------------------------------------------------ K5
@@ -204,10 +205,11 @@ extern "C" size_t bk_chol_work_bytes(int a) {
     return (aa * aa + 3 * aa) * sizeof(double) + aa * sizeof(int) + 64;
 }
 
-extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
-                              int ldm, int* info, void* work, void* stream) {
+namespace bk {
+int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop, double* m, int ldm, int* info,
+                void* work, cudaStream_t st, bool pairs) {
     if (a <= 0) {
-        BK_RET(cudaMemsetAsync(info, 0, 3 * sizeof(int), as_stream(stream)));
+        BK_RET(cudaMemsetAsync(info, 0, 3 * sizeof(int), st));
         return 0;
     }
     auto s = static_cast<double*>(work);  // a x a (used when a > kCholSmemMaxA)
@@ -218,11 +220,14 @@ extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref
     BK_RET(attr);
     const size_t small = (3 * static_cast<size_t>(a) + (a + 1) / 2) * sizeof(double);
     const size_t smem = small + (a <= kCholSmemMaxA ? static_cast<size_t>(a) * a * sizeof(double) : 0);
-    // small blocks: per-pivot work is tiny, so fewer warps mean fewer redundant
-    // decision evaluations and a cheaper barrier on the sequential path
-    const int threads = 1024;
-    chol_drop_kernel<<<1, threads, smem, as_stream(stream)>>>(a, g, ldg, ref2, drop, m, ldm, info, s);
+    chol_drop_kernel<<<1, 1024, smem, st>>>(a, g, ldg, ref2, drop, m, ldm, info, s, pairs ? 1 : 0);
     BK_LAUNCHED();
+}
+}  // namespace bk
+
+extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
+                              int ldm, int* info, void* work, void* stream) {
+    return chol_launch(a, g, ldg, ref2, drop, m, ldm, info, work, as_stream(stream), false);
 }
 
 extern "C" size_t bk_syev_jacobi_work_bytes(int d) {

@@ -13,6 +13,8 @@
 // is a coalesced 256-byte transaction per 32 columns.  Accumulators stay in
 // registers (VPL per lane); widths beyond 32*VPL loop over column chunks.
 // HBM-bound: algorithmic bytes = nnz*12 + (n+1)*4 + 2*n*k*8 (real).
+#include <cstdlib>
+
 #include "bk_common.cuh"
 
 namespace bk {
@@ -23,14 +25,16 @@ __global__ void __launch_bounds__(256) spmm_d_kernel(int n, const int32_t* __res
                                                       const int32_t* __restrict__ ci,
                                                       const double* __restrict__ val,
                                                       const double* __restrict__ x, int ldx, int k,
-                                                      double* __restrict__ y, int ldy) {
+                                                      double* __restrict__ y, int ldy, int tile) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // each CTA sweeps a contiguous chunk of rows, its warps interleaved within
-    // the chunk, so X rows shared by neighbouring rows (stencil offsets +-1,
-    // +-grid line) are re-read from L1 instead of L2
-    const int rpc = ceil_div(n, gridDim.x);
-    const int r_begin = blockIdx.x * rpc, r_end = min(n, r_begin + rpc);
-    for (int row = r_begin + warp; row < r_end; row += nw) {
+    // Rows are dealt out in tiles of `tile` consecutive rows, tile t to CTA
+    // t mod grid (grid = resident CTAs), so all SMs sweep the matrix together:
+    // the X rows live at any moment are a narrow band around the sweep front
+    // (plus the stencil's far offsets) that stays in L2, and neighbouring rows
+    // inside a tile re-hit L1.  (Contiguous per-CTA chunks spread the band over
+    // the whole matrix and re-read X from HBM ~6x at k = 160.)
+    for (int t0 = blockIdx.x * tile; t0 < n; t0 += gridDim.x * tile)
+    for (int row = t0 + warp; row < min(n, t0 + tile); row += nw) {
         const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
         for (int c0 = 0; c0 < k; c0 += 32 * VPL) {
             double acc[VPL];
@@ -213,6 +217,21 @@ int spmm_grid(int n) {
     return max(1, min(want, kSMs * 16));
 }
 
+// tile rows per CTA step and resident CTAs per SM for spmm_d_kernel
+// (BK_SPMM_TILE / BK_SPMM_CPS override, for tuning runs only)
+struct SpmmShape {
+    int tile, cps;
+};
+SpmmShape spmm_shape() {
+    static const SpmmShape sh = [] {
+        SpmmShape r{64, 4};
+        if (const char* e = getenv("BK_SPMM_TILE")) r.tile = max(8, atoi(e));
+        if (const char* e = getenv("BK_SPMM_CPS")) r.cps = max(1, atoi(e));
+        return r;
+    }();
+    return sh;
+}
+
 }  // namespace
 }  // namespace bk
 
@@ -232,14 +251,20 @@ extern "C" int bk_spmm_d(int n, const int32_t* rp, const int32_t* ci, const doub
             spmm_d2_kernel<2><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
         BK_LAUNCHED();
     }
+    const SpmmShape sh = spmm_shape();
+    const int tg = max(1, min(ceil_div(n, sh.tile), kSMs * sh.cps));
     if (k <= 32)
-        spmm_d_kernel<1><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
+        spmm_d_kernel<1><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
     else if (k <= 64)
-        spmm_d_kernel<2><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
+        spmm_d_kernel<2><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
     else if (k <= 96)
-        spmm_d_kernel<3><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
+        spmm_d_kernel<3><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
+    else if (k <= 128)
+        spmm_d_kernel<4><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
+    else if (k <= 160)
+        spmm_d_kernel<5><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
     else
-        spmm_d_kernel<4><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
+        spmm_d_kernel<6><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
     BK_LAUNCHED();
 }
 

@@ -3,22 +3,22 @@
 // Replaces sym_eig_small (proj/src/kernel.cpp:95-100: Eigen's
 // SelfAdjointEigenSolver = Householder tridiagonalisation + implicit QR) with the
 // same first stage and a parallel second stage:
-//   1. tridiag_kernel   Householder reduction of 0.5(H + H^T) to tridiagonal
-//                       T = Q^T H Q (one CTA; trailing block in shared memory
-//                       once it fits, L2 before).
+//   1. tridiag_*        Householder reduction of 0.5(H + H^T) to tridiagonal
+//                       T = Q^T H Q: a thread-block cluster holding H in
+//                       distributed shared memory (d <= ~640), else a
+//                       cooperative grid kernel over an L2-resident copy
+//                       (also the complex Hermitian path, config 5).
 //   2. bisect_kernel    the wanted eigenvalues of T by Sturm-count multisection,
 //                       one warp per eigenvalue (32 probe points per round).
-//   3. group_kernel +   eigenvectors of T by inverse iteration, one warp per
-//      invit_kernel     group of (near-)degenerate eigenvalues (relative gap
-//                       < 1e-7 ||T||): members are orthogonalised against the
-//                       group (modified Gram-Schmidt) every step, so exact
-//                       multiplets come out orthonormal.
-//   4. CholQR2 of U     (K2 Gram + K4 Cholesky + K3 update): vectors of distinct
-//                       eigenvalues are orthogonal to O(eps ||T|| / gap); the
-//                       re-orthonormalisation mixes them by the same amount,
-//                       which moves residuals by only O(eps ||T||).
-//   5. backtr_kernel    Z = Q U, one warp per eigenvector applying the stored
-//                       reflectors.
+//   3. invit_kernel     eigenvectors of T by inverse iteration, one warp per
+//                       wanted eigenvalue, distinct pseudo-random starts.
+//   4. group_kernel +   clusters of (near-)degenerate eigenvalues (gap <
+//      group_chol +     1e-7 ||T||) orthonormalised as blocks (K2 Gram, one-CTA
+//      Newton-Schulz    Cholesky per cluster, K3 update), then two Newton-Schulz
+//                       steps: vectors of distinct clusters are orthogonal to
+//                       O(eps ||T|| / gap), so the polish moves residuals by
+//                       only O(eps ||T||).
+//   5. backtr_*         Z = Q U applying the stored reflectors.
 // Why not Jacobi for d > 64: a cyclic Jacobi sweep is d-1 dependent rounds and
 // ~10 sweeps are needed, so it is latency-bound (96 ms at d = 288 on one CTA,
 // profiles/r01_bench_first.log); this path has O(d) dependent steps in total.
@@ -41,109 +41,6 @@ constexpr int kSyevJacobiMaxD = 48;
 // a: d x d working copy (row-major, lda = d), symmetric, both triangles kept.
 // On exit: diag[k], off[k] (T(k+1,k)), reflector k stored in vref[k*d + i]
 // for i < d-k-1 (v[0] = 1), tau[k].
-__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(int d, const double* __restrict__ h, int ldh,
-                                                               double* __restrict__ a, double* __restrict__ vref,
-                                                               double* __restrict__ tau, double* __restrict__ diag,
-                                                               double* __restrict__ off) {
-    extern __shared__ double sm[];
-    __shared__ double red[kTriThreads / 32];
-    __shared__ double s_scal[4];
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-    double* v = sm;          // d
-    double* p = sm + d;      // d
-    double* tri = sm + 2 * d;  // trailing block once it fits
-    for (int e = tid; e < d * d; e += nt) {
-        const int i = e / d, j = e % d;
-        a[e] = 0.5 * (h[static_cast<size_t>(i) * ldh + j] + h[static_cast<size_t>(j) * ldh + i]);
-    }
-    __syncthreads();
-    bool in_smem = false;
-    int base = 0;  // row/col offset of `tri` inside a
-    auto A = [&](int i, int j) -> double& {  // trailing-block accessor, i, j >= base
-        return in_smem ? tri[(i - base) * (d - base) + (j - base)] : a[static_cast<size_t>(i) * d + j];
-    };
-    auto block_sum = [&](double x) {
-        x = warp_sum(x);
-        if (lane == 0) red[wid] = x;
-        __syncthreads();
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += red[w];
-        __syncthreads();
-        return s;
-    };
-    for (int k = 0; k + 2 < d; ++k) {
-        const int m = d - k - 1;
-        if (!in_smem && m <= kTriSmemMaxM) {
-            // move the trailing (m+1) x (m+1) block (rows/cols >= k) into shared memory
-            base = k;
-            const int mm = d - base;
-            for (int e = tid; e < mm * mm; e += nt) tri[e] = a[static_cast<size_t>(base + e / mm) * d + base + e % mm];
-            __syncthreads();
-            in_smem = true;
-        }
-        // (a) reflector from x = A(k+1:, k)
-        double xs = 0.0;
-        for (int i = 1 + tid; i < m; i += nt) {
-            const double x = A(k + 1 + i, k);
-            xs = fma(x, x, xs);
-        }
-        const double xnorm2 = block_sum(xs);
-        if (tid == 0) {
-            const double alpha = A(k + 1, k);
-            diag[k] = A(k, k);
-            double t = 0.0, beta = alpha, scal = 0.0;
-            if (xnorm2 > 0.0) {
-                beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
-                t = (beta - alpha) / beta;
-                scal = 1.0 / (alpha - beta);
-            }
-            off[k] = beta;
-            tau[k] = t;
-            s_scal[0] = t;
-            s_scal[1] = scal;
-        }
-        __syncthreads();
-        const double t = s_scal[0], scal = s_scal[1];
-        for (int i = tid; i < m; i += nt) {
-            const double vi = i == 0 ? 1.0 : A(k + 1 + i, k) * scal;
-            v[i] = vi;
-            vref[static_cast<size_t>(k) * d + i] = vi;
-        }
-        __syncthreads();
-        if (t == 0.0) continue;  // H = I: nothing to update (uniform branch)
-        // (b) p = t * A22 v   (warp per row, lanes across the row)
-        for (int i = wid; i < m; i += nw) {
-            double s = 0.0;
-            for (int j = lane; j < m; j += 32) s = fma(A(k + 1 + i, k + 1 + j), v[j], s);
-            s = warp_sum(s);
-            if (lane == 0) p[i] = t * s;
-        }
-        __syncthreads();
-        // (c) w = p - (t/2)(p^T v) v
-        double pv = 0.0;
-        for (int i = tid; i < m; i += nt) pv = fma(p[i], v[i], pv);
-        const double kk = -0.5 * t * block_sum(pv);
-        for (int i = tid; i < m; i += nt) p[i] = fma(kk, v[i], p[i]);
-        __syncthreads();
-        // (d) A22 -= v w^T + w v^T
-        for (int e = tid; e < m * m; e += nt) {
-            const int i = e / m, j = e % m;
-            double& x = A(k + 1 + i, k + 1 + j);
-            x -= v[i] * p[j] + p[i] * v[j];
-        }
-        __syncthreads();
-    }
-    if (tid == 0) {
-        if (d >= 2) {
-            diag[d - 2] = A(d - 2, d - 2);
-            off[d - 2] = A(d - 1, d - 2);
-            tau[d - 2] = 0.0;
-        }
-        diag[d - 1] = A(d - 1, d - 1);
-        off[d - 1] = 0.0;
-        if (d >= 1) tau[d - 1] = 0.0;
-    }
-}
 
 // Fused variant (the one launched): the rank-2 update of step k-1 is applied
 // lazily inside step k's single pass over the trailing block, which also
@@ -738,9 +635,243 @@ __global__ void rm_to_cm_small(int d, int k, const double* __restrict__ rm, int 
     }
 }
 
+// ------------------------------------------------------------------ grid-cooperative path
+// Real and complex Hermitian reduction over an L2-resident copy of H, for the
+// projected problems too large for one cluster's shared memory (real d > ~640)
+// and for every complex one (config 5: d up to 3*384 = 1152).  LAPACK
+// zhetd2/zlarfg conventions: H_j = I - tau_j v_j v_j^H with v_j[0] = 1 and
+// H_j^H x = beta e_1, beta REAL, so T = Q^H A Q is a real symmetric tridiagonal
+// even for complex A and the real bisection / inverse iteration above apply
+// unchanged; Z = Q U is complex.
+//
+// One grid.sync() per column: the rank-2 update of step j-1 is applied lazily
+// inside step j's single pass over the trailing rows (each warp owns rows
+// r = j+1+gw, gw + #warps, ...), which also accumulates p_j = tau_j A v_j.
+// Every CTA rebuilds the reflector redundantly from row j (deterministic
+// reductions, so all CTAs hold bit-identical v_j), P and the p^H v partials
+// are double-buffered across steps.
+__device__ __forceinline__ double re_(double a) { return a; }
+__device__ __forceinline__ double re_(double2 a) { return a.x; }
+__device__ __forceinline__ double im_(double) { return 0.0; }
+__device__ __forceinline__ double im_(double2 a) { return a.y; }
+__device__ __forceinline__ double cj(double a) { return a; }
+__device__ __forceinline__ double2 cj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double mul(double a, double b) { return a * b; }
+__device__ __forceinline__ double2 mul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 operator-(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 scal(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double scal(double s, double a) { return s * a; }
+template <class E>
+__device__ __forceinline__ E mk(double r, double i);
+template <>
+__device__ __forceinline__ double mk<double>(double r, double) { return r; }
+template <>
+__device__ __forceinline__ double2 mk<double2>(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ double wsum(double v) { return warp_sum(v); }
+__device__ __forceinline__ double2 wsum(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
+__device__ __forceinline__ double abs2(double a) { return a * a; }
+__device__ __forceinline__ double abs2(double2 a) { return a.x * a.x + a.y * a.y; }
+// 1 / z
+__device__ __forceinline__ double inv_(double a) { return 1.0 / a; }
+__device__ __forceinline__ double2 inv_(double2 a) {
+    const double s = 1.0 / (a.x * a.x + a.y * a.y);
+    return make_double2(a.x * s, -a.y * s);
+}
+
+constexpr int kCoopThreads = 512;
+
+// A <- (H + H^H)/2, full storage (lda = d)
+template <class E>
+__global__ void sym_copy_kernel(int d, const E* __restrict__ h, int ldh, E* __restrict__ a) {
+    const int total = d * d;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int i = e / d, j = e - i * d;
+        const E x = h[static_cast<size_t>(i) * ldh + j], y = cj(h[static_cast<size_t>(j) * ldh + i]);
+        a[e] = scal(0.5, x + y);
+    }
+}
+
+template <class E>
+__global__ void __launch_bounds__(kCoopThreads) tridiag_coop_kernel(int d, E* __restrict__ a, E* __restrict__ vref,
+                                                                     E* __restrict__ tau, double* __restrict__ dg,
+                                                                     double* __restrict__ off, E* __restrict__ pbuf,
+                                                                     E* __restrict__ part) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ unsigned char coop_sm[];
+    E* vprev = reinterpret_cast<E*>(coop_sm);
+    E* wprev = vprev + d;
+    E* vcur = wprev + d;
+    __shared__ double red_d[kCoopThreads / 32];
+    __shared__ E red_e[kCoopThreads / 32];
+    __shared__ double s_diag;
+    __shared__ E s_pv;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int gwarps = gridDim.x * nw, gw = blockIdx.x * nw + wid;
+    bool hp = false;
+    for (int j = 0; j + 1 < d; ++j) {
+        const int buf = j & 1;
+        // ---- A: row j (pending update applied), reflector of x = conj(row j)[j+1:]
+        double xn2 = 0.0;
+        for (int c = j + tid; c < d; c += blockDim.x) {
+            E av = a[static_cast<size_t>(j) * d + c];
+            if (hp) av = av - (mul(vprev[j], cj(wprev[c])) + mul(wprev[j], cj(vprev[c])));
+            if (c == j) {
+                s_diag = re_(av);
+            } else {
+                const E x = cj(av);
+                vcur[c] = x;
+                if (c >= j + 2) xn2 += abs2(x);
+            }
+        }
+        xn2 = warp_sum(xn2);
+        if (lane == 0) red_d[wid] = xn2;
+        __syncthreads();
+        xn2 = 0.0;
+        for (int w = 0; w < nw; ++w) xn2 += red_d[w];
+        const E alpha = vcur[j + 1];
+        E t = mk<E>(0.0, 0.0);
+        double beta = re_(alpha);
+        E sc = mk<E>(0.0, 0.0);
+        const bool refl = !(xn2 == 0.0 && im_(alpha) == 0.0);
+        if (refl) {
+            const double ar = re_(alpha), ai = im_(alpha);
+            beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+            t = mk<E>((beta - ar) / beta, -ai / beta);
+            sc = inv_(alpha - mk<E>(beta, 0.0));
+        }
+        __syncthreads();  // every thread has read alpha before v overwrites vcur[j+1]
+        for (int c = j + 1 + tid; c < d; c += blockDim.x) {
+            const E v = c == j + 1 ? mk<E>(1.0, 0.0) : (refl ? mul(sc, vcur[c]) : mk<E>(0.0, 0.0));
+            vcur[c] = v;
+            if (blockIdx.x == 0) vref[static_cast<size_t>(j) * d + (c - j - 1)] = v;
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+            tau[j] = t;
+            dg[j] = s_diag;
+            off[j] = beta;
+        }
+        __syncthreads();
+        // ---- B: owned trailing rows: apply update j-1, p_j = tau_j A v_j
+        E pv = mk<E>(0.0, 0.0);
+        for (int r = j + 1 + gw; r < d; r += gwarps) {
+            E s = mk<E>(0.0, 0.0);
+            E* row = a + static_cast<size_t>(r) * d;
+            const E vr = hp ? vprev[r] : mk<E>(0.0, 0.0), wr = hp ? wprev[r] : mk<E>(0.0, 0.0);
+            for (int c = j + 1 + lane; c < d; c += 32) {
+                E av = row[c];
+                if (hp) {
+                    av = av - (mul(vr, cj(wprev[c])) + mul(wr, cj(vprev[c])));
+                    row[c] = av;
+                }
+                s = s + mul(av, vcur[c]);
+            }
+            s = wsum(s);
+            const E p = mul(t, s);
+            if (lane == 0) pbuf[static_cast<size_t>(buf) * d + r] = p;
+            pv = pv + mul(cj(p), vcur[r]);
+        }
+        if (lane == 0) red_e[wid] = pv;
+        __syncthreads();
+        if (tid == 0) {
+            E acc = mk<E>(0.0, 0.0);
+            for (int w = 0; w < nw; ++w) acc = acc + red_e[w];
+            part[static_cast<size_t>(buf) * gridDim.x + blockIdx.x] = acc;
+        }
+        grid.sync();
+        // ---- C: w_j = p_j - (tau_j / 2)(p_j^H v_j) v_j
+        if (tid == 0) {
+            E acc = mk<E>(0.0, 0.0);
+            for (int g = 0; g < static_cast<int>(gridDim.x); ++g)
+                acc = acc + part[static_cast<size_t>(buf) * gridDim.x + g];
+            s_pv = acc;
+        }
+        __syncthreads();
+        const E aw = scal(-0.5, mul(t, s_pv));
+        E* tmp = vprev;
+        vprev = vcur;
+        vcur = tmp;
+        for (int c = j + 1 + tid; c < d; c += blockDim.x)
+            wprev[c] = pbuf[static_cast<size_t>(buf) * d + c] + mul(aw, vprev[c]);
+        hp = true;
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        E av = a[static_cast<size_t>(d - 1) * d + d - 1];
+        if (hp) av = av - (mul(vprev[d - 1], cj(wprev[d - 1])) + mul(wprev[d - 1], cj(vprev[d - 1])));
+        dg[d - 1] = re_(av);
+    }
+}
+
+// Z = Q U (U real, column-major d x n_need) applying H_{d-2} ... H_0; CB
+// columns per CTA held in registers (R rows per thread), one CTA barrier per
+// reflector; z row-major (ldz elements).
+template <class E, int R>
+__global__ void __launch_bounds__(256) backtr_cta_kernel(int d, int n_need, const E* __restrict__ vref,
+                                                          const E* __restrict__ tau, const double* __restrict__ u,
+                                                          E* __restrict__ z, int ldz) {
+    constexpr int CB = 4;
+    __shared__ E red[2][8][CB];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int col0 = blockIdx.x * CB;
+    E x[CB][R];
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int i = tid + 256 * q;
+            x[c][q] = mk<E>(i < d && col0 + c < n_need ? u[static_cast<size_t>(col0 + c) * d + i] : 0.0, 0.0);
+        }
+    int b = 0;
+    for (int j = d - 2; j >= 0; --j) {
+        const E t = tau[j];
+        if (re_(t) == 0.0 && im_(t) == 0.0) continue;
+        const E* v = vref + static_cast<size_t>(j) * d - (j + 1);  // v[i] for i in [j+1, d)
+        E vv[R];
+        E s[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) s[c] = mk<E>(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int i = tid + 256 * q;
+            vv[q] = i > j && i < d ? v[i] : mk<E>(0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < CB; ++c) s[c] = s[c] + mul(cj(vv[q]), x[c][q]);
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            s[c] = wsum(s[c]);
+            if (lane == 0) red[b][wid][c] = s[c];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            E tot = mk<E>(0.0, 0.0);
+            for (int w = 0; w < 8; ++w) tot = tot + red[b][w][c];
+            s[c] = mul(t, tot);
+        }
+        b ^= 1;
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < CB; ++c) x[c][q] = x[c][q] - mul(vv[q], s[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int i = tid + 256 * q;
+            if (i < d && col0 + c < n_need) z[static_cast<size_t>(i) * ldz + col0 + c] = x[c][q];
+        }
+}
+
 struct SyevWs {
     double *a, *vref, *tau, *dg, *off, *e2, *u, *urm, *u2rm, *gram, *m, *chol, *scratch;
     int *gstart, *ngroups, *cinfo, *ginfo;
+    double *za, *zv, *ztau, *zp, *zpart;  // grid-cooperative / complex path (interleaved complex)
 };
 
 size_t carve(SyevWs* w, void* base, int d) {
@@ -770,6 +901,11 @@ size_t carve(SyevWs* w, void* base, int d) {
     t.ngroups = reinterpret_cast<int*>(take(64));
     t.cinfo = reinterpret_cast<int*>(take(64));
     t.ginfo = reinterpret_cast<int*>(take(static_cast<size_t>(d) * 16 + 64));
+    t.za = reinterpret_cast<double*>(take(2 * dd * 8));
+    t.zv = reinterpret_cast<double*>(take(2 * dd * 8));
+    t.ztau = reinterpret_cast<double*>(take(2 * static_cast<size_t>(d) * 8 + 16));
+    t.zp = reinterpret_cast<double*>(take(4 * static_cast<size_t>(d) * 8 + 32));
+    t.zpart = reinterpret_cast<double*>(take(4 * static_cast<size_t>(kSMs) * 8 + 32));
     const size_t gram_ws = bk_gram_work_bytes(d, d, d);
     double* gw = reinterpret_cast<double*>(take(gram_ws));
     (void)gw;
@@ -783,6 +919,109 @@ size_t carve(SyevWs* w, void* base, int d) {
 using namespace bk;
 
 extern "C" size_t bk_syev_tri_work_bytes(int d) { return carve(nullptr, nullptr, d > 0 ? d : 1); }
+
+namespace bk {
+namespace {
+// eigenvalues (bisection) and orthonormal eigenvectors U (column-major d x
+// n_need in w.u) of the tridiagonal T in (w.dg, w.off)
+int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, void* stream) {
+    const cudaStream_t s = as_stream(stream);
+    bisect_kernel<<<ceil_div(n_need * 32, 256), 256, 0, s>>>(d, w.dg, w.off, n_need, values, w.e2);
+    group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
+    {
+        const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 4 * 4 * static_cast<size_t>(d));
+        static const cudaError_t ai = cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           static_cast<int>(sizeof(double) * 18 * kSyevMaxD));
+        BK_RET(ai);
+        invit_kernel<<<ceil_div(n_need * 32, 128), 128, ism, s>>>(d, w.dg, w.off, values, n_need, w.u);
+    }
+    cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need);
+    // clusters -> orthonormal blocks: Gram, per-cluster Cholesky (block-diagonal
+    // R^{-1}), update
+    {
+        int rc = bk_gram_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work, stream);
+        if (rc) return rc;
+        BK_RET(cudaMemsetAsync(w.m, 0, sizeof(double) * n_need * n_need, s));
+        // Schur complement in shared memory for clusters up to smax columns
+        int smax = n_need < 160 ? n_need : 160;
+        while (smax > 0 && static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8 > 28800) --smax;
+        const size_t gsm = sizeof(double) * (static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8);
+        static const cudaError_t ag = cudaFuncSetAttribute(group_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           226 * 1024);
+        BK_RET(ag);
+        group_chol_kernel<<<n_need, 1024, gsm, s>>>(n_need, w.gram, w.gstart, w.ngroups, w.m, w.scratch,
+                                                    w.ginfo, smax);
+        rc = bk_gemm_d(d, w.urm, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, w.u2rm, n_need, stream);
+        if (rc) return rc;
+    }
+    // two Newton-Schulz steps U <- U (3I - U^T U)/2: after the cluster step the
+    // columns are orthonormal to O(eps ||T|| / gap) (gap >= 1e-7 ||T|| between
+    // clusters), so the error squares twice to ~1e-16 — GEMM-only
+    for (int pass = 0; pass < 2; ++pass) {
+        double* src = pass == 0 ? w.u2rm : w.urm;
+        double* dst = pass == 0 ? w.urm : w.u2rm;
+        int rc = bk_gram_d(d, src, n_need, n_need, src, n_need, n_need, w.gram, n_need, gram_work, stream);
+        if (rc) return rc;
+        rc = bk_ns_coeff_d(n_need, w.gram, n_need, w.m, n_need, stream);
+        if (rc) return rc;
+        rc = bk_gemm_d(d, src, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, dst, n_need, stream);
+        if (rc) return rc;
+    }
+    std::swap(w.urm, w.u2rm);  // result in u2rm -> name it urm below
+    rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.urm, n_need, w.u);
+    BK_LAUNCHED();
+}
+
+// grid-cooperative tridiagonalisation (E = double or double2) of the sym/Hermitian
+// part of h into w.dg, w.off and reflectors (w.zv, w.ztau)
+template <class E>
+int coop_tridiag(int d, const double* h, int ldh, SyevWs& w, cudaStream_t s) {
+    sym_copy_kernel<E><<<max(1, min(ceil_div(d * d, 256), 8 * kSMs)), 256, 0, s>>>(
+        d, reinterpret_cast<const E*>(h), ldh, reinterpret_cast<E*>(w.za));
+    const size_t smem = 3 * static_cast<size_t>(d) * sizeof(E);
+    static const cudaError_t attr = prep_smem(tridiag_coop_kernel<E>, 3 * sizeof(E) * kSyevMaxD);
+    BK_RET(attr);
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        BK_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop_kernel<E>, kCoopThreads,
+                                                              3 * sizeof(E) * kSyevMaxD));
+        if (per_sm < 1) return static_cast<int>(cudaErrorLaunchOutOfResources);
+    }
+    int grid = max(1, min(ceil_div(d, kCoopThreads / 32), kSMs));
+    grid = min(grid, per_sm * kSMs);
+    int dd = d;
+    E* a = reinterpret_cast<E*>(w.za);
+    E* v = reinterpret_cast<E*>(w.zv);
+    E* t = reinterpret_cast<E*>(w.ztau);
+    E* pb = reinterpret_cast<E*>(w.zp);
+    E* pt = reinterpret_cast<E*>(w.zpart);
+    double* dg = w.dg;
+    double* off = w.off;
+    void* args[] = {&dd, &a, &v, &t, &dg, &off, &pb, &pt};
+    BK_RET(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tridiag_coop_kernel<E>), dim3(grid),
+                                       dim3(kCoopThreads), args, smem, s));
+    return 0;
+}
+
+template <class E>
+int backtr_cta(int d, int n_need, const SyevWs& w, E* z, int ldz, cudaStream_t s) {
+    const int blocks = ceil_div(n_need, 4);
+    const E* v = reinterpret_cast<const E*>(w.zv);
+    const E* t = reinterpret_cast<const E*>(w.ztau);
+    if (d <= 256)
+        backtr_cta_kernel<E, 1><<<blocks, 256, 0, s>>>(d, n_need, v, t, w.u, z, ldz);
+    else if (d <= 512)
+        backtr_cta_kernel<E, 2><<<blocks, 256, 0, s>>>(d, n_need, v, t, w.u, z, ldz);
+    else if (d <= 768)
+        backtr_cta_kernel<E, 3><<<blocks, 256, 0, s>>>(d, n_need, v, t, w.u, z, ldz);
+    else if (d <= 1024)
+        backtr_cta_kernel<E, 4><<<blocks, 256, 0, s>>>(d, n_need, v, t, w.u, z, ldz);
+    else
+        backtr_cta_kernel<E, 5><<<blocks, 256, 0, s>>>(d, n_need, v, t, w.u, z, ldz);
+    BK_LAUNCHED();
+}
+}  // namespace
+}  // namespace bk
 
 extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double* values, double* z, int ldz,
                              void* work, int* info, void* stream) {
@@ -833,51 +1072,25 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         if (e == cudaSuccess) launched = true;
         else (void)cudaGetLastError();  // cluster not schedulable: fall back below
     }
-    if (!launched) tridiag_fused_kernel<<<1, kTriThreads, smem, s>>>(d, h, ldh, w.a, w.vref, w.tau, w.dg, w.off);
-    bisect_kernel<<<ceil_div(n_need * 32, 256), 256, 0, s>>>(d, w.dg, w.off, n_need, values, w.e2);
-    group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
-    {
-        const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 4 * 4 * static_cast<size_t>(d));
-        static const cudaError_t ai = cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           static_cast<int>(sizeof(double) * 18 * kSyevMaxD));
-        BK_RET(ai);
-        invit_kernel<<<ceil_div(n_need * 32, 128), 128, ism, s>>>(d, w.dg, w.off, values, n_need, w.u);
+    bool coop = false;
+    if (!launched) {
+        if (d > 256) {
+            // large d: the grid-cooperative reduction (one grid sync per column)
+            const int rc = coop_tridiag<double>(d, h, ldh, w, s);
+            if (rc) return rc;
+            coop = true;
+        } else {
+            tridiag_fused_kernel<<<1, kTriThreads, smem, s>>>(d, h, ldh, w.a, w.vref, w.tau, w.dg, w.off);
+        }
     }
-    cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need);
-    // clusters -> orthonormal blocks: Gram, per-cluster Cholesky (block-diagonal
-    // R^{-1}), update
     {
-        int rc = bk_gram_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work, stream);
-        if (rc) return rc;
-        BK_RET(cudaMemsetAsync(w.m, 0, sizeof(double) * n_need * n_need, s));
-        // Schur complement in shared memory for clusters up to smax columns
-        int smax = n_need < 160 ? n_need : 160;
-        while (smax > 0 && static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8 > 28800) --smax;
-        const size_t gsm = sizeof(double) * (static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8);
-        static const cudaError_t ag = cudaFuncSetAttribute(group_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           226 * 1024);
-        BK_RET(ag);
-        group_chol_kernel<<<n_need, 1024, gsm, s>>>(n_need, w.gram, w.gstart, w.ngroups, w.m, w.scratch,
-                                                    w.ginfo, smax);
-        rc = bk_gemm_d(d, w.urm, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, w.u2rm, n_need, stream);
+        const int rc = tri_vectors(d, n_need, values, w, gram_work, stream);
         if (rc) return rc;
     }
-    // two Newton-Schulz steps U <- U (3I - U^T U)/2: after the cluster step the
-    // columns are orthonormal to O(eps ||T|| / gap) (gap >= 1e-7 ||T|| between
-    // clusters), so the error squares twice to ~1e-16 — GEMM-only
-    for (int pass = 0; pass < 2; ++pass) {
-        double* src = pass == 0 ? w.u2rm : w.urm;
-        double* dst = pass == 0 ? w.urm : w.u2rm;
-        int rc = bk_gram_d(d, src, n_need, n_need, src, n_need, n_need, w.gram, n_need, gram_work, stream);
+    if (coop) {
+        const int rc = backtr_cta<double>(d, n_need, w, z, ldz, s);
         if (rc) return rc;
-        rc = bk_ns_coeff_d(n_need, w.gram, n_need, w.m, n_need, stream);
-        if (rc) return rc;
-        rc = bk_gemm_d(d, src, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, dst, n_need, stream);
-        if (rc) return rc;
-    }
-    std::swap(w.urm, w.u2rm);  // result in u2rm -> name it urm below
-    rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.urm, n_need, w.u);
-    {
+    } else {
         const size_t bs = sizeof(double) * 8 * static_cast<size_t>(d);
         const int blocks = ceil_div(n_need, 8);
         static const cudaError_t ab4 = prep_smem(backtr_reg_kernel<4>, sizeof(double) * 8 * kSyevMaxD);
@@ -899,6 +1112,37 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         else
             backtr_kernel<<<ceil_div(n_need * 32, 128), 128, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
     }
+    BK_RET(cudaMemsetAsync(info, 0, 2 * sizeof(int), s));
+    BK_LAUNCHED();
+}
+
+// Complex Hermitian projected problem (config 5): h, z interleaved complex
+// row-major (ldh, ldz in complex elements); values real ascending.
+extern "C" size_t bk_syev_z_work_bytes(int d) { return carve(nullptr, nullptr, d > 0 ? d : 1); }
+
+extern "C" int bk_syev_z(int d, const double* h, int ldh, int n_need, double* values, double* z, int ldz, void* work,
+                         int* info, void* stream) {
+    if (d <= 0) return 0;
+    if (d > kSyevMaxD) return static_cast<int>(cudaErrorInvalidValue);
+    if (n_need <= 0 || n_need > d) n_need = d;
+    const cudaStream_t s = as_stream(stream);
+    SyevWs w;
+    const size_t total = carve(&w, work, d);
+    void* gram_work = static_cast<char*>(work) + total - ((bk_gram_work_bytes(d, d, d) + 255) & ~size_t(255));
+    if (d == 1) {
+        // 1x1: value = Re h, vector = 1
+        const double zero_one[2] = {1.0, 0.0};
+        BK_RET(cudaMemcpyAsync(values, h, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        BK_RET(cudaMemcpyAsync(z, zero_one, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
+        BK_RET(cudaMemsetAsync(info, 0, 2 * sizeof(int), s));
+        return 0;
+    }
+    int rc = coop_tridiag<double2>(d, h, ldh, w, s);
+    if (rc) return rc;
+    rc = tri_vectors(d, n_need, values, w, gram_work, stream);
+    if (rc) return rc;
+    rc = backtr_cta<double2>(d, n_need, w, reinterpret_cast<double2*>(z), ldz, s);
+    if (rc) return rc;
     BK_RET(cudaMemsetAsync(info, 0, 2 * sizeof(int), s));
     BK_LAUNCHED();
 }

@@ -281,15 +281,17 @@ __global__ void cg_check_kernel(int k, const double* rs, const double* bnorm, in
     if (threadIdx.x == 0) count[0] = cnt;
 }
 
+// sh = 1: complex columns as (re, im) pairs of the real view; the CG scalars
+// are per complex column (real for a Hermitian operator)
 __global__ void cg_step1_kernel(int n, int k, const double* rs, const double* pap, int* active, double* x,
                                 int ldx, double* r, int ldr, const double* p, int ldp, const double* ap,
-                                int ldap) {
+                                int ldap, int sh) {
     const int64_t total = static_cast<int64_t>(n) * k;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(e / k), c = static_cast<int>(e % k);
-        if (!active[c] || !(pap[c] > 0.0)) continue;
-        const double alpha = rs[c] / pap[c];
+        const int i = static_cast<int>(e / k), c = static_cast<int>(e % k), cs = c >> sh;
+        if (!active[cs] || !(pap[cs] > 0.0)) continue;
+        const double alpha = rs[cs] / pap[cs];
         x[static_cast<size_t>(i) * ldx + c] += alpha * p[static_cast<size_t>(i) * ldp + c];
         r[static_cast<size_t>(i) * ldr + c] -= alpha * ap[static_cast<size_t>(i) * ldap + c];
     }
@@ -301,13 +303,13 @@ __global__ void cg_deactivate_kernel(int k, const double* pap, int* active) {
 }
 
 __global__ void cg_step2_kernel(int n, int k, const double* rs, const double* rs_new, const int* active,
-                                const double* r, int ldr, double* p, int ldp) {
+                                const double* r, int ldr, double* p, int ldp, int sh) {
     const int64_t total = static_cast<int64_t>(n) * k;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(e / k), c = static_cast<int>(e % k);
-        if (!active[c]) continue;
-        const double beta = rs_new[c] / rs[c];
+        const int i = static_cast<int>(e / k), c = static_cast<int>(e % k), cs = c >> sh;
+        if (!active[cs]) continue;
+        const double beta = rs_new[cs] / rs[cs];
         double* pp = p + static_cast<size_t>(i) * ldp + c;
         *pp = r[static_cast<size_t>(i) * ldr + c] + beta * *pp;
     }
@@ -447,40 +449,60 @@ extern "C" int bk_cg_check_d(int k, const double* rs, const double* bnorm, int* 
     BK_LAUNCHED();
 }
 
-extern "C" int bk_cg_step1_d(int n, int k, const double* rs, const double* pap, int* active, double* x,
-                             int ldx, double* r, int ldr, const double* p, int ldp, const double* ap, int ldap,
-                             void* stream) {
+static int cg_step1(int n, int k, const double* rs, const double* pap, int* active, double* x, int ldx, double* r,
+                    int ldr, const double* p, int ldp, const double* ap, int ldap, void* stream, int sh) {
     if (n <= 0 || k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
-    cg_step1_kernel<<<elem_grid(static_cast<int64_t>(n) * k), 256, 0, s>>>(n, k, rs, pap, active, x, ldx, r,
-                                                                           ldr, p, ldp, ap, ldap);
+    const int kr = k << sh;
+    cg_step1_kernel<<<elem_grid(static_cast<int64_t>(n) * kr), 256, 0, s>>>(
+        n, kr, rs, pap, active, x, ldx << sh, r, ldr << sh, p, ldp << sh, ap, ldap << sh, sh);
     cg_deactivate_kernel<<<ceil_div(k, 256), 256, 0, s>>>(k, pap, active);
     BK_LAUNCHED();
 }
-
-extern "C" int bk_cg_step2_d(int n, int k, double* rs, const double* rs_new, const int* active,
-                             const double* r, int ldr, double* p, int ldp, void* stream) {
+static int cg_step2(int n, int k, double* rs, const double* rs_new, const int* active, const double* r, int ldr,
+                    double* p, int ldp, void* stream, int sh) {
     if (n <= 0 || k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
-    cg_step2_kernel<<<elem_grid(static_cast<int64_t>(n) * k), 256, 0, s>>>(n, k, rs, rs_new, active, r, ldr,
-                                                                           p, ldp);
+    const int kr = k << sh;
+    cg_step2_kernel<<<elem_grid(static_cast<int64_t>(n) * kr), 256, 0, s>>>(n, kr, rs, rs_new, active, r,
+                                                                            ldr << sh, p, ldp << sh, sh);
     cg_commit_rs<<<ceil_div(k, 256), 256, 0, s>>>(k, rs, rs_new, active);
     BK_LAUNCHED();
+}
+
+extern "C" int bk_cg_step1_d(int n, int k, const double* rs, const double* pap, int* active, double* x,
+                             int ldx, double* r, int ldr, const double* p, int ldp, const double* ap, int ldap,
+                             void* stream) {
+    return cg_step1(n, k, rs, pap, active, x, ldx, r, ldr, p, ldp, ap, ldap, stream, 0);
+}
+extern "C" int bk_cg_step1_z(int n, int k, const double* rs, const double* pap, int* active, double* x,
+                             int ldx, double* r, int ldr, const double* p, int ldp, const double* ap, int ldap,
+                             void* stream) {
+    return cg_step1(n, k, rs, pap, active, x, ldx, r, ldr, p, ldp, ap, ldap, stream, 1);
+}
+extern "C" int bk_cg_step2_d(int n, int k, double* rs, const double* rs_new, const int* active,
+                             const double* r, int ldr, double* p, int ldp, void* stream) {
+    return cg_step2(n, k, rs, rs_new, active, r, ldr, p, ldp, stream, 0);
+}
+extern "C" int bk_cg_step2_z(int n, int k, double* rs, const double* rs_new, const int* active,
+                             const double* r, int ldr, double* p, int ldp, void* stream) {
+    return cg_step2(n, k, rs, rs_new, active, r, ldr, p, ldp, stream, 1);
 }
 
 namespace bk {
 namespace {
 __global__ void cgs2_commit_kernel(int n, const double* __restrict__ v, const double* __restrict__ nrm2,
                                    const double* __restrict__ ref2, double drop, double* __restrict__ out, int ldo,
-                                   int* __restrict__ counter) {
-    // every block evaluates the (identical) decision; block 0 bumps the counter
+                                   int* __restrict__ counter, int cw) {
+    // every block evaluates the (identical) decision; block 0 bumps the counter.
+    // v: n x cw real view (cw = 2: one complex column), out: real view, ldo doubles
     const double r2 = *ref2, v2 = *nrm2;
     const bool keep = r2 > 0.0 && isfinite(v2) && sqrt(v2) >= drop * sqrt(r2);
     if (!keep) return;
     const int col = *counter;
     const double inv = 1.0 / sqrt(v2);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        out[static_cast<size_t>(i) * ldo + col] = v[i] * inv;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * cw; e += gridDim.x * blockDim.x)
+        out[static_cast<size_t>(e / cw) * ldo + col * cw + e % cw] = v[e] * inv;
 }
 __global__ void counter_bump(const double* __restrict__ nrm2, const double* __restrict__ ref2, double drop,
                              int* __restrict__ counter) {
@@ -493,7 +515,15 @@ __global__ void counter_bump(const double* __restrict__ nrm2, const double* __re
 extern "C" int bk_cgs2_commit_d(int n, const double* v, const double* nrm2, const double* ref2, double drop,
                                 double* out, int ldo, int* counter, void* stream) {
     const cudaStream_t s = as_stream(stream);
-    cgs2_commit_kernel<<<elem_grid(n), 256, 0, s>>>(n, v, nrm2, ref2, drop, out, ldo, counter);
+    cgs2_commit_kernel<<<elem_grid(n), 256, 0, s>>>(n, v, nrm2, ref2, drop, out, ldo, counter, 1);
+    counter_bump<<<1, 1, 0, s>>>(nrm2, ref2, drop, counter);
+    BK_LAUNCHED();
+}
+extern "C" int bk_cgs2_commit_z(int n, const double* v, const double* nrm2, const double* ref2, double drop,
+                                double* out, int ldo, int* counter, void* stream) {
+    const cudaStream_t s = as_stream(stream);
+    cgs2_commit_kernel<<<elem_grid(2 * static_cast<int64_t>(n)), 256, 0, s>>>(n, v, nrm2, ref2, drop, out, 2 * ldo,
+                                                                             counter, 2);
     counter_bump<<<1, 1, 0, s>>>(nrm2, ref2, drop, counter);
     BK_LAUNCHED();
 }

@@ -31,10 +31,13 @@ constexpr double kDropTol = 1e-8;  // kDropTolDefault, proj/src/kernel.hpp:17
 
 int round8(int x) { return (x + 7) & ~7; }
 
+// A block view: ld and column offsets count scalar elements; cw = 2 for
+// complex128 (interleaved (re, im) doubles), so column c starts at p + c*cw.
 struct Blk {
     double* p;
     int ld;
-    Blk at(int c) const { return {p + c, ld}; }
+    int cw;
+    Blk at(int c) const { return {p + static_cast<size_t>(c) * cw, ld, cw}; }
 };
 
 thread_local double g_host_call_s = 0.0;  // BLOCKEIG_TIMING: host time inside CUDA / bk_* calls
@@ -99,7 +102,7 @@ struct Stagnation {
 class Engine {
 public:
     Engine(const SparseSym& a, const SolverConfig& cfg, SolverKind kind)
-        : a_(a), cfg_(cfg), kind_(kind), n_(a.rows()), rng_(cfg.seed) {
+        : a_(a), cfg_(cfg), kind_(kind), n_(a.rows()), cw_(a.is_complex() ? 2 : 1), rng_(cfg.seed) {
         BKC(cudaSetDevice(cfg.device));
         csr_ = &a.device_csr(cfg.device, cfg.largest);
         BKC(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -112,32 +115,45 @@ public:
         ldS_ = round8(std::max(dcap_ + tcap_, 8));
         ldT_ = round8(std::max(tcap_, 8));
         const size_t n = static_cast<size_t>(std::max(n_, 1));
-        for (auto& s : S_) s.alloc(n * ldS_ * sizeof(double));
-        AS_.alloc(n * ldS_ * sizeof(double));
-        R_.alloc(n * ldT_ * sizeof(double));
-        XD_.alloc(n * ldT_ * sizeof(double));
-        T1_.alloc(n * ldT_ * sizeof(double));
-        T2_.alloc(n * ldT_ * sizeof(double));
-        PT_.alloc(n * ldT_ * sizeof(double));
-        VEC_.alloc(n * sizeof(double));
+        const size_t es = sizeof(double) * cw_;  // bytes per scalar element
+        for (auto& s : S_) s.alloc(n * ldS_ * es);
+        AS_.alloc(n * ldS_ * es);
+        R_.alloc(n * ldT_ * es);
+        XD_.alloc(n * ldT_ * es);
+        T1_.alloc(n * ldT_ * es);
+        T2_.alloc(n * ldT_ * es);
+        PT_.alloc(n * ldT_ * es);
+        VEC_.alloc(n * es);
         const size_t dc = static_cast<size_t>(dcap_) + tcap_;
         ldH_ = static_cast<int>(dc);
-        H_.alloc(dc * dc * sizeof(double));
-        Z_.alloc(dc * dc * sizeof(double));
-        ZC_.alloc(dc * dc * sizeof(double));
-        CZ_.alloc(dc * dc * sizeof(double));
+        H_.alloc(dc * dc * es);
+        Z_.alloc(dc * dc * es);
+        ZC_.alloc(dc * dc * es);
+        CZ_.alloc(dc * dc * es);
         VALS_.alloc(dc * sizeof(double));
-        COEF_.alloc(dc * static_cast<size_t>(tcap_) * sizeof(double) + 64);
-        GB_.alloc(static_cast<size_t>(tcap_) * tcap_ * sizeof(double));
-        M1_.alloc(static_cast<size_t>(tcap_) * tcap_ * sizeof(double));
-        M2_.alloc(static_cast<size_t>(tcap_) * tcap_ * sizeof(double));
+        COEF_.alloc(dc * static_cast<size_t>(tcap_) * es + 64);
+        GB_.alloc(static_cast<size_t>(tcap_) * tcap_ * es);
+        M1_.alloc(static_cast<size_t>(tcap_) * tcap_ * es);
+        M2_.alloc(static_cast<size_t>(tcap_) * tcap_ * es);
         SMALL_.alloc(8 * dc * sizeof(double));
         INFO_.alloc(64 * sizeof(int));
-        size_t work = bk_gram_work_bytes(n_, static_cast<int>(dc), static_cast<int>(dc));
-        work = std::max(work, bk_chol_work_bytes(std::max(tcap_, 1)));
-        work = std::max(work, bk_syev_work_bytes(static_cast<int>(dc)));
-        work = std::max(work, bk_residual_work_bytes(n_, static_cast<int>(dc)));
-        work = std::max(work, bk_colnorm2_work_bytes(n_, static_cast<int>(dc)));
+        const int idc = static_cast<int>(dc);
+        size_t work;
+        if (cw_ == 1) {
+            work = bk_gram_work_bytes(n_, idc, idc);
+            work = std::max(work, bk_chol_work_bytes(std::max(tcap_, 1)));
+            work = std::max(work, bk_syev_work_bytes(idc));
+            work = std::max(work, bk_residual_work_bytes(n_, idc));
+            work = std::max(work, bk_colnorm2_work_bytes(n_, idc));
+        } else {
+            if (dc > 1200) throw std::invalid_argument("complex solve: projected dimension exceeds 1200");
+            work = bk_gram_z_work_bytes(n_, idc, idc);
+            work = std::max(work, bk_chol_z_work_bytes(std::max(tcap_, 1)));
+            work = std::max(work, bk_syev_z_work_bytes(idc));
+            work = std::max(work, bk_residual_z_work_bytes(n_, idc));
+            work = std::max(work, bk_colnorm2_z_work_bytes(n_, idc));
+            CEXP_.alloc(bk_gemm_z_work_bytes(idc, idc));
+        }
         WORK_.alloc(work);
         if (cfg.precond == Precond::diagonal) {
             std::vector<double> t(n);
@@ -166,10 +182,11 @@ private:
     StrategyConfig strategy_;
     // ---------------------------------------------------------------- primitives
     void* st() const { return stream_; }
-    Blk S(int i) const { return {S_[i].d(), ldS_}; }
-    Blk AS() const { return {AS_.d(), ldS_}; }
-    Blk T1() const { return {T1_.d(), ldT_}; }
-    Blk T2() const { return {T2_.d(), ldT_}; }
+    Blk B(double* p, int ld) const { return {p, ld, cw_}; }
+    Blk S(int i) const { return B(S_[i].d(), ldS_); }
+    Blk AS() const { return B(AS_.d(), ldS_); }
+    Blk T1() const { return B(T1_.d(), ldT_); }
+    Blk T2() const { return B(T2_.d(), ldT_); }
 
     void sync() {
         const auto t0 = std::chrono::steady_clock::now();
@@ -265,25 +282,53 @@ private:
     void spmm(Blk x, int k, Blk y) {
         if (k <= 0) return;
         auto t = prof_begin();
-        BKC(bk_spmm_d(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
-                      y.ld, st()));
-        prof_end(t, K_SPMM, 12.0 * csr_->nnz_full + 4.0 * (n_ + 1) + 16.0 * n_ * k, 2.0 * csr_->nnz_full * k);
+        if (cw_ == 1)
+            BKC(bk_spmm_d(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
+                          y.ld, st()));
+        else
+            BKC(bk_spmm_z(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
+                          y.ld, st()));
+        // complex: nnz*(16+4) + (n+1)*4 + 2*n*k*16 bytes, 8*nnz*k flops
+        prof_end(t, K_SPMM, (8.0 * cw_ + 4.0) * csr_->nnz_full + 4.0 * (n_ + 1) + 16.0 * cw_ * n_ * k,
+                 2.0 * cw_ * cw_ * csr_->nnz_full * k);
     }
     // K2: flops 2*rows*a*b; bytes 8*rows*(a+b)
     void gram(int rows, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc) {
         auto t = prof_begin();
-        BKC(bk_gram_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), st()));
-        prof_end(t, K_GRAM, 8.0 * rows * (a + b), 2.0 * rows * a * b);
+        if (cw_ == 1)
+            BKC(bk_gram_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), st()));
+        else
+            BKC(bk_gram_z(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), st()));
+        prof_end(t, K_GRAM, 8.0 * cw_ * rows * (a + b), 2.0 * cw_ * cw_ * rows * a * b);
     }
     // K3: flops 2*rows*d*k; bytes 8*rows*(d + k (+k when beta != 0))
     void gemm(int rows, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
               double* y, int ldy) {
         auto t = prof_begin();
-        BKC(bk_gemm_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, st()));
-        prof_end(t, K_GEMM, 8.0 * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * rows * d * k);
+        if (cw_ == 1)
+            BKC(bk_gemm_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, st()));
+        else
+            BKC(bk_gemm_z(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, CEXP_.p(), st()));
+        prof_end(t, K_GEMM, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * cw_ * cw_ * rows * d * k);
     }
+    // column movement and elementwise ops work on the real view (cw doubles per element)
     void copy(int rows, Blk src, int k, Blk dst) {
-        if (k > 0 && rows > 0) BKO(bk_copy_cols_d(rows, src.p, src.ld, k, dst.p, dst.ld, st()));
+        if (k > 0 && rows > 0) BKO(bk_copy_cols_d(rows, src.p, src.ld * cw_, k * cw_, dst.p, dst.ld * cw_, st()));
+    }
+    void colnorm2(int rows, Blk x, int k, double* out) {
+        if (cw_ == 1) BKO(bk_colnorm2_d(rows, x.p, x.ld, k, out, WORK_.p(), st()));
+        else BKO(bk_colnorm2_z(rows, x.p, x.ld, k, out, WORK_.p(), st()));
+    }
+    void ns_coeff(int a, const double* g, int ldg, double* m, int ldm) {
+        if (cw_ == 1) BKO(bk_ns_coeff_d(a, g, ldg, m, ldm, st()));
+        else BKO(bk_ns_coeff_z(a, g, ldg, m, ldm, st()));
+    }
+    void scale_rows(int rows, int k, const double* t, Blk x, Blk y) {
+        BKO(bk_scale_rows_d(rows, k * cw_, t, x.p, x.ld * cw_, y.p, y.ld * cw_, st()));
+    }
+    void zero_rows(Blk x, int k, int r0, int r1) { BKO(bk_zero_rows_d(x.p, x.ld * cw_, k * cw_, r0, r1, st())); }
+    void lincomb(int rows, int k, double a, Blk x, double b, Blk y, Blk out) {
+        BKO(bk_lincomb_d(rows, k * cw_, a, x.p, x.ld * cw_, b, y.p, y.ld * cw_, out.p, out.ld * cw_, st()));
     }
 
     // host std::mt19937_64 / normal_distribution block (random_block,
@@ -292,7 +337,8 @@ private:
     void random_block(int cols, Blk dst) {
         if (cols <= 0) return;
         const auto t0 = std::chrono::steady_clock::now();
-        std::vector<double> h(static_cast<size_t>(n_) * cols);
+        // complex: real then imaginary part of each entry (random_block<complex>)
+        std::vector<double> h(static_cast<size_t>(n_) * cols * cw_);
         rng_.take(h.data(), h.size());
         upload_colmajor(h.data(), cols, dst);
         rng_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -301,10 +347,11 @@ private:
     double rng_s_ = 0.0;
     int64_t rng_cols_ = 0;
     void upload_colmajor(const double* h, int cols, Blk dst) {
-        const size_t bytes = static_cast<size_t>(n_) * cols * sizeof(double);
+        const size_t bytes = static_cast<size_t>(n_) * cols * sizeof(double) * cw_;
         if (stage_.bytes() < bytes) stage_.alloc(bytes);
         BKC(cudaMemcpyAsync(stage_.d(), h, bytes, cudaMemcpyHostToDevice, stream_));
-        BKC(bk_cm_to_rm_d(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
+        if (cw_ == 1) BKC(bk_cm_to_rm_d(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
+        else BKC(bk_cm_to_rm_z(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
         sync();  // the host buffer may be released by the caller
     }
 
@@ -314,7 +361,7 @@ private:
     int proj_ortho(int rows, Blk w, int a, Blk q, int m, Blk out) {
         if (a <= 0) return 0;
         double* ref2 = SMALL_.d();  // a doubles
-        BKO(bk_colnorm2_d(rows, w.p, w.ld, a, ref2, WORK_.p(), st()));
+        colnorm2(rows, w, a, ref2);
         if (m > 0)
             for (int pass = 0; pass < 2; ++pass) {
                 gram(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a);
@@ -323,23 +370,24 @@ private:
         gram(rows, w.p, w.ld, a, w.p, w.ld, a, GB_.d(), a);
         int* info = INFO_.as<int>();
         auto tc = prof_begin();
-        BKC(bk_chol_drop_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
-        prof_end(tc, K_CHOL, 8.0 * a * a, a * a * a / 3.0);
+        if (cw_ == 1) BKC(bk_chol_drop_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
+        else BKC(bk_chol_drop_z(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
+        prof_end(tc, K_CHOL, 8.0 * cw_ * a * a, cw_ * cw_ * a * a * a / 3.0);
         BKC(cudaMemcpyAsync(pin_.info, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         sync();
-        if (debug_) debug_pivots(a, ref2);
+        if (debug_ && cw_ == 1) debug_pivots(a, ref2);
         if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
         if (pin_.info[1]) return cgs2_fallback(rows, w, a, q, m, out);
         const int kept = pin_.info[0];
         if (kept == 0) return 0;
-        Blk pt{PT_.d(), ldT_};
+        Blk pt = B(PT_.d(), ldT_);
         gemm(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld);
         // second pass: the block is orthonormal to ~1e-8 after the pivot-checked
         // first pass (p >= 1e-8 g_jj bounds its condition), so one Newton-Schulz
         // step W1 (3I - G)/2 restores orthogonality to ~1e-16 without a second
         // sequential factorisation or host round trip
         gram(rows, pt.p, pt.ld, kept, pt.p, pt.ld, kept, GB_.d(), kept);
-        BKO(bk_ns_coeff_d(kept, GB_.d(), kept, M2_.d(), kept, st()));
+        ns_coeff(kept, GB_.d(), kept, M2_.d(), kept);
         gemm(rows, pt.p, pt.ld, kept, M2_.d(), kept, kept, 1.0, 0.0, out.p, out.ld);
         return kept;
     }
@@ -382,11 +430,11 @@ private:
         (void)m;
         ++fallbacks_;
         const double* ref2 = SMALL_.d();  // set by proj_ortho
-        Blk v{VEC_.d(), 1};
+        Blk v = B(VEC_.d(), 1);
         double* c = COEF_.d();
         double* nrm2 = SMALL_.d() + tcap_;
         int* counter = INFO_.as<int>() + 32;
-        BKO(bk_zero_rows_d(out.p, out.ld, a, 0, rows, st()));
+        zero_rows(out, a, 0, rows);
         BKC(cudaMemsetAsync(counter, 0, sizeof(int), stream_));
         for (int j = 0; j < a; ++j) {
             copy(rows, w.at(j), 1, v);
@@ -395,8 +443,9 @@ private:
                     gram(rows, out.p, out.ld, j, v.p, 1, 1, c, 1);
                     gemm(rows, out.p, out.ld, j, c, 1, 1, -1.0, 1.0, v.p, 1);
                 }
-            BKO(bk_colnorm2_d(rows, v.p, 1, 1, nrm2, WORK_.p(), st()));
-            BKO(bk_cgs2_commit_d(rows, v.p, nrm2, ref2 + j, kDropTol, out.p, out.ld, counter, st()));
+            colnorm2(rows, v, 1, nrm2);
+            if (cw_ == 1) BKO(bk_cgs2_commit_d(rows, v.p, nrm2, ref2 + j, kDropTol, out.p, out.ld, counter, st()));
+            else BKO(bk_cgs2_commit_z(rows, v.p, nrm2, ref2 + j, kDropTol, out.p, out.ld, counter, st()));
         }
         BKC(cudaMemcpyAsync(pin_.info + 13, counter, sizeof(int), cudaMemcpyDeviceToHost, stream_));
         sync();
@@ -426,14 +475,23 @@ private:
         spmm(s.at(as_from), d - as_from, AS().at(as_from));
         {  // H = S^T (A S): upper tiles only, mirrored (symmetrised by the eigensolver anyway)
             auto tg = prof_begin();
-            BKC(bk_gram_sym_d(n_, s.p, s.ld, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
-            // algorithmic flops of a symmetric Gram: n d (d + 1)
-            prof_end(tg, K_GRAM, 8.0 * n_ * 2 * d, 1.0 * n_ * d * (d + 1.0));
+            if (cw_ == 1) {
+                BKC(bk_gram_sym_d(n_, s.p, s.ld, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
+                // algorithmic flops of a symmetric Gram: n d (d + 1)
+                prof_end(tg, K_GRAM, 8.0 * n_ * 2 * d, 1.0 * n_ * d * (d + 1.0));
+            } else {
+                // complex: the full Gram (the Hermitian one-triangle form would count 4 n d (d + 1))
+                BKC(bk_gram_z(n_, s.p, s.ld, d, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
+                prof_end(tg, K_GRAM, 16.0 * n_ * 2 * d, 8.0 * n_ * d * d);
+            }
         }
         int* info = INFO_.as<int>() + 8;
         auto ts = prof_begin();
-        BKC(bk_syev_d(d, H_.d(), ldH_, n_need > 0 ? n_need : d, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
-        prof_end(ts, K_SYEV, 16.0 * d * d, 0.0);
+        if (cw_ == 1)
+            BKC(bk_syev_d(d, H_.d(), ldH_, n_need > 0 ? n_need : d, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
+        else
+            BKC(bk_syev_z(d, H_.d(), ldH_, n_need > 0 ? n_need : d, VALS_.d(), Z_.d(), ldH_, WORK_.p(), info, st()));
+        prof_end(ts, K_SYEV, 16.0 * cw_ * d * d, 0.0);
         BKC(cudaMemcpyAsync(pin_.info + 8, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         syev_pending_ = true;
     }
@@ -462,11 +520,15 @@ private:
         double* rn2 = SMALL_.d();
         double* vn2 = SMALL_.d() + dcap_ + tcap_;
         auto tr = prof_begin();
-        BKC(bk_residual_d(n_, v.p, v.ld, AS_.d(), ldS_, VALS_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0, rn2,
-                          vn2, WORK_.p(), st()));
+        if (cw_ == 1)
+            BKC(bk_residual_d(n_, v.p, v.ld, AS_.d(), ldS_, VALS_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0, rn2,
+                              vn2, WORK_.p(), st()));
+        else
+            BKC(bk_residual_z(n_, v.p, v.ld, AS_.d(), ldS_, VALS_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0, rn2,
+                              vn2, WORK_.p(), st()));
         double* rec = SMALL_.d() + 2 * (dcap_ + tcap_);
         BKC(bk_convergence_d(k, rn2, vn2, VALS_.d(), norm_a_, n_ev, cfg_.tol, nullptr, rec, st()));
-        prof_end(tr, K_RESID, 24.0 * n_ * k, 6.0 * n_ * k);
+        prof_end(tr, K_RESID, 24.0 * cw_ * n_ * k, 6.0 * cw_ * n_ * k);
         BKC(cudaMemcpyAsync(pin_.rec, rec, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         sync();
         check_syev();
@@ -483,7 +545,7 @@ private:
                 spmm(x, k, T2());
                 ax_known = T2();
             }
-            BKO(bk_lincomb_d(n_, k, cfg_.op_c, x.p, x.ld, -1.0, ax_known.p, ax_known.ld, y.p, y.ld, st()));
+            lincomb(n_, k, cfg_.op_c, x, -1.0, ax_known, y);
             return;
         }
         // (A - zeta I)^{-1} = M M^T with M = R^{-1} from the dense Cholesky
@@ -503,8 +565,10 @@ private:
         out_.status = status;
         out_.values.resize(n_ev);
         BKC(cudaMemcpyAsync(out_.values.data(), VALS_.d(), n_ev * sizeof(double), cudaMemcpyDeviceToHost, stream_));
-        BKC(bk_rm_to_cm_d(n_, n_ev, v.p, v.ld, PT_.d(), n_, st()));
-        out_.vectors.resize(static_cast<size_t>(n_) * n_ev);
+        if (cw_ == 1) BKC(bk_rm_to_cm_d(n_, n_ev, v.p, v.ld, PT_.d(), n_, st()));
+        else BKC(bk_rm_to_cm_z(n_, n_ev, v.p, v.ld, PT_.d(), n_, st()));
+        out_.complex_vectors = cw_ == 2;
+        out_.vectors.resize(static_cast<size_t>(n_) * n_ev * cw_);
         BKC(cudaMemcpyAsync(out_.vectors.data(), PT_.d(), out_.vectors.size() * sizeof(double),
                             cudaMemcpyDeviceToHost, stream_));
         sync();
@@ -540,12 +604,13 @@ private:
     SolverConfig cfg_;
     SolverKind kind_;
     int n_;
+    int cw_;  // doubles per scalar element: 1 real, 2 complex128
     NormalPairStream rng_;  // the reference's per-solve mt19937_64 normal stream, produced ahead
     const DeviceCsr* csr_ = nullptr;
     cudaStream_t stream_ = nullptr;
     int tcap_ = 0, dcap_ = 0, ldS_ = 0, ldT_ = 0, ldH_ = 0;
     DevMem S_[2], AS_, R_, XD_, T1_, T2_, PT_, VEC_, H_, Z_, ZC_, CZ_, VALS_, COEF_, GB_, M1_, M2_, SMALL_,
-        INFO_, WORK_, TD_, INV_, stage_;
+        INFO_, WORK_, TD_, INV_, stage_, CEXP_;
     DevMem CG_[6];
     Pinned pin_;
     double norm_a_ = 0.0;
@@ -567,6 +632,8 @@ void Engine::factor_shift_invert() {
     if (n_ > 2000)
         throw std::invalid_argument(
             "shift-and-invert SI is limited to n <= 2000 on the device build; use the shifted operator mode");
+    if (cw_ != 1)
+        throw std::invalid_argument("shift-and-invert SI: complex matrices need the shifted operator mode");
     const size_t nn = static_cast<size_t>(n_) * n_;
     std::vector<double> dense(nn, 0.0);
     const double sgn = cfg_.largest ? -1.0 : 1.0;
@@ -597,7 +664,7 @@ int Engine::initial_block(const double* x0, int x0_cols, Blk dst) {
         random_block(n_ex, T1());
     }
     meter_.ortho(n_, n_ex);
-    const int kept = proj_ortho(n_, T1(), n_ex, {nullptr, 0}, 0, dst);
+    const int kept = proj_ortho(n_, T1(), n_ex, B(nullptr, 0), 0, dst);
     if (x0 != nullptr && kept < n_ex) throw std::invalid_argument("initial block is rank deficient");
     if (kept < n_ex) fresh_cols(n_ex - kept, dst, kept);
     return n_ex;
@@ -614,7 +681,7 @@ void Engine::solve_si() {
     int n_now = n_ex;
     BlockSizer sizer(strategy_);
     Stagnation guard;
-    const Blk xd{XD_.d(), ldT_};
+    const Blk xd = B(XD_.d(), ldT_);
     for (int j = 1; j <= cfg_.max_iters; ++j) {
         meter_.begin_iteration();
         const Blk v = S(cur_);
@@ -648,7 +715,7 @@ void Engine::solve_si() {
             }
         }
         meter_.ortho(n_, ycols);
-        const int kept = proj_ortho(n_, T1(), ycols, {nullptr, 0}, 0, S(cur_));
+        const int kept = proj_ortho(n_, T1(), ycols, B(nullptr, 0), 0, S(cur_));
         if (kept < n_now) fresh_cols(n_now - kept, S(cur_), kept);
         rayleigh_ritz(S(cur_), n_now, 0);
         lift(S(cur_), n_now, Z_.d(), ldH_, n_now, S(1 - cur_));
@@ -673,7 +740,7 @@ void Engine::solve_sd() {
     cur_ ^= 1;
     int n_now = n_ex;
     BlockSizer sizer(strategy_);
-    const Blk xd{XD_.d(), ldT_};
+    const Blk xd = B(XD_.d(), ldT_);
     const double* td = TD_.bytes() ? TD_.d() : nullptr;
     for (int j = 1; j <= cfg_.max_iters; ++j) {
         meter_.begin_iteration();
@@ -703,7 +770,7 @@ void Engine::solve_sd() {
                 ev = Event::expand;
             }
         }
-        BKO(bk_scale_rows_d(n_, n_old, td, R_.d(), ldT_, T1().p, ldT_, st()));
+        scale_rows(n_, n_old, td, B(R_.d(), ldT_), T1());
         meter_.proj_ortho(n_, n_old, xb);
         const int kw = proj_ortho(n_, T1(), n_old, v, xb, v.at(xb));
         if (kw == 0) {
@@ -735,9 +802,9 @@ void Engine::solve_lobpcg() {
     cur_ ^= 1;
     int n_now = n_ex, np = 0, prev_lock = 0;
     BlockSizer sizer(strategy_);
-    const Blk xd{XD_.d(), ldT_};
+    const Blk xd = B(XD_.d(), ldT_);
     const double* td = TD_.bytes() ? TD_.d() : nullptr;
-    const Blk zc{ZC_.d(), ldH_}, cz{CZ_.d(), ldH_}, z{Z_.d(), ldH_};
+    const Blk zc = B(ZC_.d(), ldH_), cz = B(CZ_.d(), ldH_), z = B(Z_.d(), ldH_);
     for (int j = 1; j <= cfg_.max_iters; ++j) {
         meter_.begin_iteration();
         Blk s = S(cur_);
@@ -758,7 +825,7 @@ void Engine::solve_lobpcg() {
             np -= drop;
         }
         // W = T R(:, lock:) orthonormalised against [X, P]
-        BKO(bk_scale_rows_d(n_, active, td, R_.d() + lock, ldT_, T1().p, ldT_, st()));
+        scale_rows(n_, active, td, B(R_.d(), ldT_).at(lock), T1());
         int m = n_now + np;
         meter_.proj_ortho(n_, active, m);
         mark(0);
@@ -824,7 +891,7 @@ void Engine::solve_lobpcg() {
         const int ahl = n_now - lock;  // n_now is post-expansion here
         copy(ds, z, n_now, zc);
         copy(ds, z.at(lock), ahl, cz);
-        BKO(bk_zero_rows_d(cz.p, cz.ld, ahl, 0, n_now, st()));
+        zero_rows(cz, ahl, 0, n_now);
         mark(0);
         const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now));
         mark(4);
@@ -861,11 +928,11 @@ void Engine::solve_tracemin() {
     rayleigh_ritz(S(cur_), n_ex, 0);
     lift(S(cur_), n_ex, Z_.d(), ldH_, n_ex, S(1 - cur_));
     cur_ ^= 1;
-    const size_t blk = static_cast<size_t>(std::max(n_, 1)) * ldT_ * sizeof(double);
+    const size_t blk = static_cast<size_t>(std::max(n_, 1)) * ldT_ * sizeof(double) * cw_;
     for (int i = 0; i < 4; ++i) CG_[i].alloc(blk);
     CG_[4].alloc(8 * static_cast<size_t>(tcap_) * sizeof(double));
     CG_[5].alloc(static_cast<size_t>(tcap_) * sizeof(int) + 64);
-    const Blk cx{CG_[0].d(), ldT_}, cr{CG_[1].d(), ldT_}, cp{CG_[2].d(), ldT_}, cap{CG_[3].d(), ldT_};
+    const Blk cx = B(CG_[0].d(), ldT_), cr = B(CG_[1].d(), ldT_), cp = B(CG_[2].d(), ldT_), cap = B(CG_[3].d(), ldT_);
     double* rs = CG_[4].d();
     double* bnorm = rs + tcap_;
     double* pap = rs + 2 * tcap_;
@@ -873,7 +940,7 @@ void Engine::solve_tracemin() {
     int* act = CG_[5].as<int>();
     int n_now = n_ex;
     BlockSizer sizer(strategy_);
-    const Blk xd{XD_.d(), ldT_};
+    const Blk xd = B(XD_.d(), ldT_);
     for (int j = 1; j <= cfg_.max_iters; ++j) {
         meter_.begin_iteration();
         const Blk v = S(cur_);
@@ -890,11 +957,11 @@ void Engine::solve_tracemin() {
             gemm(n_, v.p, v.ld, k, COEF_.d(), k, k, -1.0, 1.0, u.p, u.ld);
         };
         // rhs = P_V R; x = 0; p = r = rhs
-        copy(n_, {R_.d(), ldT_}, k, cr);
+        copy(n_, B(R_.d(), ldT_), k, cr);
         project(cr);
-        BKO(bk_axpby_d(n_, k, 0.0, cr.p, cr.ld, 0.0, cx.p, cx.ld, st()));
+        BKO(bk_axpby_d(n_, k * cw_, 0.0, cr.p, cr.ld * cw_, 0.0, cx.p, cx.ld * cw_, st()));
         copy(n_, cr, k, cp);
-        BKO(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs, WORK_.p(), st()));
+        colnorm2(n_, cr, k, rs);
         std::vector<double> h_rs(k);
         BKC(cudaMemcpyAsync(h_rs.data(), rs, k * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         sync();
@@ -919,13 +986,19 @@ void Engine::solve_tracemin() {
             project(T2());
             spmm(T2(), k, cap);
             project(cap);
-            BKC(bk_coldot_d(n_, cp.p, cp.ld, cap.p, cap.ld, k, pap, WORK_.p(), st()));
-            BKC(bk_cg_step1_d(n_, k, rs, pap, act, cx.p, cx.ld, cr.p, cr.ld, cp.p, cp.ld, cap.p, cap.ld, st()));
-            BKO(bk_colnorm2_d(n_, cr.p, cr.ld, k, rs_new, WORK_.p(), st()));
-            BKC(bk_cg_step2_d(n_, k, rs, rs_new, act, cr.p, cr.ld, cp.p, cp.ld, st()));
+            if (cw_ == 1) {
+                BKC(bk_coldot_d(n_, cp.p, cp.ld, cap.p, cap.ld, k, pap, WORK_.p(), st()));
+                BKC(bk_cg_step1_d(n_, k, rs, pap, act, cx.p, cx.ld, cr.p, cr.ld, cp.p, cp.ld, cap.p, cap.ld, st()));
+            } else {
+                BKC(bk_coldot_z(n_, cp.p, cp.ld, cap.p, cap.ld, k, pap, WORK_.p(), st()));
+                BKC(bk_cg_step1_z(n_, k, rs, pap, act, cx.p, cx.ld, cr.p, cr.ld, cp.p, cp.ld, cap.p, cap.ld, st()));
+            }
+            colnorm2(n_, cr, k, rs_new);
+            if (cw_ == 1) BKC(bk_cg_step2_d(n_, k, rs, rs_new, act, cr.p, cr.ld, cp.p, cp.ld, st()));
+            else BKC(bk_cg_step2_z(n_, k, rs, rs_new, act, cr.p, cr.ld, cp.p, cp.ld, st()));
         }
         // y = V - delta
-        BKO(bk_lincomb_d(n_, k, 1.0, v.p, v.ld, -1.0, cx.p, cx.ld, T1().p, ldT_, st()));
+        lincomb(n_, k, 1.0, v, -1.0, cx, T1());
         Event ev = Event::none;
         int ycols = n_now;
         if (d == Decision::expand) {
@@ -940,7 +1013,7 @@ void Engine::solve_tracemin() {
             }
         }
         meter_.ortho(n_, ycols);
-        const int kept = proj_ortho(n_, T1(), ycols, {nullptr, 0}, 0, S(cur_));
+        const int kept = proj_ortho(n_, T1(), ycols, B(nullptr, 0), 0, S(cur_));
         if (kept < n_now) fresh_cols(n_now - kept, S(cur_), kept);
         rayleigh_ritz(S(cur_), n_now, 0);
         lift(S(cur_), n_now, Z_.d(), ldH_, n_now, S(1 - cur_));
@@ -999,7 +1072,6 @@ SolverConfig resolve_config(SolverConfig cfg, SolverKind kind, const StrategyCon
 SolveOutput solve(SolverKind kind, const SparseSym& a, const SolverConfig& cfg_in, const StrategyConfig& s,
                   const double* x0, int x0_cols) {
     const auto t0 = std::chrono::steady_clock::now();
-    if (a.is_complex()) throw std::invalid_argument("complex Hermitian solves are not available in this build");
     const SolverConfig cfg = resolve_config(cfg_in, kind, s, a.rows());
     Engine e(a, cfg, kind);
     e.set_strategy(s);

@@ -114,9 +114,15 @@ void host_spmv(const SparseSym& a, const std::vector<double>& x, std::vector<dou
     }
 }
 
-double host_nrm2(const std::vector<double>& v) {
+// complex: |z|^2 = re^2 + im^2 formed per element, then accumulated (the
+// oracle's nrm2 over std::complex entries), so the estimate is bit-identical
+double host_nrm2(const std::vector<double>& v, bool cplx) {
     double s = 0.0;
-    for (double x : v) s += x * x;
+    if (!cplx) {
+        for (double x : v) s += x * x;
+    } else {
+        for (size_t i = 0; i + 1 < v.size(); i += 2) s += v[i] * v[i] + v[i + 1] * v[i + 1];
+    }
     return std::sqrt(s);
 }
 
@@ -133,14 +139,14 @@ double SparseSym::norm_est() const {
     std::normal_distribution<double> dist(0.0, 1.0);
     std::vector<double> v(static_cast<size_t>(n_) * (complex_ ? 2 : 1));
     for (auto& x : v) x = dist(rng);
-    double nrm = host_nrm2(v);
+    double nrm = host_nrm2(v, complex_);
     if (nrm == 0.0) return 0.0;
     for (auto& x : v) x /= nrm;
     std::vector<double> w, t;
     for (int it = 0; it < 30; ++it) {
         host_spmv(*this, v, t);
         host_spmv(*this, t, w);
-        nrm = host_nrm2(w);
+        nrm = host_nrm2(w, complex_);
         if (nrm == 0.0) {
             norm_cache_->store(0.0, std::memory_order_relaxed);
             return 0.0;
@@ -148,7 +154,7 @@ double SparseSym::norm_est() const {
         for (size_t i = 0; i < v.size(); ++i) v[i] = w[i] / nrm;
     }
     host_spmv(*this, v, t);
-    const double est = host_nrm2(t);
+    const double est = host_nrm2(t, complex_);
     norm_cache_->store(est, std::memory_order_relaxed);
     return est;
 }

@@ -1,0 +1,230 @@
+"""complex128 (Hermitian) path on the B200 — config 5's data type.
+
+The reference is real-only; the complex path is new and its
+oracle is the complex instantiation of the CPU restatement ("parity unpinned"
+for complex in DESIGN.md).  Kernel tests compare against numpy fp64/complex128;
+solver tests compare the product with the oracle on the same seeded inputs:
+eigenvalues within 1e-9 relative, residuals below tol, trajectory parity.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2409_05572_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+_D = C.c_void_p
+_I = C.c_int
+
+
+@pytest.fixture(scope="module")
+def bk(product):
+    f = product.lib
+    for name in ("bk_gram_z_work_bytes",):
+        getattr(f, name).restype = C.c_size_t
+        getattr(f, name).argtypes = [_I, _I, _I]
+    for name in ("bk_gemm_z_work_bytes", "bk_colnorm2_z_work_bytes", "bk_residual_z_work_bytes"):
+        getattr(f, name).restype = C.c_size_t
+        getattr(f, name).argtypes = [_I, _I]
+    for name in ("bk_syev_z_work_bytes", "bk_chol_z_work_bytes"):
+        getattr(f, name).restype = C.c_size_t
+        getattr(f, name).argtypes = [_I]
+    f.bk_gram_z.argtypes = [_I, _D, _I, _I, _D, _I, _I, _D, _I, _D, _D]
+    f.bk_gemm_z.argtypes = [_I, _D, _I, _I, _D, _I, _I, C.c_double, C.c_double, _D, _I, _D, _D]
+    f.bk_colnorm2_z.argtypes = [_I, _D, _I, _I, _D, _D, _D]
+    f.bk_syev_z.argtypes = [_I, _D, _I, _I, _D, _D, _I, _D, _D, _D]
+    f.bk_chol_drop_z.argtypes = [_I, _D, _I, _D, C.c_double, _D, _I, _D, _D, _D]
+    f.bk_spmm_z.argtypes = [_I, _D, _D, _D, _D, _I, _I, _D, _I, _D]
+    return f
+
+
+def dev(x):
+    x = np.ascontiguousarray(x)
+    if np.iscomplexobj(x):
+        x = x.view(np.float64)
+    return torch.as_tensor(x, device="cuda")
+
+
+def host_c(t, shape):
+    return t.cpu().numpy().view(np.complex128).reshape(shape)
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def crandn(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def zeros_c(*shape):
+    return torch.zeros(shape[:-1] + (2 * shape[-1],), dtype=torch.float64, device="cuda")
+
+
+def work(nbytes):
+    return torch.empty(nbytes // 8 + 1, dtype=torch.float64, device="cuda")
+
+
+@pytest.mark.parametrize("n,a,b", [(5000, 37, 53), (20000, 96, 96), (777, 1, 5)])
+def test_gram_z(bk, n, a, b):
+    rng = np.random.default_rng(n + a)
+    x, y = crandn(rng, n, a), crandn(rng, n, b)
+    c = zeros_c(a, b)
+    ws = work(bk.bk_gram_z_work_bytes(n, a, b))
+    assert bk.bk_gram_z(n, ptr(dev(x)), a, a, ptr(dev(y)), b, b, ptr(c), b, ptr(ws), stream()) == 0
+    torch.cuda.synchronize()
+    ref = x.conj().T @ y
+    # fp64 accumulation over n terms: 1e-13 relative to the entry scale sqrt(n)
+    assert np.abs(host_c(c, (a, b)) - ref).max() < 1e-13 * n
+
+
+@pytest.mark.parametrize("n,d,k", [(5000, 40, 24), (3000, 96, 160)])
+def test_gemm_z(bk, n, d, k):
+    rng = np.random.default_rng(d * k)
+    x, cm, y0 = crandn(rng, n, d), crandn(rng, d, k), crandn(rng, n, k)
+    y = dev(y0)
+    ws = work(bk.bk_gemm_z_work_bytes(d, k))
+    assert bk.bk_gemm_z(n, ptr(dev(x)), d, d, ptr(dev(cm)), k, k, -1.0, 1.0, ptr(y), k, ptr(ws), stream()) == 0
+    torch.cuda.synchronize()
+    ref = y0 - x @ cm
+    assert np.abs(host_c(y, (n, k)) - ref).max() < 1e-12 * d
+
+
+def test_colnorm2_z(bk):
+    rng = np.random.default_rng(3)
+    n, k = 10000, 33
+    x = crandn(rng, n, k)
+    out = torch.zeros(k, dtype=torch.float64, device="cuda")
+    ws = work(bk.bk_colnorm2_z_work_bytes(n, k))
+    assert bk.bk_colnorm2_z(n, ptr(dev(x)), k, k, ptr(out), ptr(ws), stream()) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy(), np.sum(np.abs(x) ** 2, axis=0), rtol=1e-13)
+
+
+def herm(rng, d, lam):
+    q, _ = np.linalg.qr(crandn(rng, d, d))
+    return (q * lam) @ q.conj().T
+
+
+@pytest.mark.parametrize("d,need", [(2, 2), (17, 17), (120, 40), (300, 100), (700, 260)])
+def test_syev_z(bk, d, need):
+    rng = np.random.default_rng(d)
+    lam = np.sort(rng.uniform(-3, 9, d))
+    lam[5:9] = lam[5] if d > 9 else lam[5:9]  # an exact 4-fold multiplet
+    h = herm(rng, d, lam)
+    vals = torch.zeros(d, dtype=torch.float64, device="cuda")
+    z = zeros_c(d, d)
+    ws = work(bk.bk_syev_z_work_bytes(d))
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    assert bk.bk_syev_z(d, ptr(dev(h)), d, need, ptr(vals), ptr(z), d, ptr(ws), ptr(info), stream()) == 0
+    torch.cuda.synchronize()
+    v = vals.cpu().numpy()[:need]
+    zz = host_c(z, (d, d))[:, :need]
+    scale = np.abs(lam).max()
+    np.testing.assert_allclose(v, np.sort(lam)[:need], atol=1e-12 * scale * max(1, d / 50))
+    assert np.abs(zz.conj().T @ zz - np.eye(need)).max() < 1e-12
+    assert np.linalg.norm(h @ zz - zz * v, axis=0).max() < 1e-12 * scale * max(1, d / 50)
+
+
+def _chol_z(bk, w):
+    a = w.shape[1]
+    g = w.conj().T @ w
+    ref2 = np.sum(np.abs(w) ** 2, axis=0)
+    m = zeros_c(a, a)
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    ws = work(bk.bk_chol_z_work_bytes(a))
+    assert bk.bk_chol_drop_z(a, ptr(dev(g)), a, ptr(dev(ref2)), 1e-8, ptr(m), a, ptr(info), ptr(ws),
+                             stream()) == 0
+    torch.cuda.synchronize()
+    return host_c(m, (a, a)), [int(i) for i in info.cpu()]
+
+
+def test_chol_drop_z(bk):
+    # a zero column is dropped with certainty (pair-locked: re and im twins
+    # together); a well-separated column is kept; the rest is orthonormalised
+    rng = np.random.default_rng(11)
+    n, a = 4000, 24
+    w = crandn(rng, n, a)
+    w[:, 9] = 0.0
+    w[:, 15] = 1e-3 * w[:, 15] + w[:, 14]
+    m, info = _chol_z(bk, w)
+    kept, unsure, bad = info[:3]
+    assert kept == a - 1 and unsure == 0 and bad == 0
+    assert np.abs(m[9]).max() == 0.0
+    q = w @ m[:, :kept]
+    assert np.abs(q.conj().T @ q - np.eye(kept)).max() < 1e-8  # one CholQR pass (NS polish follows)
+    # an exactly dependent column cannot be decided from the Gram: reported as
+    # uncertain so the driver re-runs the block with column CGS2
+    w[:, 7] = (1 + 2j) * w[:, 3] - 0.5j * w[:, 1]
+    _, info = _chol_z(bk, w)
+    assert info[1] == 1
+
+
+def test_spmm_z_magnetic(bk, oracle):
+    rp, col, val = W.magnetic(32, 1.0 / 16)
+    n = 32 * 32
+    full = W.full_from_lower(n, rp, col, val)
+    rng = np.random.default_rng(5)
+    k = 19
+    x = crandn(rng, n, k)
+    y = zeros_c(n, k)
+    f_rp = dev(full.indptr.astype(np.int32))
+    f_col = dev(full.indices.astype(np.int32))
+    f_val = dev(full.data.astype(np.complex128))
+    assert bk.bk_spmm_z(n, ptr(f_rp), ptr(f_col), ptr(f_val), ptr(dev(x)), k, k, ptr(y), k, stream()) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(host_c(y, (n, k)), full @ x, atol=1e-13 * 8 * np.abs(x).max())
+
+
+def disordered_magnetic(side, phi, w, seed):
+    """Magnetic Laplacian plus a random on-site potential: a Hermitian test matrix
+    without the Landau-level degeneracy (so vectors and trajectories are defined)."""
+    rp, col, val = W.magnetic(side, phi)
+    n = side * side
+    val = val.copy()
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    pot = np.random.default_rng(seed).uniform(-w / 2, w / 2, n)
+    val[col == rows] += pot
+    return n, rp, col, val
+
+
+@pytest.mark.parametrize("solver", ["lobpcg", "sd", "si"])
+def test_complex_solvers_match_oracle(product, oracle, solver):
+    n, rp, col, val = disordered_magnetic(24, 1.0 / 8, 2.0, 7)
+    kw = dict(n_ev=6, tol=1e-9, max_iters=3000, seed=3)
+    ext = {}
+    if solver == "si":
+        ext = dict(op_mode=1, op_shift=9.0)
+    out = []
+    for L in (product, oracle):
+        a = L.from_csr(n, rp, col, val)
+        out.append(L.solve(a, solver, strategy=L.strategy_config("fix"), ext=L.solve_ext(**ext) if ext else None,
+                           **kw))
+    g, o = out
+    assert g.status == o.status == 0
+    np.testing.assert_allclose(g.values, o.values, rtol=1e-9)
+    full = W.full_from_lower(n, rp, col, val).toarray()
+    ev = np.linalg.eigvalsh(full)[:6]
+    np.testing.assert_allclose(g.values, ev, rtol=1e-9)
+    v = g.vectors
+    assert np.iscomplexobj(v)
+    na = product.from_csr(n, rp, col, val).norm_est()
+    assert na == oracle.from_csr(n, rp, col, val).norm_est()  # bit-identical host estimate
+    r = full @ v - v * g.values
+    for i in range(6):
+        assert np.linalg.norm(r[:, i]) <= 2 * 1e-9 * (na + abs(g.values[i])) * np.linalg.norm(v[:, i])
+    assert np.abs(v.conj().T @ v - np.eye(6)).max() < 1e-10
+    # SD keeps W columns whose remaining norm sits at the 1e-8 drop threshold for
+    # hundreds of iterations here (most of its orthonormalisations take the
+    # exact-CGS2 route), so threshold decisions flip with rounding and its
+    # iteration count is only bounded (parity); the others are close
+    slack = o.iterations // 2 if solver == "sd" else max(2, o.iterations // 10)
+    assert abs(g.iterations - o.iterations) <= slack, (g.iterations, o.iterations)
