@@ -146,7 +146,6 @@ public:
             work = std::max(work, bk_residual_work_bytes(n_, idc));
             work = std::max(work, bk_colnorm2_work_bytes(n_, idc));
         } else {
-            if (dc > 1200) throw std::invalid_argument("complex solve: projected dimension exceeds 1200");
             work = bk_gram_z_work_bytes(n_, idc, idc);
             work = std::max(work, bk_chol_z_work_bytes(std::max(tcap_, 1)));
             work = std::max(work, bk_syev_z_work_bytes(idc));
@@ -485,6 +484,7 @@ private:
                 prof_end(tg, K_GRAM, 16.0 * n_ * 2 * d, 8.0 * n_ * d * d);
             }
         }
+        if (d > 1200) throw std::runtime_error("Rayleigh-Ritz dimension exceeds the device eigensolver limit (1200)");
         int* info = INFO_.as<int>() + 8;
         auto ts = prof_begin();
         if (cw_ == 1)
