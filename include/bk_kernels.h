@@ -174,6 +174,10 @@ BK_API int bk_cgs2_commit_d(int n, const double* v, const double* nrm2, const do
 BK_API size_t bk_gram_z_work_bytes(int n, int a, int b);
 BK_API int bk_gram_z(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
                      int ldc, void* work, void* stream);
+/* Hermitian H = X^H Y (d x d) when X^H Y is known to be Hermitian (Rayleigh-Ritz):
+ * upper tiles only; work: bk_gram_z_work_bytes(n, d, d) */
+BK_API int bk_gram_sym_z(int n, const double* x, int ldx, const double* y, int ldy, int d, double* c, int ldc,
+                         void* work, void* stream);
 BK_API size_t bk_gemm_z_work_bytes(int d, int k);
 BK_API int bk_gemm_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
                      double beta, double* y, int ldy, void* work, void* stream);

@@ -160,6 +160,21 @@ extern "C" int bk_gram_z(int n, const double* x, int ldx, int a, const double* y
     BK_LAUNCHED();
 }
 
+// Hermitian Rayleigh-Ritz matrix H = S^H (A S): the real symmetric-tile Gram
+// of the real views computes only the 96 x 96 tiles on and above the diagonal
+// and mirrors the rest by transposition; the combine step then yields exactly
+// C[p][q] = conj(C[q][p]) below the diagonal tiles (4 n d (d+1)-class flops)
+extern "C" int bk_gram_sym_z(int n, const double* x, int ldx, const double* y, int ldy, int d, double* c, int ldc,
+                             void* work, void* stream) {
+    if (d <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    double* gp = reinterpret_cast<double*>(static_cast<char*>(work) + align256(bk_gram_work_bytes(n, 2 * d, 2 * d)));
+    int rc = bk_gram_sym_d(n, x, 2 * ldx, y, 2 * ldy, 2 * d, gp, 2 * d, work, stream);
+    if (rc) return rc;
+    gram_combine_kernel<<<small_grid(static_cast<int64_t>(d) * d), 256, 0, s>>>(d, d, gp, c, ldc);
+    BK_LAUNCHED();
+}
+
 extern "C" size_t bk_gemm_z_work_bytes(int d, int k) { return 4 * static_cast<size_t>(d > 0 ? d : 1) * (k > 0 ? k : 1) * sizeof(double); }
 
 extern "C" int bk_gemm_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,

@@ -479,9 +479,9 @@ private:
                 // algorithmic flops of a symmetric Gram: n d (d + 1)
                 prof_end(tg, K_GRAM, 8.0 * n_ * 2 * d, 1.0 * n_ * d * (d + 1.0));
             } else {
-                // complex: the full Gram (the Hermitian one-triangle form would count 4 n d (d + 1))
-                BKC(bk_gram_z(n_, s.p, s.ld, d, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
-                prof_end(tg, K_GRAM, 16.0 * n_ * 2 * d, 8.0 * n_ * d * d);
+                // complex Hermitian: upper tiles only, 4 n d (d + 1) flops
+                BKC(bk_gram_sym_z(n_, s.p, s.ld, AS_.d(), ldS_, d, H_.d(), ldH_, WORK_.p(), st()));
+                prof_end(tg, K_GRAM, 16.0 * n_ * 2 * d, 4.0 * n_ * d * (d + 1.0));
             }
         }
         if (d > 1200) throw std::runtime_error("Rayleigh-Ritz dimension exceeds the device eigensolver limit (1200)");

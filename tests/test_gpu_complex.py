@@ -34,6 +34,7 @@ def bk(product):
         getattr(f, name).restype = C.c_size_t
         getattr(f, name).argtypes = [_I]
     f.bk_gram_z.argtypes = [_I, _D, _I, _I, _D, _I, _I, _D, _I, _D, _D]
+    f.bk_gram_sym_z.argtypes = [_I, _D, _I, _D, _I, _I, _D, _I, _D, _D]
     f.bk_gemm_z.argtypes = [_I, _D, _I, _I, _D, _I, _I, C.c_double, C.c_double, _D, _I, _D, _D]
     f.bk_colnorm2_z.argtypes = [_I, _D, _I, _I, _D, _D, _D]
     f.bk_syev_z.argtypes = [_I, _D, _I, _I, _D, _D, _I, _D, _D, _D]
@@ -84,6 +85,30 @@ def test_gram_z(bk, n, a, b):
     ref = x.conj().T @ y
     # fp64 accumulation over n terms: 1e-13 relative to the entry scale sqrt(n)
     assert np.abs(host_c(c, (a, b)) - ref).max() < 1e-13 * n
+
+
+@pytest.mark.parametrize("n,d", [(6000, 130), (3000, 47)])
+def test_gram_sym_z(bk, n, d):
+    # Rayleigh-Ritz form S^H (A S) with Hermitian A: upper tiles + Hermitian mirror
+    rng = np.random.default_rng(d)
+    s = crandn(rng, n, d)
+    b = crandn(rng, n, 8)
+    as_ = b @ (b.conj().T @ s) + 3.0 * s  # A = B B^H + 3 I, Hermitian
+    c = zeros_c(d, d)
+    ws = work(bk.bk_gram_z_work_bytes(n, d, d))
+    assert bk.bk_gram_sym_z(n, ptr(dev(s)), d, ptr(dev(as_)), d, d, ptr(c), d, ptr(ws), stream()) == 0
+    torch.cuda.synchronize()
+    h = host_c(c, (d, d))
+    ref = s.conj().T @ as_
+    assert np.abs(h - ref).max() < 1e-12 * np.abs(ref).max()
+    # tiles below the diagonal are exact Hermitian mirrors; diagonal tiles are
+    # computed, so Hermitian to rounding (the eigensolver symmetrises)
+    assert np.abs(h - h.conj().T).max() < 1e-13 * np.abs(ref).max()
+    t = 48  # complex entries per 96-wide real tile
+    for p in range(d):
+        for q in range(d):
+            if p // t > q // t:
+                assert h[p, q] == np.conj(h[q, p])
 
 
 @pytest.mark.parametrize("n,d,k", [(5000, 40, 24), (3000, 96, 160)])
