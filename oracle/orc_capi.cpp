@@ -390,6 +390,8 @@ int beig_result_diagnostics(const beig_result* r, int* cgs2_fallbacks, int* max_
     return BEIG_OK;
 }
 
+void beig_release_device_cache(void) {}  // no device memory in the oracle
+
 // ---- analysis checks: outside the hot path; not restated by the oracle ----
 int beig_theory_example3x3(beig_example3x3* out) {
     if (!out) return invalid("beig_theory_example3x3: null argument");

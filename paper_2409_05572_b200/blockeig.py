@@ -133,11 +133,12 @@ SYMBOLS = {
     "beig_result_seconds": (C.c_double, [_P]),
     "beig_result_kernel_stats": (C.c_int, [_P, C.c_int, C.POINTER(KernelStat)]),
     "beig_result_diagnostics": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "beig_release_device_cache": (None, []),
 }
 REFERENCE_SYMBOLS = [s for s in SYMBOLS if s not in (
     "beig_matrix_from_csr", "beig_zmatrix_from_csr", "beig_matrix_is_complex",
     "beig_solve_ext_default", "beig_solve_ex", "beig_result_vectors_z", "beig_result_seconds",
-    "beig_result_kernel_stats", "beig_result_diagnostics")]
+    "beig_result_kernel_stats", "beig_result_diagnostics", "beig_release_device_cache")]
 
 
 class BlockeigError(RuntimeError):

@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <utility>
 
 #include "bk_chol.cuh"
@@ -1049,7 +1050,8 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     size_t csmem = 0;
     const int C = tridiag_cluster_size(d, &csmem);
     bool launched = false;
-    if (C > 0) {
+    static const bool force_coop = getenv("BK_SYEV_COOP") != nullptr;  // tuning runs only
+    if (C > 0 && !force_coop) {
         static const cudaError_t a1 = cudaFuncSetAttribute(tridiag_cluster_kernel,
                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 8192);
         static const cudaError_t a2 =
@@ -1074,7 +1076,7 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     }
     bool coop = false;
     if (!launched) {
-        if (d > 256) {
+        if (d > 256 || force_coop) {
             // large d: the grid-cooperative reduction (one grid sync per column)
             const int rc = coop_tridiag<double>(d, h, ldh, w, s);
             if (rc) return rc;

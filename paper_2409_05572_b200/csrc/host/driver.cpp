@@ -612,7 +612,13 @@ private:
     DevMem S_[2], AS_, R_, XD_, T1_, T2_, PT_, VEC_, H_, Z_, ZC_, CZ_, VALS_, COEF_, GB_, M1_, M2_, SMALL_,
         INFO_, WORK_, TD_, INV_, stage_, CEXP_;
     DevMem CG_[6];
-    Pinned pin_;
+    // pinned staging is per host thread and outlives the solve (cudaFreeHost
+    // synchronises the device and costs ms per solve)
+    static Pinned& pinned() {
+        static thread_local Pinned* p = new Pinned;
+        return *p;
+    }
+    Pinned& pin_ = pinned();
     double norm_a_ = 0.0;
     Meter meter_;
     SolveOutput out_;
@@ -1073,10 +1079,19 @@ SolveOutput solve(SolverKind kind, const SparseSym& a, const SolverConfig& cfg_i
                   const double* x0, int x0_cols) {
     const auto t0 = std::chrono::steady_clock::now();
     const SolverConfig cfg = resolve_config(cfg_in, kind, s, a.rows());
-    Engine e(a, cfg, kind);
-    e.set_strategy(s);
-    SolveOutput out = e.run(x0, x0_cols);
+    SolveOutput out;
+    double t_setup = 0.0, t_run = 0.0;
+    {
+        Engine e(a, cfg, kind);
+        e.set_strategy(s);
+        t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out = e.run(x0, x0_cols);
+        t_run = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() - t_setup;
+    }
     out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (std::getenv("BLOCKEIG_TIMING"))
+        std::fprintf(stderr, "[blockeig] solve: setup %.4fs run %.4fs teardown %.4fs\n", t_setup, t_run,
+                     out.seconds - t_setup - t_run);
     return out;
 }
 

@@ -50,7 +50,7 @@ public:
     ~DevMem();
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
-    DevMem(DevMem&& o) noexcept : p_(o.p_), bytes_(o.bytes_) { o.p_ = nullptr, o.bytes_ = 0; }
+    DevMem(DevMem&& o) noexcept : p_(o.p_), bytes_(o.bytes_), dev_(o.dev_) { o.p_ = nullptr, o.bytes_ = 0; }
     void alloc(size_t bytes);
     template <class T> T* as() const { return static_cast<T*>(p_); }
     void* p() const { return p_; }
@@ -60,7 +60,11 @@ public:
 private:
     void* p_ = nullptr;
     size_t bytes_ = 0;
+    int dev_ = 0;
 };
+
+// empty the device block cache (see matrix.cpp)
+void release_device_cache();
 
 // ---------------------------------------------------------------- matrix
 // Lower-triangle CSR with the reference invariants (proj/src/matio.cpp:17-35):

@@ -7,6 +7,9 @@
 #include <cctype>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 #include <fstream>
 #include <sstream>
 #include <unordered_map>
@@ -20,18 +23,92 @@ void cuda_check(int code, const char* what) {
         throw CudaError(std::string(what) + ": " + cudaGetErrorString(static_cast<cudaError_t>(code)));
 }
 
+// ---------------------------------------------------------------- device block cache
+// Solves allocate their S / AS / work blocks (GBs) on entry and release them on
+// exit; cudaMalloc/cudaFree of that much costs 0.05-0.25 s per solve and
+// cudaFree synchronises the device.  Released blocks are kept per device and
+// reused best-fit (within 2x) by the next solve; on an allocation failure the
+// cache is emptied and the allocation retried.  BLOCKEIG_NO_CACHE=1 disables it;
+// beig_release_device_cache() empties it.  A block is only returned after its
+// owner synchronised its stream (Engine's destructor), so reuse is race-free.
+namespace {
+struct CachedBlock {
+    void* p;
+    size_t bytes;
+    int dev;
+};
+// never destroyed: handles released during process exit still return blocks safely
+std::mutex& g_cache_mu = *new std::mutex;
+std::vector<CachedBlock>& g_cache = *new std::vector<CachedBlock>;
+const bool g_cache_off = std::getenv("BLOCKEIG_NO_CACHE") != nullptr;
+
+void* cache_take(size_t bytes, size_t* got, int dev) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t best = g_cache.size();
+    for (size_t i = 0; i < g_cache.size(); ++i) {
+        const auto& b = g_cache[i];
+        if (b.dev == dev && b.bytes >= bytes && b.bytes <= 2 * bytes &&
+            (best == g_cache.size() || b.bytes < g_cache[best].bytes))
+            best = i;
+    }
+    if (best == g_cache.size()) return nullptr;
+    void* p = g_cache[best].p;
+    *got = g_cache[best].bytes;
+    g_cache.erase(g_cache.begin() + static_cast<std::ptrdiff_t>(best));
+    return p;
+}
+
+void cache_drop_all() {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& b : g_cache) {
+        cudaSetDevice(b.dev);
+        cudaFree(b.p);
+    }
+    cudaSetDevice(cur);
+    g_cache.clear();
+}
+}  // namespace
+
+void release_device_cache() { cache_drop_all(); }
+
 DevMem::~DevMem() {
-    if (p_) cudaFree(p_);
+    if (!p_) return;
+    if (g_cache_off) {
+        cudaFree(p_);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.push_back({p_, bytes_, dev_});
 }
 
 void DevMem::alloc(size_t bytes) {
     if (p_) {
-        cudaFree(p_);
+        DevMem old;
+        old.p_ = p_;
+        old.bytes_ = bytes_;
+        old.dev_ = dev_;
         p_ = nullptr;
         bytes_ = 0;
     }
     if (bytes == 0) return;
-    cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc");
+    cuda_check(cudaGetDevice(&dev_), "cudaGetDevice");
+    if (!g_cache_off) {
+        size_t got = 0;
+        if (void* p = cache_take(bytes, &got, dev_)) {
+            p_ = p;
+            bytes_ = got;
+            return;
+        }
+    }
+    cudaError_t e = cudaMalloc(&p_, bytes);
+    if (e == cudaErrorMemoryAllocation && !g_cache_off) {
+        (void)cudaGetLastError();
+        cache_drop_all();
+        e = cudaMalloc(&p_, bytes);
+    }
+    cuda_check(e, "cudaMalloc");
     bytes_ = bytes;
 }
 

@@ -117,4 +117,4 @@ if not only or "spmm" in only:
         ms = timeit(lambda: f.bk_spmm_d(wl.n, p(rp), p(ci), p(vv), p(x), 344, k, p(y), 344, S()))
         bytes_ = 12 * full.nnz + 4 * (wl.n + 1) + 16 * wl.n * k
         out[f"spmm_k{k}"] = {"ms": ms, "gbs": bytes_ / ms / 1e6}
-print(json.dumps(out, indent=1))
+print(json.dumps(out))
