@@ -163,7 +163,6 @@ GramPlan gram_plan(int n, int a, int b) {
     // tiles x splits must not exceed 2 x 148 or a straggler wave doubles the time
     int splits = max(1, (2 * kSMs) / tiles);
     splits = max(1, min(splits, ceil_div(n, 256)));  // >= 256 rows per split
-    splits = min(splits, 96);
     int rps = ceil_div(n, splits);
     rps = ceil_div(rps, GTK) * GTK;
     splits = max(1, ceil_div(n, rps));
@@ -258,10 +257,13 @@ cudaError_t prep(K kernel, size_t smem) {
 using namespace bk;
 
 extern "C" size_t bk_gram_work_bytes(int n, int a, int b) {
-    // enough for any tile count (the symmetric variant launches fewer tiles and
-    // therefore more splits): the one-tile plan has the most splits
-    const GramPlan p = gram_plan(max(n, 1), 1, 1);
-    return static_cast<size_t>(p.splits) * max(a, 1) * max(b, 1) * sizeof(double);
+    // partials = splits x a' x b' for any call with a' <= a, b' <= b: splits x
+    // tiles <= 2 x 148 (+ rounding) and a' b' <= tiles x 96^2 (x 2 for the
+    // symmetric variant, which launches only the upper tiles), and splits <=
+    // n / 256 + 1
+    const size_t cap = 2 * (2 * static_cast<size_t>(kSMs) + 8) * GTM * GTN;
+    const size_t small = (static_cast<size_t>(ceil_div(max(n, 1), 256)) + 1) * max(a, 1) * max(b, 1);
+    return std::min(cap, small) * sizeof(double);
 }
 
 namespace bk {

@@ -46,7 +46,7 @@ def timeit(fn, reps=20):
 out = {}
 n = 262144
 if not only or "gram" in only:
-    for a, b in [(288, 288), (192, 96), (96, 96), (96, 1)]:
+    for a, b in [(288, 288), (288, 96), (192, 96), (96, 96), (69, 69), (96, 1)]:
         x = torch.randn(n, 344, dtype=torch.float64, device="cuda")
         y = torch.randn(n, 344, dtype=torch.float64, device="cuda")
         c = torch.zeros(a, b, dtype=torch.float64, device="cuda")
