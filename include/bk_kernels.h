@@ -57,6 +57,19 @@ BK_API int bk_gram_sym_d(int n, const double* x, int ldx, const double* y, int l
 BK_API int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k,
                      double alpha, double beta, double* y, int ldy, void* stream);
 
+/* predicated launches: the kernels return at once unless *run_if != 0 (device
+ * flag), so a data-dependent step costs no host round trip */
+BK_API int bk_gram_if_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
+                        int ldc, void* work, const int* run_if, void* stream);
+BK_API int bk_gemm_if_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                        double beta, double* y, int ldy, const int* run_if, void* stream);
+/* K4 "twice is enough" test after the first projection pass (DGKS, eta^2 = eta2):
+ * flag[0] = 1 iff some column j has ||c_j||^2 > (1 - eta2) ||w_j||^2 (ref2), i.e.
+ * lost more than 1 - eta2 of its squared norm; c: m x a (ldc elements, cw = 1 real
+ * / 2 complex) */
+BK_API int bk_dgks_flag_d(int m, int a, const double* c, int ldc, int cw, const double* ref2, double eta2,
+                          int* flag, void* stream);
+
 /* ---- column sums of squares: out[j] = sum_i |X_ij|^2 (deterministic) ---- */
 BK_API size_t bk_colnorm2_work_bytes(int n, int k);
 BK_API int bk_colnorm2_d(int n, const double* x, int ldx, int k, double* out, void* work,
@@ -179,6 +192,10 @@ BK_API int bk_gram_z(int n, const double* x, int ldx, int a, const double* y, in
 BK_API int bk_gram_sym_z(int n, const double* x, int ldx, const double* y, int ldy, int d, double* c, int ldc,
                          void* work, void* stream);
 BK_API size_t bk_gemm_z_work_bytes(int d, int k);
+BK_API int bk_gram_if_z(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
+                        int ldc, void* work, const int* run_if, void* stream);
+BK_API int bk_gemm_if_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                        double beta, double* y, int ldy, void* work, const int* run_if, void* stream);
 BK_API int bk_gemm_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
                      double beta, double* y, int ldy, void* work, void* stream);
 BK_API size_t bk_colnorm2_z_work_bytes(int n, int k);

@@ -175,6 +175,29 @@ extern "C" int bk_gram_sym_z(int n, const double* x, int ldx, const double* y, i
     BK_LAUNCHED();
 }
 
+// predicated (device flag) variants for the second Gram-Schmidt pass
+extern "C" int bk_gram_if_z(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
+                            int ldc, void* work, const int* run_if, void* stream) {
+    if (a <= 0 || b <= 0 || n <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    double* gp = reinterpret_cast<double*>(static_cast<char*>(work) + align256(bk_gram_work_bytes(n, 2 * a, 2 * b)));
+    int rc = bk_gram_if_d(n, x, 2 * ldx, 2 * a, y, 2 * ldy, 2 * b, gp, 2 * b, work, run_if, stream);
+    if (rc) return rc;
+    gram_combine_kernel<<<small_grid(static_cast<int64_t>(a) * b), 256, 0, s>>>(a, b, gp, c, ldc);  // harmless if skipped
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_gemm_if_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                            double beta, double* y, int ldy, void* work, const int* run_if, void* stream) {
+    if (n <= 0 || k <= 0 || d <= 0) return 0;
+    const cudaStream_t s = as_stream(stream);
+    double* e = static_cast<double*>(work);
+    expand_kernel<<<small_grid(static_cast<int64_t>(d) * k), 256, 0, s>>>(d, k, c, ldc, e);
+    const int rc = static_cast<int>(cudaGetLastError());
+    if (rc) return rc;
+    return bk_gemm_if_d(n, x, 2 * ldx, 2 * d, e, 2 * k, 2 * k, alpha, beta, y, 2 * ldy, run_if, stream);
+}
+
 extern "C" size_t bk_gemm_z_work_bytes(int d, int k) { return 4 * static_cast<size_t>(d > 0 ? d : 1) * (k > 0 ? k : 1) * sizeof(double); }
 
 extern "C" int bk_gemm_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,

@@ -55,7 +55,9 @@ __device__ __forceinline__ void load_rows(double* dst, int pitch, const double* 
 template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16, bool SYM = false>
 __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double* __restrict__ x, int ldx, int a,
                                                              const double* __restrict__ y, int ldy, int b,
-                                                             double* __restrict__ out, int ldo, int rows_per_split) {
+                                                             double* __restrict__ out, int ldo, int rows_per_split,
+                                                             const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;  // device-side predication (bk_*_if_d)
     constexpr int NT = WM * WN * 32;
     constexpr int PX = TM + 4, PY = TN + 4;
     constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
@@ -138,7 +140,8 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
 // C[i][j] = sum_s work[s][i][j] in split order; with `sym`, entries of the
 // strictly-lower tiles (never computed) are mirrored from the upper ones
 __global__ void gram_reduce(int splits, int a, int b, const double* __restrict__ work, double* __restrict__ c,
-                            int ldc, int sym, int tile) {
+                            int ldc, int sym, int tile, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
     const int64_t total = static_cast<int64_t>(a) * b;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -174,7 +177,8 @@ template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16>
 __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(int n, const double* __restrict__ x, int ldx, int d,
                                                              const double* __restrict__ cm, int ldc, int k,
                                                              double alpha, double beta, double* __restrict__ y,
-                                                             int ldy) {
+                                                             int ldy, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
     constexpr int NT = WM * WN * 32;
     constexpr int PX = TK + 4, PC = TN + 4;
     constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
@@ -270,7 +274,7 @@ namespace bk {
 namespace {
 template <bool SYM>
 int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
-                void* work, cudaStream_t s) {
+                void* work, cudaStream_t s, const int* run_if = nullptr) {
     auto k16 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, true, SYM>;
     auto k8 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, false, SYM>;
     static const cudaError_t a1 = prep(k16, kGramSmem);
@@ -287,13 +291,13 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
     double* dst = direct ? c : w;
     const int ldo = direct ? ldc : b;
     if (aligned16(x, ldx) && aligned16(y, ldy))
-        k16<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
+        k16<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split, run_if);
     else
-        k8<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split);
+        k8<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split, run_if);
     if (!direct) {
         const int64_t total = static_cast<int64_t>(a) * b;
         gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
-            p.splits, a, b, w, c, ldc, SYM ? 1 : 0, GTM);
+            p.splits, a, b, w, c, ldc, SYM ? 1 : 0, GTM, run_if);
     }
     BK_LAUNCHED();
 }
@@ -319,14 +323,10 @@ extern "C" int bk_gram_sym_d(int n, const double* x, int ldx, const double* y, i
     return gram_launch<true>(n, x, ldx, d, y, ldy, d, c, ldc, work, s);
 }
 
-extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
-                         double beta, double* y, int ldy, void* stream) {
-    if (n <= 0 || k <= 0) return 0;
-    const cudaStream_t s = as_stream(stream);
-    if (d <= 0) {
-        if (beta == 1.0) return 0;
-        return bk_axpby_d(n, k, 0.0, y, ldy, beta, y, ldy, stream);
-    }
+namespace bk {
+namespace {
+int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
+                double* y, int ldy, cudaStream_t s, const int* run_if) {
     auto k16 = gemm_kernel<UTM, UTN, UTK, UWM, UWN, UST, true>;
     auto k8 = gemm_kernel<UTM, UTN, UTK, UWM, UWN, UST, false>;
     static const cudaError_t a1 = prep(k16, kGemmSmem);
@@ -335,8 +335,34 @@ extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c
     BK_RET(a2);
     const dim3 grid(ceil_div(n, UTM), ceil_div(k, UTN));
     if (aligned16(x, ldx))
-        k16<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy);
+        k16<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
     else
-        k8<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy);
+        k8<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
     BK_LAUNCHED();
+}
+}  // namespace
+}  // namespace bk
+
+extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                         double beta, double* y, int ldy, void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    if (d <= 0) {
+        if (beta == 1.0) return 0;
+        return bk_axpby_d(n, k, 0.0, y, ldy, beta, y, ldy, stream);
+    }
+    return gemm_launch(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, as_stream(stream), nullptr);
+}
+
+// predicated variants: the launch is unconditional (no host round trip), the
+// kernels return at once unless *run_if != 0 (device flag, e.g. bk_dgks_flag_d)
+extern "C" int bk_gram_if_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
+                            int ldc, void* work, const int* run_if, void* stream) {
+    if (a <= 0 || b <= 0 || n <= 0) return 0;
+    return gram_launch<false>(n, x, ldx, a, y, ldy, b, c, ldc, work, as_stream(stream), run_if);
+}
+
+extern "C" int bk_gemm_if_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                            double beta, double* y, int ldy, const int* run_if, void* stream) {
+    if (n <= 0 || k <= 0 || d <= 0) return 0;
+    return gemm_launch(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, as_stream(stream), run_if);
 }

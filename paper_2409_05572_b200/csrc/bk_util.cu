@@ -527,3 +527,38 @@ extern "C" int bk_cgs2_commit_z(int n, const double* v, const double* nrm2, cons
     counter_bump<<<1, 1, 0, s>>>(nrm2, ref2, drop, counter);
     BK_LAUNCHED();
 }
+
+// "Twice is enough" test (Daniel-Gragg-Kaufman-Stewart, eta = 1/sqrt(2)) for the
+// block Gram-Schmidt of K4: after pass 1, ||w_j - Q c_j||^2 = ||w_j||^2 - ||c_j||^2
+// (Q orthonormal), and pass 2 is only needed when some column lost more than
+// half its squared norm (eta2 = 1/2).  flag[0] = 1 requests pass 2; the pass-2
+// kernels are launched unconditionally and predicated on it (bk_*_if_d), so no
+// host round trip.  c: m x a coefficient block (ldc elements, cw = 2 complex).
+namespace bk {
+namespace {
+__global__ void dgks_flag_kernel(int m, int a, const double* __restrict__ c, int ldc, int cw,
+                                 const double* __restrict__ ref2, double eta2, int* __restrict__ flag) {
+    int need = 0;
+    for (int j = threadIdx.x; j < a; j += blockDim.x) {
+        double s = 0.0;
+        for (int l = 0; l < m; ++l)
+            for (int q = 0; q < cw; ++q) {
+                const double v = c[(static_cast<size_t>(l) * ldc + j) * cw + q];
+                s = fma(v, v, s);
+            }
+        const double r2 = ref2[j];
+        if (r2 > 0.0 && !(s <= (1.0 - eta2) * r2)) need = 1;  // NaN -> pass 2
+    }
+    need = __syncthreads_or(need);
+    if (threadIdx.x == 0) flag[0] = need;
+}
+}  // namespace
+}  // namespace bk
+
+extern "C" int bk_dgks_flag_d(int m, int a, const double* c, int ldc, int cw, const double* ref2, double eta2,
+                              int* flag, void* stream) {
+    const cudaStream_t s = as_stream(stream);
+    if (a <= 0) return static_cast<int>(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    dgks_flag_kernel<<<1, 256, 0, s>>>(m, a, c, ldc, cw, ref2, eta2, flag);
+    BK_LAUNCHED();
+}

@@ -227,6 +227,7 @@ private:
         int cls;
         cudaEvent_t a, b;
         double bytes, flops;
+        const int* pred;  // predicated launch: host copy of its device flag (valid at resolve)
     };
     std::vector<cudaEvent_t> ev_pool_;
     std::vector<Pending> pending_;
@@ -247,17 +248,21 @@ private:
         BKC(cudaEventRecord(e, stream_));
         return e;
     }
-    void prof_end(cudaEvent_t a, int cls, double bytes, double flops) {
+    void prof_end(cudaEvent_t a, int cls, double bytes, double flops, const int* pred = nullptr) {
         if (!a) return;
         cudaEvent_t b = take_event();
         BKC(cudaEventRecord(b, stream_));
-        pending_.push_back({cls, a, b, bytes, flops});
+        pending_.push_back({cls, a, b, bytes, flops, pred});
     }
     void prof_resolve() {
         for (size_t i = 0; i < pending_.size(); ++i) {
             auto& p = pending_[i];
             float ms = 0.f;
             BKC(cudaEventElapsedTime(&ms, p.a, p.b));
+            if (p.pred && *p.pred == 0) {  // predicated off: an empty launch, not K2/K3 work
+                p.cls = K_OTHER;
+                p.bytes = p.flops = 0.0;
+            }
             auto& k = kstats_[p.cls];
             k.launches += 1;
             k.ms += ms;
@@ -310,6 +315,23 @@ private:
             BKC(bk_gemm_z(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, CEXP_.p(), st()));
         prof_end(t, K_GEMM, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * cw_ * cw_ * rows * d * k);
     }
+    // predicated K2/K3 (run only when *flag != 0 on the device); the profile
+    // entry is resolved against the flag's host copy (pin_.info[3]) at the next sync
+    void gram_if(int rows, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
+                 const int* flag) {
+        auto t = prof_begin();
+        if (cw_ == 1) BKC(bk_gram_if_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), flag, st()));
+        else BKC(bk_gram_if_z(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), flag, st()));
+        prof_end(t, K_GRAM, 8.0 * cw_ * rows * (a + b), 2.0 * cw_ * cw_ * rows * a * b, &pin_.info[3]);
+    }
+    void gemm_if(int rows, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                 double beta, double* y, int ldy, const int* flag) {
+        auto t = prof_begin();
+        if (cw_ == 1) BKC(bk_gemm_if_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, flag, st()));
+        else BKC(bk_gemm_if_z(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, CEXP_.p(), flag, st()));
+        prof_end(t, K_GEMM, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * cw_ * cw_ * rows * d * k,
+                 &pin_.info[3]);
+    }
     // column movement and elementwise ops work on the real view (cw doubles per element)
     void copy(int rows, Blk src, int k, Blk dst) {
         if (k > 0 && rows > 0) BKO(bk_copy_cols_d(rows, src.p, src.ld * cw_, k * cw_, dst.p, dst.ld * cw_, st()));
@@ -361,19 +383,29 @@ private:
         if (a <= 0) return 0;
         double* ref2 = SMALL_.d();  // a doubles
         colnorm2(rows, w, a, ref2);
-        if (m > 0)
-            for (int pass = 0; pass < 2; ++pass) {
-                gram(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a);
-                gemm(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld);
-            }
+        int* info = INFO_.as<int>();  // [0..2] Cholesky info, [3] DGKS flag
+        if (m > 0) {
+            // the reference's CGS2 projects twice (kernel.cpp:73-80); the second
+            // block pass runs only when the first removed more than half of some
+            // column's squared norm ("twice is enough", DGKS eta = 1/sqrt 2) —
+            // decided on the device, the pass-2 kernels are predicated on it
+            gram(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a);
+            gemm(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld);
+            BKO(bk_dgks_flag_d(m, a, COEF_.d(), a, cw_, ref2, 0.5, info + 3, st()));
+            gram_if(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a, info + 3);
+            gemm_if(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld, info + 3);
+        } else {
+            BKC(cudaMemsetAsync(info + 3, 0, sizeof(int), stream_));
+        }
         gram(rows, w.p, w.ld, a, w.p, w.ld, a, GB_.d(), a);
-        int* info = INFO_.as<int>();
         auto tc = prof_begin();
         if (cw_ == 1) BKC(bk_chol_drop_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
         else BKC(bk_chol_drop_z(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
         prof_end(tc, K_CHOL, 8.0 * cw_ * a * a, cw_ * cw_ * a * a * a / 3.0);
-        BKC(cudaMemcpyAsync(pin_.info, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        BKC(cudaMemcpyAsync(pin_.info, info, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         sync();
+        pass2_ += pin_.info[3];
+        ++proj_calls_;
         if (debug_ && cw_ == 1) debug_pivots(a, ref2);
         if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
         if (pin_.info[1]) return cgs2_fallback(rows, w, a, q, m, out);
@@ -579,6 +611,9 @@ private:
         out_.work.rr_dim = meter_.iter_rr_dim;
         out_.rr_flops = meter_.rr_flops;
         out_.cgs2_fallbacks = fallbacks_;
+        if (std::getenv("BLOCKEIG_TIMING"))
+            std::fprintf(stderr, "[blockeig] second Gram-Schmidt pass taken in %lld of %lld orthonormalisations\n",
+                         static_cast<long long>(pass2_), static_cast<long long>(proj_calls_));
         out_.max_jacobi_sweeps = max_sweeps_;
         if (std::getenv("BLOCKEIG_TIMING"))
             std::fprintf(stderr,
@@ -623,6 +658,7 @@ private:
     Meter meter_;
     SolveOutput out_;
     int fallbacks_ = 0, max_sweeps_ = 0;
+    int64_t pass2_ = 0, proj_calls_ = 0;  // DGKS second passes taken / orthonormalisations
     bool syev_pending_ = false;
     const bool debug_ = std::getenv("BLOCKEIG_DEBUG") != nullptr;
     int cur_ = 0;  // which S buffer holds the current block
