@@ -133,6 +133,43 @@ def barrier(dist):
         dist.barrier()
 
 
+def count_launches(solve_once):
+    """Kernel launches of one solve, counted by CUPTI (torch.profiler) — every
+    kernel of libblockeig_b200.so (namespace bk::), not a self-reported count.
+    Run once after the timed region (the profiler perturbs timing)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    try:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            solve_once()
+            torch.cuda.synchronize()
+    except Exception:  # CUPTI unavailable (e.g. under ncu)
+        return None, {}
+    names = {}
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA and "bk::" in e.name:
+            short = e.name.split("(")[0].replace("void ", "").replace("bk::(anonymous namespace)::", "")
+            names[short] = names.get(short, 0) + 1
+    return sum(names.values()), dict(sorted(names.items(), key=lambda kv: -kv[1]))
+
+
+def ncu_traffic(kernel):
+    """DRAM traffic per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/*_ncu_full.json, tools/ncu_full_summary.py)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")), reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            k = d.get("classes", {}).get(kernel)
+            if k and k.get("dram_bytes_per_launch"):
+                return k["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+        except (OSError, ValueError):
+            continue
+    return None, None
+
+
 def oracle_sample(w, threads):
     """CPU oracle on the first 1 and 2 iterations; extrapolate to the solve."""
     L = B.Library(ORACLE_SO)
@@ -235,6 +272,7 @@ def main():
     barrier(dist)
     clocks = sampler.stop()
     t_step = reduce_max(dist, float(np.mean(times)))
+    launches_per_solve, launch_names = count_launches(solve_once)
     vals = res.values
     ref = W.lap3d_eigs(64, 64)
     max_rel = float(np.max(np.abs(vals - ref) / ref))
@@ -291,6 +329,11 @@ def main():
 
     roofline = roof(top)
     roofline["share_of_step"] = agg[top]["ms"] / total_ms if total_ms else None
+    traffic, traffic_src = ncu_traffic(top)
+    if traffic:
+        roofline["traffic"] = traffic
+        roofline["traffic_source"] = traffic_src
+        roofline["algorithmic_bytes_per_launch"] = agg[top]["bytes"] / agg[top]["launches"]
     roofline["by_kernel"] = {k: roof(k) for k in ("spmm", "gram", "gemm") if agg[k]["launches"]}
 
     line = {
@@ -304,7 +347,11 @@ def main():
         "iterations": int(np.mean(iters)), "max_rel_err_vs_closed_form": max_rel,
         "clocks": clocks,
         "e2e": {"value": e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(round(sum(v["launches"] for v in agg.values()) / len(stats))),
+        # CUPTI-counted launches of this library's kernels over the K timed solves
+        "gpu_launches": int(launches_per_solve * args.steps) if launches_per_solve else
+        int(round(sum(v["launches"] for v in agg.values()) / len(stats))) * args.steps,
+        "gpu_launches_per_solve": launches_per_solve,
+        "launches_by_kernel": launch_names,
         "roofline": roofline, "kernels": kernels,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(ORACLE_SO):

@@ -44,12 +44,21 @@ __global__ void __launch_bounds__(256) colnorm2_partial(int n, const double* __r
     }
 }
 
-__global__ void sum_partials(int nb, int k, const double* __restrict__ partial, double* __restrict__ out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= k) return;
+// out[c] = sum_b partial[b][c]: one warp per column, lanes stride the row
+// blocks, fixed butterfly — deterministic (a serial loop over 512 partials per
+// thread cost ~100 us per call)
+__device__ __forceinline__ double warp_colsum(int nb, int k, const double* __restrict__ partial, int c) {
+    const int lane = threadIdx.x & 31;
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += partial[static_cast<size_t>(b) * k + c];
-    out[c] = s;
+    for (int b = lane; b < nb; b += 32) s += partial[static_cast<size_t>(b) * k + c];
+    return warp_sum(s);
+}
+
+__global__ void sum_partials(int nb, int k, const double* __restrict__ partial, double* __restrict__ out) {
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (c >= k) return;
+    const double s = warp_colsum(nb, k, partial, c);
+    if ((threadIdx.x & 31) == 0) out[c] = s;
 }
 
 // R = AV - V diag(lambda); W = t .* R (columns >= w_from); norms of R and V
@@ -96,15 +105,13 @@ __global__ void __launch_bounds__(256) residual_partial(int n, const double* __r
 
 __global__ void residual_finish(int nb, int k, const double* __restrict__ pr, const double* __restrict__ pv,
                                 double* __restrict__ rn2, double* __restrict__ vn2) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (c >= k) return;
-    double s = 0.0, sv = 0.0;
-    for (int b = 0; b < nb; ++b) {
-        s += pr[static_cast<size_t>(b) * k + c];
-        sv += pv[static_cast<size_t>(b) * k + c];
+    const double s = warp_colsum(nb, k, pr, c), sv = warp_colsum(nb, k, pv, c);
+    if ((threadIdx.x & 31) == 0) {
+        rn2[c] = s;
+        vn2[c] = sv;
     }
-    rn2[c] = s;
-    vn2[c] = sv;
 }
 
 // rr.cpp:22-38 on device; one CTA
@@ -344,7 +351,7 @@ extern "C" int bk_colnorm2_d(int n, const double* x, int ldx, int k, double* out
     const int nb = row_blocks(n);
     auto partial = static_cast<double*>(work);
     colnorm2_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(n, x, ldx, k, partial);
-    sum_partials<<<ceil_div(k, 128), 128, 0, s>>>(nb, k, partial, out);
+    sum_partials<<<ceil_div(k, 8), 256, 0, s>>>(nb, k, partial, out);
     BK_LAUNCHED();
 }
 
@@ -361,7 +368,7 @@ extern "C" int bk_residual_d(int n, const double* v, int ldv, const double* av, 
     auto pv = pr + static_cast<size_t>(nb) * k;
     residual_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(
         n, v, ldv, av, ldav, lambda, k, r, ldr, t, w, ldw, w_from, pr, pv);
-    residual_finish<<<ceil_div(k, 128), 128, 0, s>>>(nb, k, pr, pv, rn2, vn2);
+    residual_finish<<<ceil_div(k, 8), 256, 0, s>>>(nb, k, pr, pv, rn2, vn2);
     BK_LAUNCHED();
 }
 
@@ -439,7 +446,7 @@ extern "C" int bk_coldot_d(int n, const double* x, int ldx, const double* y, int
     const int nb = row_blocks(n);
     auto partial = static_cast<double*>(work);
     coldot_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(n, x, ldx, y, ldy, k, partial);
-    sum_partials<<<ceil_div(k, 128), 128, 0, s>>>(nb, k, partial, out);
+    sum_partials<<<ceil_div(k, 8), 256, 0, s>>>(nb, k, partial, out);
     BK_LAUNCHED();
 }
 
@@ -536,16 +543,20 @@ extern "C" int bk_cgs2_commit_z(int n, const double* v, const double* nrm2, cons
 // host round trip.  c: m x a coefficient block (ldc elements, cw = 2 complex).
 namespace bk {
 namespace {
-__global__ void dgks_flag_kernel(int m, int a, const double* __restrict__ c, int ldc, int cw,
-                                 const double* __restrict__ ref2, double eta2, int* __restrict__ flag) {
+__global__ void __launch_bounds__(1024) dgks_flag_kernel(int m, int a, const double* __restrict__ c, int ldc,
+                                                          int cw, const double* __restrict__ ref2, double eta2,
+                                                          int* __restrict__ flag) {
+    // one warp per column, lanes over the m coefficient rows
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     int need = 0;
-    for (int j = threadIdx.x; j < a; j += blockDim.x) {
+    for (int j = wid; j < a; j += nw) {
         double s = 0.0;
-        for (int l = 0; l < m; ++l)
+        for (int l = lane; l < m; l += 32)
             for (int q = 0; q < cw; ++q) {
                 const double v = c[(static_cast<size_t>(l) * ldc + j) * cw + q];
                 s = fma(v, v, s);
             }
+        s = warp_sum(s);
         const double r2 = ref2[j];
         if (r2 > 0.0 && !(s <= (1.0 - eta2) * r2)) need = 1;  // NaN -> pass 2
     }
@@ -559,6 +570,6 @@ extern "C" int bk_dgks_flag_d(int m, int a, const double* c, int ldc, int cw, co
                               int* flag, void* stream) {
     const cudaStream_t s = as_stream(stream);
     if (a <= 0) return static_cast<int>(cudaMemsetAsync(flag, 0, sizeof(int), s));
-    dgks_flag_kernel<<<1, 256, 0, s>>>(m, a, c, ldc, cw, ref2, eta2, flag);
+    dgks_flag_kernel<<<1, 1024, 0, s>>>(m, a, c, ldc, cw, ref2, eta2, flag);
     BK_LAUNCHED();
 }
