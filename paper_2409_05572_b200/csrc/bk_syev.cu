@@ -265,20 +265,39 @@ __global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, cons
         }
         __syncthreads();
         // phase 2: fused pending update + p = t A22 v on local rows i >= k+1
+        // four local rows per warp pass: v / vp / wp are loaded once for the four
+        // rows and the four dot-product chains overlap (latency, not flops, bounds
+        // this phase)
         const int t1 = k + 1 <= rank ? 0 : (k + 1 - rank + C - 1) / C;
-        for (int tt = t1 + wid; tt < nloc; tt += nw) {
-            const int i = rank + C * tt;
-            if (i >= d) break;
-            double* row = A + static_cast<size_t>(tt) * d;
-            const double vpi = vp[i], wpi = wp[i];
-            double s = 0.0;
-            for (int j = k + 1 + lane; j < d; j += 32) {
-                const double x = row[j] - (vpi * wp[j] + wpi * vp[j]);
-                row[j] = x;
-                s = fma(x, v[j], s);
+        for (int tb = t1 + 4 * wid; tb < nloc; tb += 4 * nw) {
+            int ii[4];
+            double* rows[4];
+            double vpi[4], wpi[4], s[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int tt = tb + q;
+                ii[q] = rank + C * tt;
+                const bool ok = tt < nloc && ii[q] < d;
+                rows[q] = ok ? A + static_cast<size_t>(tt) * d : nullptr;
+                vpi[q] = ok ? vp[ii[q]] : 0.0;
+                wpi[q] = ok ? wp[ii[q]] : 0.0;
+                s[q] = 0.0;
             }
-            s = warp_sum(s) * t;
-            if (lane < C) cl.map_shared_rank(p, lane)[i] = s;
+            for (int j = k + 1 + lane; j < d; j += 32) {
+                const double vj = v[j], vpj = vp[j], wpj = wp[j];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (rows[q]) {
+                        const double x = rows[q][j] - (vpi[q] * wpj + wpi[q] * vpj);
+                        rows[q][j] = x;
+                        s[q] = fma(x, vj, s[q]);
+                    }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s[q] = warp_sum(s[q]) * t;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (rows[q] && lane < C) cl.map_shared_rank(p, lane)[ii[q]] = s[q];
         }
         cl.sync();
         // phase 3 (replicated): w = p - (t/2)(p^T v) v becomes the pending update
@@ -334,17 +353,38 @@ int tridiag_cluster_size(int d, size_t* smem) {
 }
 
 // ------------------------------------------------------------------ 2. bisection
+// Number of eigenvalues of T below x: sign changes of the leading principal
+// minors p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} (Wilkinson's continuant
+// form of the Sturm sequence; two dependent FMAs per step instead of the
+// LDL^T form's division, whose ~60-cycle latency bounded the chain).  The
+// pair (p_{i-1}, p_i) is rescaled by exact powers of two to stay in range; a
+// zero minor takes the sign opposite to its predecessor (the LDL^T form's
+// "q = -pivmin" convention).
 __device__ __forceinline__ int sturm_count(int d, const double* __restrict__ dg, const double* __restrict__ off,
                                            double x, double pivmin) {
+    (void)pivmin;
+    constexpr double kBig = 0x1p+500, kScale = 0x1p-500;
     int cnt = 0;
-    double q = dg[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
+    double pm = 1.0;       // p_{i-1}
+    double p = dg[0] - x;  // p_i
+    bool neg_prev = false;  // sign of p_{i-1} (p_0 = 1 > 0)
+    bool neg = p < 0.0 || (p == 0.0 && !neg_prev);
+    cnt += neg != neg_prev;
     for (int i = 1; i < d; ++i) {
         const double e = off[i - 1];
-        q = dg[i] - x - (e * e) / q;
-        if (fabs(q) < pivmin) q = -pivmin;
-        cnt += q < 0.0;
+        const double pn = fma(dg[i] - x, p, -(e * e) * pm);
+        pm = p;
+        p = pn;
+        neg_prev = neg;
+        neg = p < 0.0 || (p == 0.0 && !neg_prev);
+        cnt += neg != neg_prev;
+        if (fabs(p) > kBig || fabs(pm) > kBig) {
+            p *= kScale;
+            pm *= kScale;
+        } else if (fabs(p) < kScale && fabs(pm) < kScale) {
+            p *= kBig;
+            pm *= kBig;
+        }
     }
     return cnt;
 }
@@ -506,7 +546,9 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
     }
     __syncwarp();
     const double shift = lam[j];
-    for (int it = 0; it < 3; ++it) {
+    // two steps: with the shift accurate to ~eps ||T|| and clusters (gap < 1e-7 ||T||)
+    // treated as blocks, each step shrinks foreign components by <= eps/1e-7
+    for (int it = 0; it < 2; ++it) {
         if (lane == 0) tri_solve_shifted(d, dg, off, shift, tiny, b, u0, u1, u2, piv);
         __syncwarp();
         double nn = 0.0;
