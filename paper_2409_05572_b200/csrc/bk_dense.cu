@@ -14,13 +14,14 @@
 //      q*(q^T v) (kernel.cpp:76,79).
 //
 // Tiles are sized to the block widths of the solver (multiples of 96 at the
-// reference defaults n_ex = 1.5 n_ev): Gram 96 x 96 per CTA with 8 warps of
-// 48 x 24 (18 DMMA per 4-deep k step against 9 fragment loads); update 128 rows
-// x 96 columns with 8 warps of 32 x 48 (24 DMMA per k step).  Operands stream
+// reference defaults n_ex = 1.5 n_ev): Gram 96 x 96 per CTA with 4 warps of
+// 48 x 48 (36 DMMA per 4-deep k step against 12 fragment loads); update 128 rows
+// x 96 columns with 4 warps of 64 x 48 (48 DMMA per k step).  Operands stream
 // global -> shared with cp.async (16-byte when the view is 16-byte aligned,
 // tails zero-filled) through a multi-stage ring; shared pitches are 4 (mod 16)
 // doubles so fragment loads of a half-warp hit 16 distinct 8-byte banks.
 #include <algorithm>
+#include <cstdlib>
 
 #include "bk_common.cuh"
 
@@ -153,21 +154,20 @@ __global__ void gram_reduce(int splits, int a, int b, const double* __restrict__
     }
 }
 
-constexpr int GTM = 96, GTN = 96, GTK = 16, GWM = 2, GWN = 4, GST = 4;
-constexpr size_t kGramSmem = sizeof(double) * GST * GTK * ((GTM + 4) + (GTN + 4));
+constexpr int GTM = 96, GTN = 96, GTK = 16, GWM = 2, GWN = 2, GST = 4;
 
 struct GramPlan {
     int splits, rows_per_split;
 };
 
-GramPlan gram_plan(int n, int a, int b) {
+GramPlan gram_plan(int n, int a, int b, int cps = 2, int tk = GTK) {
     const int tiles = ceil_div(a, GTM) * ceil_div(b, GTN);
-    // one wave: 2 resident CTAs per SM (register / shared-memory limited), so
-    // tiles x splits must not exceed 2 x 148 or a straggler wave doubles the time
-    int splits = max(1, (2 * kSMs) / tiles);
+    // one wave: cps resident CTAs per SM (register / shared-memory limited), so
+    // tiles x splits must not exceed cps x 148 or a straggler wave doubles the time
+    int splits = max(1, (cps * kSMs) / tiles);
     splits = max(1, min(splits, ceil_div(n, 256)));  // >= 256 rows per split
     int rps = ceil_div(n, splits);
-    rps = ceil_div(rps, GTK) * GTK;
+    rps = ceil_div(rps, tk) * tk;
     splits = max(1, ceil_div(n, rps));
     return {splits, rps};
 }
@@ -245,8 +245,7 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(int n, const double*
         }
 }
 
-constexpr int UTM = 128, UTN = 96, UTK = 16, UWM = 4, UWN = 2, UST = 3;
-constexpr size_t kGemmSmem = sizeof(double) * UST * (UTM * (UTK + 4) + UTK * (UTN + 4));
+constexpr int UTM = 128, UTN = 96, UTK = 16, UWM = 2, UWN = 2, UST = 3;
 
 bool aligned16(const double* p, int ld) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld & 1) == 0; }
 
@@ -272,34 +271,63 @@ extern "C" size_t bk_gram_work_bytes(int n, int a, int b) {
 
 namespace bk {
 namespace {
-template <bool SYM>
-int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
-                void* work, cudaStream_t s, const int* run_if = nullptr) {
-    auto k16 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, true, SYM>;
-    auto k8 = gram_kernel<GTM, GTN, GTK, GWM, GWN, GST, false, SYM>;
-    static const cudaError_t a1 = prep(k16, kGramSmem);
-    static const cudaError_t a2 = prep(k8, kGramSmem);
+template <int TK, int WM, int WN, int ST, int CPS, bool SYM>
+int gram_launch_v(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
+                  void* work, cudaStream_t s, const int* run_if) {
+    constexpr size_t smem = sizeof(double) * ST * TK * ((GTM + 4) + (GTN + 4));
+    auto k16 = gram_kernel<GTM, GTN, TK, WM, WN, ST, true, SYM>;
+    auto k8 = gram_kernel<GTM, GTN, TK, WM, WN, ST, false, SYM>;
+    static const cudaError_t a1 = prep(k16, smem);
+    static const cudaError_t a2 = prep(k8, smem);
     BK_RET(a1);
     BK_RET(a2);
     const int nt = ceil_div(a, GTM);
     const int tiles = SYM ? nt * (nt + 1) / 2 : nt * ceil_div(b, GTN);
     // plan with the number of tiles actually launched
-    const GramPlan p = gram_plan(n, SYM ? tiles * GTM : a, SYM ? GTN : b);
+    const GramPlan p = gram_plan(n, SYM ? tiles * GTM : a, SYM ? GTN : b, CPS, TK);
     const dim3 grid(SYM ? tiles : nt, SYM ? 1 : ceil_div(b, GTN), p.splits);
     auto w = static_cast<double*>(work);
     const bool direct = p.splits == 1 && !SYM;  // a single split writes C directly
     double* dst = direct ? c : w;
     const int ldo = direct ? ldc : b;
     if (aligned16(x, ldx) && aligned16(y, ldy))
-        k16<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split, run_if);
+        k16<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split, run_if);
     else
-        k8<<<grid, GWM * GWN * 32, kGramSmem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split, run_if);
+        k8<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split, run_if);
     if (!direct) {
         const int64_t total = static_cast<int64_t>(a) * b;
         gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
             p.splits, a, b, w, c, ldc, SYM ? 1 : 0, GTM, run_if);
     }
     BK_LAUNCHED();
+}
+
+// BK_GRAM_VARIANT selects a tile shape for tuning runs (default 0)
+int gram_variant() {
+    static const int v = [] {
+        const char* e = getenv("BK_GRAM_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <bool SYM>
+int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
+                void* work, cudaStream_t s, const int* run_if = nullptr) {
+    switch (gram_variant()) {
+        // measured at n = 262144 (tools/tune_dense.sh): 288^2 / 288x96 / 192x96 / 96^2 TF/s
+        case 1:  // 8 warps of 48 x 24, 32-deep k steps, 3 stages, 1 CTA / SM: 23.8 / 23.8 / 23.6 / 21.7
+            return gram_launch_v<32, 2, 4, 3, 1, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+        case 2:  // 8 warps of 48 x 24, 4 stages: 28.3 / 27.7 / 26.9 / 22.5
+            return gram_launch_v<16, 2, 4, 4, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+        case 3:  // 8 warps of 48 x 24, 3 stages: 28.2 / 27.5 / 26.8 / 22.4
+            return gram_launch_v<16, 2, 4, 3, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+        case 4:  // 4 warps of 48 x 48, 32-deep, 3 stages, 1 CTA / SM: 24.6 / 24.5 / 24.3 / 22.2
+            return gram_launch_v<32, 2, 2, 3, 1, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+        default:  // 4 warps of 48 x 48 (36 DMMA per 12 fragment loads), 4 stages, 2 CTAs / SM:
+                  // 30.3 / 29.6 / 28.8 / 24.4
+            return gram_launch_v<GTK, GWM, GWN, GST, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+    }
 }
 }  // namespace
 }  // namespace bk
@@ -325,20 +353,45 @@ extern "C" int bk_gram_sym_d(int n, const double* x, int ldx, const double* y, i
 
 namespace bk {
 namespace {
-int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
-                double* y, int ldy, cudaStream_t s, const int* run_if) {
-    auto k16 = gemm_kernel<UTM, UTN, UTK, UWM, UWN, UST, true>;
-    auto k8 = gemm_kernel<UTM, UTN, UTK, UWM, UWN, UST, false>;
-    static const cudaError_t a1 = prep(k16, kGemmSmem);
-    static const cudaError_t a2 = prep(k8, kGemmSmem);
+template <int TM, int TN, int TK, int WM, int WN, int ST>
+int gemm_launch_v(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
+                  double* y, int ldy, cudaStream_t s, const int* run_if) {
+    constexpr size_t smem = sizeof(double) * ST * (TM * (TK + 4) + TK * (TN + 4));
+    auto k16 = gemm_kernel<TM, TN, TK, WM, WN, ST, true>;
+    auto k8 = gemm_kernel<TM, TN, TK, WM, WN, ST, false>;
+    static const cudaError_t a1 = prep(k16, smem);
+    static const cudaError_t a2 = prep(k8, smem);
     BK_RET(a1);
     BK_RET(a2);
-    const dim3 grid(ceil_div(n, UTM), ceil_div(k, UTN));
+    const dim3 grid(ceil_div(n, TM), ceil_div(k, TN));
     if (aligned16(x, ldx))
-        k16<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
+        k16<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
     else
-        k8<<<grid, UWM * UWN * 32, kGemmSmem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
+        k8<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
     BK_LAUNCHED();
+}
+
+// BK_GEMM_VARIANT selects a tile shape for tuning runs (default 0)
+int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
+                double* y, int ldy, cudaStream_t s, const int* run_if) {
+    static const int v = [] {
+        const char* e = getenv("BK_GEMM_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    switch (v) {
+        // n = 262144 (tools/tune_dense.sh), 288x192 / 288x96 / 192x96 / 96x96 TF/s
+        case 1:  // 32-deep, 1 CTA / SM: 23.7 / 23.5 / 22.6 / 20.0
+            return gemm_launch_v<128, 96, 32, 4, 2, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+        case 2:  // 4 stages: 21.3 / 21.1 / 20.3 / 18.2
+            return gemm_launch_v<128, 96, 16, 4, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+        case 3:  // 64-row tiles: 24.1 / 23.9 / 22.7 / 19.5
+            return gemm_launch_v<64, 96, 16, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+        case 4:  // 8 warps of 32 x 48 (the round-1 first shape): 27.8 / 27.4 / 26.0 / 22.5
+            return gemm_launch_v<128, 96, 16, 4, 2, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+        default:  // 4 warps of 64 x 48: 28.3 / 28.1 / 26.3 / 22.2
+            return gemm_launch_v<UTM, UTN, UTK, UWM, UWN, UST>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
+                                                               run_if);
+    }
 }
 }  // namespace
 }  // namespace bk

@@ -110,7 +110,6 @@ def main():
     print(json.dumps(out))
     if args.save or args.out:
         full = dict(out, values=list(map(float, vals)), history=history_rows(r))
-        full.pop("kernel_stats", None)
         suffix = f"_it{args.max_iters}" if args.max_iters else ""
         path = args.out or os.path.join(ROOT, "tests", "golden", f"oracle_{w.name}{suffix}.json")
         with open(path, "w") as f:
