@@ -332,6 +332,64 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
 }  // namespace
 }  // namespace bk
 
+// ------------------------------------------------------------------ single-column forms
+// X^T v and X c for one vector (the exact column CGS2 of K4's fallback): HBM-bound
+// GEMV shapes, where a 96 x 96 DMMA tile would waste 95 % of its work.
+namespace bk {
+namespace {
+constexpr int kGvRows = 256, kGvMaxBlocks = 512;
+
+__global__ void __launch_bounds__(256) xtv_partial(int n, const double* __restrict__ x, int ldx, int a,
+                                                   const double* __restrict__ v, int ldv,
+                                                   double* __restrict__ partial) {
+    __shared__ double red[8][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int c = blockIdx.y * 32 + tx;
+    const int nb = gridDim.x;
+    const int r0 = static_cast<int>((static_cast<int64_t>(n) * blockIdx.x) / nb);
+    const int r1 = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.x + 1)) / nb);
+    double acc = 0.0;
+    if (c < a)
+        for (int r = r0 + ty; r < r1; r += 8) acc = fma(x[static_cast<size_t>(r) * ldx + c], v[static_cast<size_t>(r) * ldv], acc);
+    red[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && c < a) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += red[i][tx];
+        partial[static_cast<size_t>(blockIdx.x) * a + c] = s;
+    }
+}
+
+__global__ void xtv_finish(int nb, int a, const double* __restrict__ partial, double* __restrict__ out, int ldo) {
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (c >= a) return;
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += partial[static_cast<size_t>(b) * a + c];
+    s = warp_sum(s);
+    if (lane == 0) out[static_cast<size_t>(c) * ldo] = s;
+}
+
+// y[i] = alpha (x[i, 0:d] . c) + beta y[i], warp per row
+__global__ void __launch_bounds__(256) xc_kernel(int n, const double* __restrict__ x, int ldx, int d,
+                                                 const double* __restrict__ cv, int ldc, double alpha, double beta,
+                                                 double* __restrict__ y, int ldy) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+        const double* xr = x + static_cast<size_t>(i) * ldx;
+        double s = 0.0;
+        for (int q = lane; q < d; q += 32) s = fma(xr[q], cv[static_cast<size_t>(q) * ldc], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+            double* yi = y + static_cast<size_t>(i) * ldy;
+            *yi = beta == 0.0 ? alpha * s : fma(alpha, s, beta * *yi);
+        }
+    }
+}
+}  // namespace
+}  // namespace bk
+
 extern "C" int bk_gram_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
                          int ldc, void* work, void* stream) {
     if (a <= 0 || b <= 0) return 0;
@@ -339,6 +397,13 @@ extern "C" int bk_gram_d(int n, const double* x, int ldx, int a, const double* y
     if (n <= 0) {
         for (int i = 0; i < a; ++i) BK_RET(cudaMemsetAsync(c + static_cast<size_t>(i) * ldc, 0, sizeof(double) * b, s));
         return 0;
+    }
+    if (b == 1 && n >= 4096) {  // X^T v (work: row blocks x a <= bk_gram_work_bytes(n, a, 1))
+        const int nb = max(1, min(ceil_div(n, kGvRows), kGvMaxBlocks));
+        auto partial = static_cast<double*>(work);
+        xtv_partial<<<dim3(nb, ceil_div(a, 32)), dim3(32, 8), 0, s>>>(n, x, ldx, a, y, ldy, partial);
+        xtv_finish<<<ceil_div(a, 8), 256, 0, s>>>(nb, a, partial, c, ldc);
+        BK_LAUNCHED();
     }
     return gram_launch<false>(n, x, ldx, a, y, ldy, b, c, ldc, work, s);
 }
@@ -402,6 +467,11 @@ extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c
     if (d <= 0) {
         if (beta == 1.0) return 0;
         return bk_axpby_d(n, k, 0.0, y, ldy, beta, y, ldy, stream);
+    }
+    if (k == 1 && n >= 4096) {  // X c for one column: a GEMV
+        xc_kernel<<<max(1, min(ceil_div(n, 8), kSMs * 16)), 256, 0, as_stream(stream)>>>(n, x, ldx, d, c, ldc, alpha,
+                                                                                         beta, y, ldy);
+        BK_LAUNCHED();
     }
     return gemm_launch(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, as_stream(stream), nullptr);
 }

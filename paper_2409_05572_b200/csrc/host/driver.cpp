@@ -303,7 +303,9 @@ private:
             BKC(bk_gram_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), st()));
         else
             BKC(bk_gram_z(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), st()));
-        prof_end(t, K_GRAM, 8.0 * cw_ * rows * (a + b), 2.0 * cw_ * cw_ * rows * a * b);
+        // only the n-row contractions are K2 work; coefficient-space ones (rows = d,
+        // HL trick) are latency-bound bookkeeping and counted as "other"
+        prof_end(t, rows >= n_ ? K_GRAM : K_OTHER, 8.0 * cw_ * rows * (a + b), 2.0 * cw_ * cw_ * rows * a * b);
     }
     // K3: flops 2*rows*d*k; bytes 8*rows*(d + k (+k when beta != 0))
     void gemm(int rows, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
@@ -313,7 +315,8 @@ private:
             BKC(bk_gemm_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, st()));
         else
             BKC(bk_gemm_z(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, CEXP_.p(), st()));
-        prof_end(t, K_GEMM, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * cw_ * cw_ * rows * d * k);
+        prof_end(t, rows >= n_ ? K_GEMM : K_OTHER, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)),
+                 2.0 * cw_ * cw_ * rows * d * k);
     }
     // predicated K2/K3 (run only when *flag != 0 on the device); the profile
     // entry is resolved against the flag's host copy (pin_.info[3]) at the next sync

@@ -85,7 +85,8 @@ def test_spmm_vs_oracle(bk, oracle, k):
     assert torch.equal(y2[:, :k], yd[:, :k])
 
 
-@pytest.mark.parametrize("n,a,b", [(1000, 13, 70), (262144, 96, 96), (5000, 288, 288), (77, 1, 1)])
+@pytest.mark.parametrize("n,a,b", [(1000, 13, 70), (262144, 96, 96), (5000, 288, 288), (77, 1, 1),
+                                   (100000, 95, 1)])
 def test_gram_vs_numpy(bk, n, a, b):
     rng = np.random.default_rng(n + a)
     x, y = rng.standard_normal((n, a)), rng.standard_normal((n, b))
@@ -99,7 +100,8 @@ def test_gram_vs_numpy(bk, n, a, b):
     assert np.abs(c.cpu().numpy() - want).max() <= 1e-13 * np.sqrt(n) * np.abs(want).max() + 1e-12
 
 
-@pytest.mark.parametrize("n,d,k,beta", [(1000, 40, 40, 0.0), (262144, 288, 96, 0.0), (5000, 96, 7, 1.0), (33, 5, 3, -1.0)])
+@pytest.mark.parametrize("n,d,k,beta", [(1000, 40, 40, 0.0), (262144, 288, 96, 0.0), (5000, 96, 7, 1.0), (33, 5, 3, -1.0),
+                                        (100000, 70, 1, 1.0)])
 def test_gemm_vs_numpy(bk, n, d, k, beta):
     rng = np.random.default_rng(d + k)
     x, cm, y0 = rng.standard_normal((n, d)), rng.standard_normal((d, k)), rng.standard_normal((n, k))
