@@ -58,10 +58,10 @@ thread_local double g_host_call_s = 0.0;  // BLOCKEIG_TIMING: host time inside C
 // pinned host staging for the per-iteration record and small infos
 struct Pinned {
     double* rec = nullptr;  // 4 doubles
-    int* info = nullptr;    // 16 ints
+    int* info = nullptr;    // 32 ints: [0..15] synchronous infos, [16..] speculative K4 slots
     Pinned() {
         BKC(cudaMallocHost(reinterpret_cast<void**>(&rec), 4 * sizeof(double)));
-        BKC(cudaMallocHost(reinterpret_cast<void**>(&info), 16 * sizeof(int)));
+        BKC(cudaMallocHost(reinterpret_cast<void**>(&info), 32 * sizeof(int)));
     }
     ~Pinned() {
         cudaFreeHost(rec);
@@ -131,6 +131,7 @@ public:
         ZC_.alloc(dc * dc * es);
         CZ_.alloc(dc * dc * es);
         VALS_.alloc(dc * sizeof(double));
+        VALS_BAK_.alloc(dc * sizeof(double));
         COEF_.alloc(dc * static_cast<size_t>(tcap_) * es + 64);
         GB_.alloc(static_cast<size_t>(tcap_) * tcap_ * es);
         M1_.alloc(static_cast<size_t>(tcap_) * tcap_ * es);
@@ -321,19 +322,20 @@ private:
     // predicated K2/K3 (run only when *flag != 0 on the device); the profile
     // entry is resolved against the flag's host copy (pin_.info[3]) at the next sync
     void gram_if(int rows, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
-                 const int* flag) {
+                 const int* flag, const int* flag_host) {
         auto t = prof_begin();
         if (cw_ == 1) BKC(bk_gram_if_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), flag, st()));
         else BKC(bk_gram_if_z(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), flag, st()));
-        prof_end(t, K_GRAM, 8.0 * cw_ * rows * (a + b), 2.0 * cw_ * cw_ * rows * a * b, &pin_.info[3]);
+        prof_end(t, rows >= n_ ? K_GRAM : K_OTHER, 8.0 * cw_ * rows * (a + b), 2.0 * cw_ * cw_ * rows * a * b,
+                 flag_host);
     }
     void gemm_if(int rows, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
-                 double beta, double* y, int ldy, const int* flag) {
+                 double beta, double* y, int ldy, const int* flag, const int* flag_host) {
         auto t = prof_begin();
         if (cw_ == 1) BKC(bk_gemm_if_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, flag, st()));
         else BKC(bk_gemm_if_z(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, CEXP_.p(), flag, st()));
-        prof_end(t, K_GEMM, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)), 2.0 * cw_ * cw_ * rows * d * k,
-                 &pin_.info[3]);
+        prof_end(t, rows >= n_ ? K_GEMM : K_OTHER, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)),
+                 2.0 * cw_ * cw_ * rows * d * k, flag_host);
     }
     // column movement and elementwise ops work on the real view (cw doubles per element)
     void copy(int rows, Blk src, int k, Blk dst) {
@@ -382,11 +384,16 @@ private:
     // K4: project w (rows x a, clobbered) against q (rows x m), orthonormalise
     // the rest with the CGS2 drop rule; kept columns land packed in out.
     // (project_orthonormalize, proj/src/kernel.cpp:65-89)
-    int proj_ortho(int rows, Blk w, int a, Blk q, int m, Blk out) {
+    // slot >= 0: speculative — no host round trip; the caller proceeds as if all
+    // a columns were kept and verifies the Cholesky info at the next record
+    // readback (spec_ok), redoing the iteration synchronously if not.
+    int proj_ortho(int rows, Blk w, int a, Blk q, int m, Blk out, int slot = -1) {
         if (a <= 0) return 0;
         double* ref2 = SMALL_.d();  // a doubles
         colnorm2(rows, w, a, ref2);
-        int* info = INFO_.as<int>();  // [0..2] Cholesky info, [3] DGKS flag
+        // [0..2] Cholesky info, [3] DGKS flag; speculative calls use their own slot
+        int* info = INFO_.as<int>() + (slot >= 0 ? 40 + 4 * slot : 0);
+        int* info_host = pin_.info + (slot >= 0 ? 16 + 4 * slot : 0);
         if (m > 0) {
             // the reference's CGS2 projects twice (kernel.cpp:73-80); the second
             // block pass runs only when the first removed more than half of some
@@ -395,8 +402,8 @@ private:
             gram(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a);
             gemm(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld);
             BKO(bk_dgks_flag_d(m, a, COEF_.d(), a, cw_, ref2, 0.5, info + 3, st()));
-            gram_if(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a, info + 3);
-            gemm_if(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld, info + 3);
+            gram_if(rows, q.p, q.ld, m, w.p, w.ld, a, COEF_.d(), a, info + 3, info_host + 3);
+            gemm_if(rows, q.p, q.ld, m, COEF_.d(), a, a, -1.0, 1.0, w.p, w.ld, info + 3, info_host + 3);
         } else {
             BKC(cudaMemsetAsync(info + 3, 0, sizeof(int), stream_));
         }
@@ -405,15 +412,20 @@ private:
         if (cw_ == 1) BKC(bk_chol_drop_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
         else BKC(bk_chol_drop_z(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
         prof_end(tc, K_CHOL, 8.0 * cw_ * a * a, cw_ * cw_ * a * a * a / 3.0);
-        BKC(cudaMemcpyAsync(pin_.info, info, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
-        sync();
-        pass2_ += pin_.info[3];
+        BKC(cudaMemcpyAsync(info_host, info, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         ++proj_calls_;
-        if (debug_ && cw_ == 1) debug_pivots(a, ref2);
-        if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
-        if (pin_.info[1]) return cgs2_fallback(rows, w, a, q, m, out);
-        const int kept = pin_.info[0];
-        if (kept == 0) return 0;
+        int kept = a;
+        if (slot >= 0) {
+            spec_expect_[slot] = a;
+        } else {
+            sync();
+            pass2_ += pin_.info[3];
+            if (debug_ && cw_ == 1) debug_pivots(a, ref2);
+            if (pin_.info[2]) throw std::runtime_error("orthonormalization: non-finite values");
+            if (pin_.info[1]) return cgs2_fallback(rows, w, a, q, m, out);
+            kept = pin_.info[0];
+            if (kept == 0) return 0;
+        }
         Blk pt = B(PT_.d(), ldT_);
         gemm(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld);
         // second pass: the block is orthonormal to ~1e-8 after the pivot-checked
@@ -545,10 +557,31 @@ private:
     struct Rep {
         double overall;
         int converged;
+        bool nonfinite;
     };
     // AV into AS[:, 0:k], R = AV - V diag(VALS) into R, record read back
     // (residual_block + assess_convergence, rr.cpp:16-38)
-    Rep residual(Blk v, int k, int n_ev) {
+    // tolerate_nonfinite: a speculative iteration is pending and will be redone
+    // if its record is non-finite (the caller decides after spec_ok())
+    // Speculation support: a redone tail needs the R and AX of its own
+    // iteration, which the next residual() overwrote.  save_ritz() keeps the
+    // Ritz values the residual used; restore_residual() recomputes R and AX
+    // with the same deterministic kernels (bit-identical), no record.
+    void save_ritz(int k) {
+        BKC(cudaMemcpyAsync(VALS_BAK_.d(), VALS_.d(), sizeof(double) * k, cudaMemcpyDeviceToDevice, stream_));
+    }
+    void restore_residual(Blk v, int k) {
+        spmm(v, k, AS());
+        double* rn2 = SMALL_.d();
+        double* vn2 = SMALL_.d() + dcap_ + tcap_;
+        if (cw_ == 1)
+            BKC(bk_residual_d(n_, v.p, v.ld, AS_.d(), ldS_, VALS_BAK_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0,
+                              rn2, vn2, WORK_.p(), st()));
+        else
+            BKC(bk_residual_z(n_, v.p, v.ld, AS_.d(), ldS_, VALS_BAK_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0,
+                              rn2, vn2, WORK_.p(), st()));
+    }
+    Rep residual(Blk v, int k, int n_ev, bool tolerate_nonfinite = false) {
         meter_.w.spmv_cols += k;
         if (debug_) std::fprintf(stderr, "[blockeig] iteration %zu k=%d\n", out_.history.size() + 1, k);
         spmm(v, k, AS());
@@ -566,9 +599,10 @@ private:
         prof_end(tr, K_RESID, 24.0 * cw_ * n_ * k, 6.0 * cw_ * n_ * k);
         BKC(cudaMemcpyAsync(pin_.rec, rec, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         sync();
-        check_syev();
-        if (pin_.rec[2] != 0.0) throw std::runtime_error("non-finite residual or Ritz value");
-        return {pin_.rec[0], static_cast<int>(pin_.rec[1])};
+        const bool bad = pin_.rec[2] != 0.0;
+        if (!(bad && tolerate_nonfinite)) check_syev();
+        if (bad && !tolerate_nonfinite) throw std::runtime_error("non-finite residual or Ritz value");
+        return {pin_.rec[0], static_cast<int>(pin_.rec[1]), bad};
     }
 
     // y = op(x): shifted operator c x - M x (extension) or shift-and-invert
@@ -615,8 +649,10 @@ private:
         out_.rr_flops = meter_.rr_flops;
         out_.cgs2_fallbacks = fallbacks_;
         if (std::getenv("BLOCKEIG_TIMING"))
-            std::fprintf(stderr, "[blockeig] second Gram-Schmidt pass taken in %lld of %lld orthonormalisations\n",
-                         static_cast<long long>(pass2_), static_cast<long long>(proj_calls_));
+            std::fprintf(stderr, "[blockeig] second Gram-Schmidt pass taken in %lld of %lld orthonormalisations; "
+                         "speculative iterations %lld, redone %lld\n",
+                         static_cast<long long>(pass2_), static_cast<long long>(proj_calls_),
+                         static_cast<long long>(spec_runs_), static_cast<long long>(spec_redos_));
         out_.max_jacobi_sweeps = max_sweeps_;
         if (std::getenv("BLOCKEIG_TIMING"))
             std::fprintf(stderr,
@@ -648,7 +684,7 @@ private:
     cudaStream_t stream_ = nullptr;
     int tcap_ = 0, dcap_ = 0, ldS_ = 0, ldT_ = 0, ldH_ = 0;
     DevMem S_[2], AS_, R_, XD_, T1_, T2_, PT_, VEC_, H_, Z_, ZC_, CZ_, VALS_, COEF_, GB_, M1_, M2_, SMALL_,
-        INFO_, WORK_, TD_, INV_, stage_, CEXP_;
+        INFO_, WORK_, TD_, INV_, stage_, CEXP_, VALS_BAK_;
     DevMem CG_[6];
     // pinned staging is per host thread and outlives the solve (cudaFreeHost
     // synchronises the device and costs ms per solve)
@@ -662,6 +698,22 @@ private:
     SolveOutput out_;
     int fallbacks_ = 0, max_sweeps_ = 0;
     int64_t pass2_ = 0, proj_calls_ = 0;  // DGKS second passes taken / orthonormalisations
+    int spec_expect_[4] = {-1, -1, -1, -1};  // speculative K4 slots: assumed kept count (-1: unused)
+    int64_t spec_runs_ = 0, spec_redos_ = 0;
+    int spec_cooldown_ = 0;
+    // after a sync: did every speculative K4 call keep all its columns, decisively?
+    bool spec_ok() {
+        bool ok = true;
+        for (int s = 0; s < 4; ++s) {
+            if (spec_expect_[s] < 0) continue;
+            const int* inf = pin_.info + 16 + 4 * s;
+            pass2_ += inf[3];
+            if (inf[2]) throw std::runtime_error("orthonormalization: non-finite values");
+            if (inf[1] || inf[0] != spec_expect_[s]) ok = false;
+            spec_expect_[s] = -1;
+        }
+        return ok;
+    }
     bool syev_pending_ = false;
     const bool debug_ = std::getenv("BLOCKEIG_DEBUG") != nullptr;
     int cur_ = 0;  // which S buffer holds the current block
@@ -715,7 +767,12 @@ int Engine::initial_block(const double* x0, int x0_cols, Blk dst) {
     return n_ex;
 }
 
-// solvers.cpp:204-259 (+ operator mode)
+// solvers.cpp:204-259 (+ operator mode).  Speculative like LOBPCG (one host
+// readback per iteration): the head (residual, stagnation guard, decision,
+// Y = op(V) into T1, expansion) runs synchronously; the tail (orthonormalise
+// Y into S, Rayleigh-Ritz, lift, shrink) is enqueued assuming the
+// orthonormalisation keeps every column and is redone from T1 (untouched by
+// the tail) if the next record shows otherwise.
 void Engine::solve_si() {
     const int n_ex = cfg_.n_ex, n_es = cfg_.n_es, n_ev = cfg_.n_ev;
     if (!cfg_.op_shifted) factor_shift_invert();
@@ -727,10 +784,54 @@ void Engine::solve_si() {
     BlockSizer sizer(strategy_);
     Stagnation guard;
     const Blk xd = B(XD_.d(), ldT_);
+    static const bool spec_off = std::getenv("BLOCKEIG_NO_SPEC") != nullptr;
+    auto tail = [&](int j, const Rep& rep, Decision d, int ycols, Event ev, bool spec) {
+        meter_.ortho(n_, ycols);
+        const int kept = proj_ortho(n_, T1(), ycols, B(nullptr, 0), 0, S(cur_), spec ? 0 : -1);
+        if (kept < n_now) fresh_cols(n_now - kept, S(cur_), kept);
+        rayleigh_ritz(S(cur_), n_now, 0);
+        lift(S(cur_), n_now, Z_.d(), ldH_, n_now, S(1 - cur_));
+        cur_ ^= 1;
+        if (d == Decision::shrink) {
+            copy(n_, S(cur_).at(n_es), n_now - n_es, xd);
+            xd_cols_ = n_now - n_es;
+            n_now = n_es;
+            ev = Event::shrink;
+        }
+        push(j, rep.overall, n_now, ev, 0);
+    };
+    struct Snap {
+        int j, cur, n_now, xd_cols, ycols;
+        Event ev;
+        Decision d;
+        Rep rep;
+        Meter meter;
+        size_t hist;
+    };
+    Snap snap{};
+    bool spec_pending = false;
+    auto settle = [&](const Rep& rep) -> bool {  // true if the previous tail was redone
+        if (!spec_pending) return false;
+        spec_pending = false;
+        if (spec_ok() && !rep.nonfinite) return false;
+        ++spec_redos_;
+        spec_cooldown_ = 8;  // failing speculations: stay synchronous for a while
+        cur_ = snap.cur;
+        n_now = snap.n_now;
+        xd_cols_ = snap.xd_cols;
+        meter_ = snap.meter;
+        out_.history.resize(snap.hist);
+        tail(snap.j, snap.rep, snap.d, snap.ycols, snap.ev, false);
+        return true;
+    };
     for (int j = 1; j <= cfg_.max_iters; ++j) {
         meter_.begin_iteration();
+        Rep rep = residual(S(cur_), n_now, n_ev, spec_pending);
+        if (settle(rep)) {
+            meter_.begin_iteration();
+            rep = residual(S(cur_), n_now, n_ev, false);
+        }
         const Blk v = S(cur_);
-        const Rep rep = residual(v, n_now, n_ev);
         if (rep.converged >= n_ev) {
             push(j, rep.overall, n_now, Event::none, 0);
             return finish(Status::converged, v, n_ev);
@@ -759,24 +860,23 @@ void Engine::solve_si() {
                 ev = Event::expand;
             }
         }
-        meter_.ortho(n_, ycols);
-        const int kept = proj_ortho(n_, T1(), ycols, B(nullptr, 0), 0, S(cur_));
-        if (kept < n_now) fresh_cols(n_now - kept, S(cur_), kept);
-        rayleigh_ritz(S(cur_), n_now, 0);
-        lift(S(cur_), n_now, Z_.d(), ldH_, n_now, S(1 - cur_));
-        cur_ ^= 1;
-        if (d == Decision::shrink) {
-            copy(n_, S(cur_).at(n_es), n_now - n_es, xd);
-            xd_cols_ = n_now - n_es;
-            n_now = n_es;
-            ev = Event::shrink;
+        const bool spec = !spec_off && d != Decision::expand && spec_cooldown_ == 0;
+        if (spec_cooldown_ > 0) --spec_cooldown_;
+        if (spec) {
+            snap = Snap{j, cur_, n_now, xd_cols_, ycols, ev, d, rep, meter_, out_.history.size()};
+            ++spec_runs_;
         }
-        push(j, rep.overall, n_now, ev, 0);
+        tail(j, rep, d, ycols, ev, spec);
+        spec_pending = spec;
     }
+    sync();
+    settle(Rep{0.0, 0, false});
     finish(Status::max_iters, S(cur_), n_ev);
 }
 
-// solvers.cpp:261-314
+// solvers.cpp:261-314.  Speculative tail as for LOBPCG: X = S(cur)[:, 0:n_now],
+// AX and R are not overwritten by the tail, so a failed speculation is redone
+// from them.
 void Engine::solve_sd() {
     const int n_ex = cfg_.n_ex, n_es = cfg_.n_es, n_ev = cfg_.n_ev;
     initial_block(x0_, x0_cols_, S(cur_));
@@ -787,15 +887,10 @@ void Engine::solve_sd() {
     BlockSizer sizer(strategy_);
     const Blk xd = B(XD_.d(), ldT_);
     const double* td = TD_.bytes() ? TD_.d() : nullptr;
-    for (int j = 1; j <= cfg_.max_iters; ++j) {
-        meter_.begin_iteration();
+    static const bool spec_off = std::getenv("BLOCKEIG_NO_SPEC") != nullptr;
+    // false when the solve ended inside
+    auto tail = [&](int j, const Rep& rep, Decision d, bool spec) -> bool {
         const Blk v = S(cur_);
-        const Rep rep = residual(v, n_now, n_ev);
-        if (rep.converged >= n_ev) {
-            push(j, rep.overall, n_now, Event::none, 0);
-            return finish(Status::converged, v, n_ev);
-        }
-        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
         Event ev = Event::none;
         const int n_old = n_now;
         int xb = n_now;
@@ -817,10 +912,11 @@ void Engine::solve_sd() {
         }
         scale_rows(n_, n_old, td, B(R_.d(), ldT_), T1());
         meter_.proj_ortho(n_, n_old, xb);
-        const int kw = proj_ortho(n_, T1(), n_old, v, xb, v.at(xb));
+        const int kw = proj_ortho(n_, T1(), n_old, v, xb, v.at(xb), spec ? 0 : -1);
         if (kw == 0) {
             push(j, rep.overall, n_now, ev, 0);
-            return finish(Status::stagnated, v, n_ev);
+            finish(Status::stagnated, v, n_ev);
+            return false;
         }
         const int ds = xb + kw;
         rayleigh_ritz(v, ds, n_old, n_now);
@@ -833,12 +929,72 @@ void Engine::solve_sd() {
             ev = Event::shrink;
         }
         push(j, rep.overall, n_now, ev, 0);
+        return true;
+    };
+    struct Snap {
+        int j, cur, n_now, xd_cols;
+        Decision d;
+        Rep rep;
+        Meter meter;
+        size_t hist;
+    };
+    Snap snap{};
+    bool spec_pending = false;
+    auto settle = [&](const Rep& rep) -> int {  // 0 ok, 1 redone, -1 solve ended
+        if (!spec_pending) return 0;
+        spec_pending = false;
+        if (spec_ok() && !rep.nonfinite) return 0;
+        ++spec_redos_;
+        spec_cooldown_ = 8;  // failing speculations: stay synchronous for a while
+        cur_ = snap.cur;
+        n_now = snap.n_now;
+        xd_cols_ = snap.xd_cols;
+        meter_ = snap.meter;
+        out_.history.resize(snap.hist);
+        restore_residual(S(cur_), n_now);  // R, AX of the redone iteration
+        return tail(snap.j, snap.rep, snap.d, false) ? 1 : -1;
+    };
+    for (int j = 1; j <= cfg_.max_iters; ++j) {
+        meter_.begin_iteration();
+        Rep rep = residual(S(cur_), n_now, n_ev, spec_pending);
+        const int st = settle(rep);
+        if (st < 0) return;
+        if (st > 0) {
+            meter_.begin_iteration();
+            rep = residual(S(cur_), n_now, n_ev, false);
+        }
+        if (rep.converged >= n_ev) {
+            push(j, rep.overall, n_now, Event::none, 0);
+            return finish(Status::converged, S(cur_), n_ev);
+        }
+        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        const bool spec = !spec_off && d != Decision::expand && spec_cooldown_ == 0;
+        if (spec_cooldown_ > 0) --spec_cooldown_;
+        if (spec) {
+            snap = Snap{j, cur_, n_now, xd_cols_, d, rep, meter_, out_.history.size()};
+            save_ritz(n_now);
+            ++spec_runs_;
+        }
+        if (!tail(j, rep, d, spec)) return;
+        spec_pending = spec;
     }
+    sync();
+    if (settle(Rep{0.0, 0, false}) < 0) return;
     finish(Status::max_iters, S(cur_), n_ev);
 }
 
 // solvers.cpp:316-401.  Layout of the current buffer: [X (n_now) | P (np)],
 // with W appended after P inside the iteration.
+//
+// One host readback per iteration: the two orthonormalisations of an
+// iteration (W against [X, P] and the HL trick's coefficient block) run
+// speculatively — the iteration is enqueued as if both kept all their columns
+// (the common case) and their Cholesky infos travel back with the next
+// residual record.  If a speculation failed (a column dropped, or an
+// undecided pivot), the iteration is restored from its snapshot (host scalars,
+// meter, history; the device state it started from — [X, P], AX, R — is not
+// overwritten by the speculative tail) and redone with synchronous decisions.
+// Expansion iterations are always synchronous.  BLOCKEIG_NO_SPEC=1 disables it.
 void Engine::solve_lobpcg() {
     const int n_ex = cfg_.n_ex, n_es = cfg_.n_es, n_ev = cfg_.n_ev;
     initial_block(x0_, x0_cols_, S(cur_));
@@ -850,35 +1006,23 @@ void Engine::solve_lobpcg() {
     const Blk xd = B(XD_.d(), ldT_);
     const double* td = TD_.bytes() ? TD_.d() : nullptr;
     const Blk zc = B(ZC_.d(), ldH_), cz = B(CZ_.d(), ldH_), z = B(Z_.d(), ldH_);
-    for (int j = 1; j <= cfg_.max_iters; ++j) {
-        meter_.begin_iteration();
+    static const bool spec_off = std::getenv("BLOCKEIG_NO_SPEC") != nullptr;
+
+    // everything after the decision; false when the solve ended inside
+    auto tail = [&](int j, const Rep& rep, int lock, Decision d, bool spec) -> bool {
         Blk s = S(cur_);
-        mark(0);
-        const Rep rep = residual(s, n_now, n_ev);
-        mark(1);
-        const int lock = std::min(rep.converged, n_now - 1);
-        if (rep.converged >= n_ev) {
-            push(j, rep.overall, n_now, Event::none, lock);
-            return finish(Status::converged, s, n_ev);
-        }
-        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
         const int active = n_now - lock;
-        // soft locking: P loses its leading (lock - prev_lock) columns
-        if (lock > prev_lock && np > 0) {
-            const int drop = std::min(lock - prev_lock, np);
-            copy(n_, s.at(n_now + drop), np - drop, s.at(n_now));
-            np -= drop;
-        }
         // W = T R(:, lock:) orthonormalised against [X, P]
         scale_rows(n_, active, td, B(R_.d(), ldT_).at(lock), T1());
         int m = n_now + np;
         meter_.proj_ortho(n_, active, m);
         mark(0);
-        const int kw = proj_ortho(n_, T1(), active, s, m, s.at(m));
+        const int kw = proj_ortho(n_, T1(), active, s, m, s.at(m), spec ? 0 : -1);
         mark(2);
         if (kw == 0) {
             push(j, rep.overall, n_now, Event::none, lock);
-            return finish(Status::stagnated, s, n_ev);
+            finish(Status::stagnated, s, n_ev);
+            return false;
         }
         Event ev = Event::none;
         const int n_old = n_now;
@@ -938,7 +1082,7 @@ void Engine::solve_lobpcg() {
         copy(ds, z.at(lock), ahl, cz);
         zero_rows(cz, ahl, 0, n_now);
         mark(0);
-        const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now));
+        const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now), spec ? 1 : -1);
         mark(4);
         meter_.w.ortho_flops += static_cast<int64_t>(ds) * (n_now - lock) * (2 * n_now + (n_now - lock));
         // [X, P] = S ZC
@@ -962,7 +1106,73 @@ void Engine::solve_lobpcg() {
         push(j, rep.overall, n_now, ev, lock);
         mark(6);
         prev_lock = lock;
+        return true;
+    };
+
+    struct Snap {
+        int j, cur, n_now, np, prev_lock, xd_cols, lock;
+        Decision d;
+        Rep rep;
+        Meter meter;
+        size_t hist;
+    };
+    Snap snap{};
+    bool spec_pending = false;
+    // verify the previous iteration's speculation (after a sync); redo it if needed
+    auto settle = [&](const Rep& rep) -> int {  // 0 ok, 1 redone, -1 solve ended
+        if (!spec_pending) return 0;
+        spec_pending = false;
+        const bool ok = spec_ok();
+        if (ok && !rep.nonfinite) return 0;
+        ++spec_redos_;
+        spec_cooldown_ = 8;  // failing speculations: stay synchronous for a while
+        cur_ = snap.cur;
+        n_now = snap.n_now;
+        np = snap.np;
+        prev_lock = snap.prev_lock;
+        xd_cols_ = snap.xd_cols;
+        meter_ = snap.meter;
+        out_.history.resize(snap.hist);
+        restore_residual(S(cur_), n_now);  // R, AX of the redone iteration
+        return tail(snap.j, snap.rep, snap.lock, snap.d, false) ? 1 : -1;
+    };
+    for (int j = 1; j <= cfg_.max_iters; ++j) {
+        meter_.begin_iteration();
+        mark(0);
+        Rep rep = residual(S(cur_), n_now, n_ev, spec_pending);
+        mark(1);
+        const int st = settle(rep);
+        if (st < 0) return;
+        if (st > 0) {
+            meter_.begin_iteration();
+            rep = residual(S(cur_), n_now, n_ev, false);
+        }
+        Blk s = S(cur_);
+        const int lock = std::min(rep.converged, n_now - 1);
+        if (rep.converged >= n_ev) {
+            push(j, rep.overall, n_now, Event::none, lock);
+            return finish(Status::converged, s, n_ev);
+        }
+        const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        // soft locking: P loses its leading (lock - prev_lock) columns
+        if (lock > prev_lock && np > 0) {
+            const int drop = std::min(lock - prev_lock, np);
+            copy(n_, s.at(n_now + drop), np - drop, s.at(n_now));
+            np -= drop;
+        }
+        const bool spec = !spec_off && d != Decision::expand && spec_cooldown_ == 0;
+        if (spec_cooldown_ > 0) --spec_cooldown_;
+        if (spec) {
+            snap = Snap{j, cur_, n_now, np, prev_lock, xd_cols_, lock, d, rep, meter_, out_.history.size()};
+            save_ritz(n_now);
+            ++spec_runs_;
+        }
+        if (!tail(j, rep, lock, d, spec)) return;
+        spec_pending = spec;
     }
+    // the last iteration may still be speculative: settle it before finishing
+    sync();
+    if (settle(Rep{0.0, 0, false}) < 0) return;
     finish(Status::max_iters, S(cur_), n_ev);
 }
 
