@@ -48,12 +48,10 @@ thread_local double g_host_call_s = 0.0;  // BLOCKEIG_TIMING: host time inside C
         g_host_call_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - _h0).count(); \
     } while (0)
 // launch + (when profiling) time it as an "other" kernel class
-#define BKO(call)                                \
-    do {                                         \
-        auto _t = prof_begin();                  \
-        BKC(call);                               \
-        prof_end(_t, K_OTHER, 0.0, 0.0);         \
-    } while (0)
+// small bookkeeping launches ("other"): not bracketed by timing events — two
+// event records per launch cost ~6 % of a profiled solve; the class's time is
+// the step time minus the timed classes
+#define BKO(call) BKC(call)
 
 // pinned host staging for the per-iteration record and small infos
 struct Pinned {
@@ -168,11 +166,10 @@ public:
             cudaStreamSynchronize(stream_);
             cudaStreamDestroy(stream_);
         }
-        for (auto& p : pending_) {
-            cudaEventDestroy(p.a);
-            cudaEventDestroy(p.b);
+        for (auto& p : pending_) {  // unresolved (solve aborted): back to the pool
+            ev_pool_.push_back(p.a);
+            ev_pool_.push_back(p.b);
         }
-        for (auto e : ev_pool_) cudaEventDestroy(e);
     }
 
     SolveOutput run(const double* x0, int x0_cols);
@@ -193,25 +190,16 @@ private:
         BKC(cudaStreamSynchronize(stream_));
         sync_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         ++syncs_;
-        if (cfg_.profile) {
-            // device-side view of the host round trip: from the previous segment's
-            // resume marker to this segment's first kernel (host think + launch time)
-            cudaEvent_t resume = take_event();
-            BKC(cudaEventRecord(resume, stream_));
-            if (resume_ev_ && !pending_.empty()) {
-                float ms = 0.f;
-                BKC(cudaEventElapsedTime(&ms, resume_ev_, pending_.front().a));
-                bubble_ms_ += ms;
-            }
-            prof_resolve();
-            if (resume_ev_) ev_pool_.push_back(resume_ev_);
-            resume_ev_ = resume;
-            return;
-        }
-        prof_resolve();
+        // profiling: the event pairs are resolved once at the end of the solve
+        // (resolving at every sync put ~100 us of cudaEventElapsedTime calls on
+        // the host critical path per iteration); only the device flags of
+        // predicated launches are captured now, before their slots are reused
+        for (size_t i = captured_; i < pending_.size(); ++i)
+            if (pending_[i].pred) pending_[i].predv = *pending_[i].pred;
+        captured_ = pending_.size();
+        if (pending_.size() > 60000) prof_resolve();
     }
-    cudaEvent_t resume_ev_ = nullptr;
-    double bubble_ms_ = 0.0;
+    size_t captured_ = 0;
     double sync_wait_s_ = 0.0;
     int64_t syncs_ = 0;
     // BLOCKEIG_TIMING: wall time per loop phase (host view, includes waits)
@@ -228,9 +216,16 @@ private:
         int cls;
         cudaEvent_t a, b;
         double bytes, flops;
-        const int* pred;  // predicated launch: host copy of its device flag (valid at resolve)
+        const int* pred;  // predicated launch: host copy of its device flag (valid at the next sync)
+        int predv;        // its value, captured at that sync
     };
-    std::vector<cudaEvent_t> ev_pool_;
+    // timing events are pooled per host thread across solves (a config-2 solve
+    // records ~30k of them)
+    static std::vector<cudaEvent_t>& event_pool() {
+        static thread_local auto* v = new std::vector<cudaEvent_t>;
+        return *v;
+    }
+    std::vector<cudaEvent_t>& ev_pool_ = event_pool();
     std::vector<Pending> pending_;
     KernelStat kstats_[K_CLASSES];
     cudaEvent_t take_event() {
@@ -253,14 +248,14 @@ private:
         if (!a) return;
         cudaEvent_t b = take_event();
         BKC(cudaEventRecord(b, stream_));
-        pending_.push_back({cls, a, b, bytes, flops, pred});
+        pending_.push_back({cls, a, b, bytes, flops, pred, 1});
     }
     void prof_resolve() {
         for (size_t i = 0; i < pending_.size(); ++i) {
             auto& p = pending_[i];
             float ms = 0.f;
             BKC(cudaEventElapsedTime(&ms, p.a, p.b));
-            if (p.pred && *p.pred == 0) {  // predicated off: an empty launch, not K2/K3 work
+            if (p.pred && p.predv == 0) {  // predicated off: an empty launch, not K2/K3 work
                 p.cls = K_OTHER;
                 p.bytes = p.flops = 0.0;
             }
@@ -280,6 +275,7 @@ private:
             ev_pool_.push_back(p.b);
         }
         pending_.clear();
+        captured_ = 0;
     }
     double gap_ms_[K_CLASSES] = {};
 
@@ -299,7 +295,7 @@ private:
     }
     // K2: flops 2*rows*a*b; bytes 8*rows*(a+b)
     void gram(int rows, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc) {
-        auto t = prof_begin();
+        auto t = rows >= n_ ? prof_begin() : nullptr;
         if (cw_ == 1)
             BKC(bk_gram_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), st()));
         else
@@ -311,7 +307,7 @@ private:
     // K3: flops 2*rows*d*k; bytes 8*rows*(d + k (+k when beta != 0))
     void gemm(int rows, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
               double* y, int ldy) {
-        auto t = prof_begin();
+        auto t = rows >= n_ ? prof_begin() : nullptr;
         if (cw_ == 1)
             BKC(bk_gemm_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, st()));
         else
@@ -323,7 +319,7 @@ private:
     // entry is resolved against the flag's host copy (pin_.info[3]) at the next sync
     void gram_if(int rows, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
                  const int* flag, const int* flag_host) {
-        auto t = prof_begin();
+        auto t = rows >= n_ ? prof_begin() : nullptr;
         if (cw_ == 1) BKC(bk_gram_if_d(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), flag, st()));
         else BKC(bk_gram_if_z(rows, x, ldx, a, y, ldy, b, c, ldc, WORK_.p(), flag, st()));
         prof_end(t, rows >= n_ ? K_GRAM : K_OTHER, 8.0 * cw_ * rows * (a + b), 2.0 * cw_ * cw_ * rows * a * b,
@@ -331,7 +327,7 @@ private:
     }
     void gemm_if(int rows, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
                  double beta, double* y, int ldy, const int* flag, const int* flag_host) {
-        auto t = prof_begin();
+        auto t = rows >= n_ ? prof_begin() : nullptr;
         if (cw_ == 1) BKC(bk_gemm_if_d(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, flag, st()));
         else BKC(bk_gemm_if_z(rows, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, CEXP_.p(), flag, st()));
         prof_end(t, rows >= n_ ? K_GEMM : K_OTHER, 8.0 * cw_ * rows * (d + k + (beta != 0.0 ? k : 0)),
@@ -363,12 +359,66 @@ private:
     void random_block(int cols, Blk dst) {
         if (cols <= 0) return;
         const auto t0 = std::chrono::steady_clock::now();
-        // complex: real then imaginary part of each entry (random_block<complex>)
-        std::vector<double> h(static_cast<size_t>(n_) * cols * cw_);
-        rng_.take(h.data(), h.size());
-        upload_colmajor(h.data(), cols, dst);
+        // complex: real then imaginary part of each entry (random_block<complex>);
+        // the stream is drawn straight into pinned chunks and DMA'd asynchronously
+        const size_t count = static_cast<size_t>(n_) * cols * cw_;
+        if (stage_.bytes() < count * sizeof(double)) stage_.alloc(count * sizeof(double));
+        chunked_h2d(stage_.d(), count, [&](double* buf, size_t, size_t len) { rng_.take(buf, len); });
+        if (cw_ == 1) BKC(bk_cm_to_rm_d(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
+        else BKC(bk_cm_to_rm_z(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
         rng_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         rng_cols_ += cols;
+    }
+    // Host <-> device through two pinned 16 MB chunks per host thread: the DMA of
+    // one chunk overlaps the host-side fill / drain of the other (pageable
+    // transfers ran at ~3-8 GB/s and synchronised the stream).
+    static constexpr size_t kChunk = size_t(2) << 20;  // doubles
+    struct PinnedChunks {
+        double* buf[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        bool used[2] = {false, false};
+        PinnedChunks() {
+            for (int i = 0; i < 2; ++i) {
+                BKC(cudaMallocHost(reinterpret_cast<void**>(&buf[i]), kChunk * sizeof(double)));
+                BKC(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+            }
+        }
+    };
+    static PinnedChunks& chunks() {
+        static thread_local PinnedChunks* c = new PinnedChunks;
+        return *c;
+    }
+    template <class Fill>
+    void chunked_h2d(double* dst, size_t count, Fill fill) {
+        auto& c = chunks();
+        for (size_t off = 0, i = 0; off < count; off += kChunk, ++i) {
+            const int b = static_cast<int>(i & 1);
+            const size_t len = std::min(kChunk, count - off);
+            if (c.used[b]) BKC(cudaEventSynchronize(c.ev[b]));  // its previous DMA is done
+            fill(c.buf[b], off, len);
+            BKC(cudaMemcpyAsync(dst + off, c.buf[b], len * sizeof(double), cudaMemcpyHostToDevice, stream_));
+            BKC(cudaEventRecord(c.ev[b], stream_));
+            c.used[b] = true;
+        }
+    }
+    void chunked_d2h(double* dst, const double* src, size_t count) {
+        auto& c = chunks();
+        const size_t nch = (count + kChunk - 1) / kChunk;
+        for (size_t i = 0; i <= nch; ++i) {
+            if (i < nch) {  // DMA chunk i (its buffer was drained at step i - 1)
+                const int b = static_cast<int>(i & 1);
+                const size_t off = i * kChunk, len = std::min(kChunk, count - off);
+                BKC(cudaMemcpyAsync(c.buf[b], src + off, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+                BKC(cudaEventRecord(c.ev[b], stream_));
+                c.used[b] = true;
+            }
+            if (i > 0) {  // drain chunk i - 1 while chunk i is in flight
+                const int b = static_cast<int>((i - 1) & 1);
+                const size_t off = (i - 1) * kChunk, len = std::min(kChunk, count - off);
+                BKC(cudaEventSynchronize(c.ev[b]));
+                std::memcpy(dst + off, c.buf[b], len * sizeof(double));
+            }
+        }
     }
     double rng_s_ = 0.0;
     int64_t rng_cols_ = 0;
@@ -638,8 +688,7 @@ private:
         else BKC(bk_rm_to_cm_z(n_, n_ev, v.p, v.ld, PT_.d(), n_, st()));
         out_.complex_vectors = cw_ == 2;
         out_.vectors.resize(static_cast<size_t>(n_) * n_ev * cw_);
-        BKC(cudaMemcpyAsync(out_.vectors.data(), PT_.d(), out_.vectors.size() * sizeof(double),
-                            cudaMemcpyDeviceToHost, stream_));
+        chunked_d2h(out_.vectors.data(), PT_.d(), out_.vectors.size());
         sync();
         if (cfg_.largest)
             for (auto& x : out_.values) x = -x;
@@ -654,6 +703,7 @@ private:
                          static_cast<long long>(pass2_), static_cast<long long>(proj_calls_),
                          static_cast<long long>(spec_runs_), static_cast<long long>(spec_redos_));
         out_.max_jacobi_sweeps = max_sweeps_;
+        prof_resolve();
         if (std::getenv("BLOCKEIG_TIMING"))
             std::fprintf(stderr,
                          "[blockeig] syncs=%lld host_wait_in_sync=%.3fs host_in_calls=%.3fs phases: other=%.3f "
@@ -662,9 +712,9 @@ private:
                          phase_s_[2], phase_s_[3], phase_s_[4], phase_s_[5], phase_s_[6], phase_s_[7]);
         if (std::getenv("BLOCKEIG_TIMING"))
             std::fprintf(stderr, "[blockeig] device gaps before class (ms): spmm=%.1f gram=%.1f gemm=%.1f syev=%.1f "
-                         "chol=%.1f resid=%.1f other=%.1f; post-sync bubbles %.1f ms; host rng %.3fs for %lld cols\n",
+                         "chol=%.1f resid=%.1f other=%.1f; host rng %.3fs for %lld cols\n",
                          gap_ms_[0], gap_ms_[1], gap_ms_[2], gap_ms_[3], gap_ms_[4], gap_ms_[5], gap_ms_[6],
-                         bubble_ms_, rng_s_, static_cast<long long>(rng_cols_));
+                         rng_s_, static_cast<long long>(rng_cols_));
         for (int c = 0; c < K_CLASSES; ++c) out_.kstats[c] = kstats_[c];
     }
 

@@ -17,6 +17,25 @@
 
 namespace b2 {
 
+// allocator whose value-initialisation is a no-op: resize() without a zero-fill
+// pass over GB-sized host result buffers
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    NoInitAlloc() = default;
+    template <class U>
+    NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U*) noexcept {}
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+
 // ---------------------------------------------------------------- errors
 // Mapped by the C ABI exactly like the reference (proj/src/capi.cpp:24-49):
 // invalid_argument -> INVALID, runtime_error -> NUMERIC, ParseError -> PARSE,
@@ -190,7 +209,9 @@ struct Record {
 struct SolveOutput {
     Status status = Status::max_iters;
     std::vector<double> values;   // n_ev, ascending (descending for `largest`)
-    std::vector<double> vectors;  // n x n_ev column-major (interleaved when complex)
+    // n x n_ev column-major (interleaved when complex); no zero-fill on resize
+    // (the device copy overwrites every element)
+    std::vector<double, NoInitAlloc<double>> vectors;
     bool complex_vectors = false;
     std::vector<Record> history;
     int iterations = 0;
