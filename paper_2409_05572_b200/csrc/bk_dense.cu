@@ -160,8 +160,8 @@ struct GramPlan {
     int splits, rows_per_split;
 };
 
-GramPlan gram_plan(int n, int a, int b, int cps = 2, int tk = GTK) {
-    const int tiles = ceil_div(a, GTM) * ceil_div(b, GTN);
+GramPlan gram_plan(int n, int a, int b, int cps = 2, int tk = GTK, int tm = GTM, int tn = GTN) {
+    const int tiles = ceil_div(a, tm) * ceil_div(b, tn);
     // one wave: cps resident CTAs per SM (register / shared-memory limited), so
     // tiles x splits must not exceed cps x 148 or a straggler wave doubles the time
     int splits = max(1, (cps * kSMs) / tiles);
@@ -271,21 +271,22 @@ extern "C" size_t bk_gram_work_bytes(int n, int a, int b) {
 
 namespace bk {
 namespace {
-template <int TK, int WM, int WN, int ST, int CPS, bool SYM>
+template <int TK, int WM, int WN, int ST, int CPS, bool SYM, int TM = GTM, int TN = GTN>
 int gram_launch_v(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
                   void* work, cudaStream_t s, const int* run_if) {
-    constexpr size_t smem = sizeof(double) * ST * TK * ((GTM + 4) + (GTN + 4));
-    auto k16 = gram_kernel<GTM, GTN, TK, WM, WN, ST, true, SYM>;
-    auto k8 = gram_kernel<GTM, GTN, TK, WM, WN, ST, false, SYM>;
+    static_assert(!SYM || TM == TN, "symmetric tiles are square");
+    constexpr size_t smem = sizeof(double) * ST * TK * ((TM + 4) + (TN + 4));
+    auto k16 = gram_kernel<TM, TN, TK, WM, WN, ST, true, SYM>;
+    auto k8 = gram_kernel<TM, TN, TK, WM, WN, ST, false, SYM>;
     static const cudaError_t a1 = prep(k16, smem);
     static const cudaError_t a2 = prep(k8, smem);
     BK_RET(a1);
     BK_RET(a2);
-    const int nt = ceil_div(a, GTM);
-    const int tiles = SYM ? nt * (nt + 1) / 2 : nt * ceil_div(b, GTN);
+    const int nt = ceil_div(a, TM);
+    const int tiles = SYM ? nt * (nt + 1) / 2 : nt * ceil_div(b, TN);
     // plan with the number of tiles actually launched
-    const GramPlan p = gram_plan(n, SYM ? tiles * GTM : a, SYM ? GTN : b, CPS, TK);
-    const dim3 grid(SYM ? tiles : nt, SYM ? 1 : ceil_div(b, GTN), p.splits);
+    const GramPlan p = gram_plan(n, SYM ? tiles * TM : a, SYM ? TN : b, CPS, TK, TM, TN);
+    const dim3 grid(SYM ? tiles : nt, SYM ? 1 : ceil_div(b, TN), p.splits);
     auto w = static_cast<double*>(work);
     const bool direct = p.splits == 1 && !SYM;  // a single split writes C directly
     double* dst = direct ? c : w;
@@ -297,9 +298,17 @@ int gram_launch_v(int n, const double* x, int ldx, int a, const double* y, int l
     if (!direct) {
         const int64_t total = static_cast<int64_t>(a) * b;
         gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
-            p.splits, a, b, w, c, ldc, SYM ? 1 : 0, GTM, run_if);
+            p.splits, a, b, w, c, ldc, SYM ? 1 : 0, TM, run_if);
     }
     BK_LAUNCHED();
+}
+
+// tile width (72 or 96) that wastes the least of a block width x: the solver's
+// widths are multiples of n_ex and n_es (96 and 69 at config 2), and a 69-wide
+// block in a 96-wide tile leaves 28 % of the DMMA work idle
+inline bool narrow_tile(int x) {
+    const int w96 = ceil_div(x, 96) * 96 - x, w72 = ceil_div(x, 72) * 72 - x;
+    return w72 < w96;
 }
 
 // BK_GRAM_VARIANT selects a tile shape for tuning runs (default 0)
@@ -324,9 +333,22 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
             return gram_launch_v<16, 2, 4, 3, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
         case 4:  // 4 warps of 48 x 48, 32-deep, 3 stages, 1 CTA / SM: 24.6 / 24.5 / 24.3 / 22.2
             return gram_launch_v<32, 2, 2, 3, 1, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
-        default:  // 4 warps of 48 x 48 (36 DMMA per 12 fragment loads), 4 stages, 2 CTAs / SM:
-                  // 30.3 / 29.6 / 28.8 / 24.4
+        default: {  // 4 warps of 48 x 48 (36 DMMA per 12 fragment loads), 4 stages, 2 CTAs / SM:
+                    // 30.3 / 29.6 / 28.8 / 24.4; 72-wide tiles (24-wide warp tiles) for widths
+                    // that fit them better
+            const bool na = narrow_tile(a), nb = narrow_tile(b);
+            if (SYM) {
+                if (na) return gram_launch_v<GTK, 3, 3, GST, 2, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                            run_if);
+            } else if (na && nb) {
+                return gram_launch_v<GTK, 3, 3, GST, 2, false, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+            } else if (nb) {
+                return gram_launch_v<GTK, 2, 3, GST, 2, false, 96, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+            } else if (na) {
+                return gram_launch_v<GTK, 3, 2, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+            }
             return gram_launch_v<GTK, GWM, GWN, GST, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+        }
     }
 }
 }  // namespace
@@ -453,7 +475,9 @@ int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc
             return gemm_launch_v<64, 96, 16, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
         case 4:  // 8 warps of 32 x 48 (the round-1 first shape): 27.8 / 27.4 / 26.0 / 22.5
             return gemm_launch_v<128, 96, 16, 4, 2, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
-        default:  // 4 warps of 64 x 48: 28.3 / 28.1 / 26.3 / 22.2
+        default:  // 4 warps of 64 x 48: 28.3 / 28.1 / 26.3 / 22.2; 72-wide output tiles when they fit k better
+            if (narrow_tile(k))
+                return gemm_launch_v<128, 72, 16, 2, 3, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
             return gemm_launch_v<UTM, UTN, UTK, UWM, UWN, UST>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
                                                                run_if);
     }
