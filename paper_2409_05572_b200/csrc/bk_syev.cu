@@ -361,7 +361,7 @@ int tridiag_cluster_size(int d, size_t* smem) {
 // zero minor takes the sign opposite to its predecessor (the LDL^T form's
 // "q = -pivmin" convention).
 __device__ __forceinline__ int sturm_count(int d, const double* __restrict__ dg, const double* __restrict__ off,
-                                           double x, double pivmin) {
+                                           double x, double pivmin, bool fast4) {
     (void)pivmin;
     constexpr double kBig = 0x1p+500, kScale = 0x1p-500;
     int cnt = 0;
@@ -370,14 +370,15 @@ __device__ __forceinline__ int sturm_count(int d, const double* __restrict__ dg,
     bool neg_prev = false;  // sign of p_{i-1} (p_0 = 1 > 0)
     bool neg = p < 0.0 || (p == 0.0 && !neg_prev);
     cnt += neg != neg_prev;
-    for (int i = 1; i < d; ++i) {
-        const double e = off[i - 1];
-        const double pn = fma(dg[i] - x, p, -(e * e) * pm);
+    auto step = [&](int i) {  // off holds the SQUARED off-diagonal here
+        const double pn = fma(dg[i] - x, p, -off[i - 1] * pm);
         pm = p;
         p = pn;
         neg_prev = neg;
         neg = p < 0.0 || (p == 0.0 && !neg_prev);
         cnt += neg != neg_prev;
+    };
+    auto rescale = [&]() {
         if (fabs(p) > kBig || fabs(pm) > kBig) {
             p *= kScale;
             pm *= kScale;
@@ -385,6 +386,20 @@ __device__ __forceinline__ int sturm_count(int d, const double* __restrict__ dg,
             p *= kBig;
             pm *= kBig;
         }
+    };
+    int i = 1;
+    if (fast4) {  // ||T|| < 2^25: four steps grow |p| by < 2^204, so rescale every fourth
+        for (; i + 3 < d; i += 4) {
+            step(i);
+            step(i + 1);
+            step(i + 2);
+            step(i + 3);
+            rescale();
+        }
+    }
+    for (; i < d; ++i) {
+        step(i);
+        rescale();
     }
     return cnt;
 }
@@ -396,6 +411,16 @@ __global__ void __launch_bounds__(256) bisect_kernel(int d, const double* __rest
     const int lane = threadIdx.x & 31;
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     (void)e2buf;
+    // T (diagonal, squared off-diagonal) in shared memory: the Sturm chain's
+    // operand loads are LDS (~30 cycles) instead of L1/L2 round trips
+    extern __shared__ double bsm_t[];
+    double* sdg = bsm_t;
+    double* se2 = bsm_t + d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        sdg[i] = dg[i];
+        se2[i] = i + 1 < d ? off[i] * off[i] : 0.0;
+    }
+    __syncthreads();
     if (j >= n_need) return;
     // Gershgorin interval and pivmin (every warp, O(d))
     double lo = INFINITY, hi = -INFINITY, emax2 = 0.0;
@@ -415,13 +440,12 @@ __global__ void __launch_bounds__(256) bisect_kernel(int d, const double* __rest
     const double slack = 2.0 * DBL_EPSILON * tnorm + pivmin;
     lo -= slack;
     hi += slack;
-    const double* e2 = off;
     // invariant: count(lo) <= j < count(hi)
     for (int it = 0; it < 40; ++it) {
         const double width = hi - lo;
         if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
         const double x = lo + width * (lane + 1) / 33.0;
-        const int c = sturm_count(d, dg, e2, x, pivmin);
+        const int c = sturm_count(d, sdg, se2, x, pivmin, tnorm < 0x1p+25);
         // first lane whose probe has more than j eigenvalues below it
         const unsigned above = __ballot_sync(0xffffffffu, c > j);
         const int first = above ? __ffs(above) - 1 : 32;
@@ -451,13 +475,16 @@ __global__ void group_kernel(int n_need, const double* __restrict__ lam, const d
     *ngroups = g;
 }
 
-// Solve (T - lam I) y = b in place (b -> y) by Gaussian elimination with partial
-// pivoting on the tridiagonal (rows i, i+1 may swap; fill in u2).  Tiny pivots are
-// replaced by +-eps*||T|| (inverse iteration on an intentionally singular shift).
-__device__ void tri_solve_shifted(int d, const double* __restrict__ dg, const double* __restrict__ off, double lam,
-                                  double tiny, double* __restrict__ b, double* __restrict__ u0,
-                                  double* __restrict__ u1, double* __restrict__ u2, int* __restrict__ piv) {
-    // rows: a_i = off[i-1] (sub), b_i = dg[i]-lam (diag), c_i = off[i] (super)
+// LU of T - lam I by Gaussian elimination with partial pivoting on the
+// tridiagonal (rows i, i+1 may swap; fill-in in u2), stored for repeated
+// solves: multipliers, swap flags, the two super-diagonals of U and the
+// reciprocal pivots (tiny pivots replaced by +-eps*||T||: inverse iteration on
+// an intentionally singular shift).  Factor once, then each inverse-iteration
+// step is division-free.
+__device__ void tri_factor(int d, const double* __restrict__ dg, const double* __restrict__ off, double lam,
+                           double tiny, double* __restrict__ mult, double* __restrict__ rinv,
+                           double* __restrict__ u1, double* __restrict__ u2, unsigned char* __restrict__ swp) {
+    auto guard = [&](double p) { return fabs(p) < tiny ? copysign(tiny, p == 0.0 ? 1.0 : p) : p; };
     double diag_cur = dg[0] - lam;
     double sup_cur = d > 1 ? off[0] : 0.0;
     double sup2_cur = 0.0;
@@ -465,40 +492,51 @@ __device__ void tri_solve_shifted(int d, const double* __restrict__ dg, const do
         const double sub = off[i];  // A(i+1, i)
         const double nd = dg[i + 1] - lam;
         const double ns = i + 2 < d ? off[i + 1] : 0.0;
-        if (fabs(sub) > fabs(diag_cur)) {
-            // swap rows i and i+1
-            const double mult = diag_cur / sub;
-            u0[i] = sub;
+        if (fabs(sub) > fabs(diag_cur)) {  // swap rows i and i+1
+            const double m = diag_cur / sub;
+            mult[i] = m;
+            swp[i] = 1;
+            rinv[i] = 1.0 / sub;
             u1[i] = nd;
             u2[i] = ns;
-            const double bi = b[i];
-            b[i] = b[i + 1];
-            b[i + 1] = bi - mult * b[i];
-            diag_cur = sup_cur - mult * nd;
-            sup_cur = sup2_cur - mult * ns;
+            diag_cur = sup_cur - m * nd;
+            sup_cur = sup2_cur - m * ns;
             sup2_cur = 0.0;
         } else {
-            const double p0 = fabs(diag_cur) < tiny ? copysign(tiny, diag_cur == 0.0 ? 1.0 : diag_cur) : diag_cur;
-            const double mult = sub / p0;
-            u0[i] = p0;
+            const double p0 = guard(diag_cur);
+            const double m = sub / p0;
+            mult[i] = m;
+            swp[i] = 0;
+            rinv[i] = 1.0 / p0;
             u1[i] = sup_cur;
             u2[i] = sup2_cur;
-            b[i + 1] -= mult * b[i];
-            diag_cur = nd - mult * sup_cur;
+            diag_cur = nd - m * sup_cur;
             sup_cur = ns;
             sup2_cur = 0.0;
         }
     }
-    u0[d - 1] = fabs(diag_cur) < tiny ? copysign(tiny, diag_cur == 0.0 ? 1.0 : diag_cur) : diag_cur;
-    // back substitution with the upper band (u0 diag, u1 first, u2 second super-diagonal)
+    rinv[d - 1] = 1.0 / guard(diag_cur);
+}
+
+// b <- (T - lam I)^{-1} b with the stored factors
+__device__ void tri_apply(int d, const double* __restrict__ mult, const double* __restrict__ rinv,
+                          const double* __restrict__ u1, const double* __restrict__ u2,
+                          const unsigned char* __restrict__ swp, double* __restrict__ b) {
+    for (int i = 0; i + 1 < d; ++i) {
+        if (swp[i]) {
+            const double bi = b[i];
+            b[i] = b[i + 1];
+            b[i + 1] = bi - mult[i] * b[i];
+        } else {
+            b[i + 1] -= mult[i] * b[i];
+        }
+    }
     for (int i = d - 1; i >= 0; --i) {
         double s = b[i];
         if (i + 1 < d) s -= u1[i] * b[i + 1];
         if (i + 2 < d) s -= u2[i] * b[i + 2];
-        const double p0 = fabs(u0[i]) < tiny ? copysign(tiny, u0[i] == 0.0 ? 1.0 : u0[i]) : u0[i];
-        b[i] = s / p0;
+        b[i] = s * rinv[i];
     }
-    (void)piv;
 }
 
 // one warp per wanted eigenvalue j; u column-major (ldu = d): column j = the
@@ -524,11 +562,13 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
     dg = sdg;
     off = soff;
     if (j >= n_need) return;
-    double* b = ism + 2 * d + static_cast<size_t>(wib) * 4 * d;
-    double* u0 = b + d;
-    double* u1 = u0 + d;
+    // per warp: b, mult, rinv, u1, u2 (5d doubles) + swap flags (d bytes)
+    double* b = ism + 2 * d + static_cast<size_t>(wib) * (5 * d + (d + 7) / 8);
+    double* mult = b + d;
+    double* rinv = mult + d;
+    double* u1 = rinv + d;
     double* u2 = u1 + d;
-    int piv[1];
+    unsigned char* swp = reinterpret_cast<unsigned char*>(u2 + d);
     double tnorm = 0.0;
     for (int i = lane; i < d; i += 32)
         tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0));
@@ -548,8 +588,10 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
     const double shift = lam[j];
     // two steps: with the shift accurate to ~eps ||T|| and clusters (gap < 1e-7 ||T||)
     // treated as blocks, each step shrinks foreign components by <= eps/1e-7
+    if (lane == 0) tri_factor(d, dg, off, shift, tiny, mult, rinv, u1, u2, swp);
+    __syncwarp();
     for (int it = 0; it < 2; ++it) {
-        if (lane == 0) tri_solve_shifted(d, dg, off, shift, tiny, b, u0, u1, u2, piv);
+        if (lane == 0) tri_apply(d, mult, rinv, u1, u2, swp, b);
         __syncwarp();
         double nn = 0.0;
         for (int i = lane; i < d; i += 32) nn = fma(b[i], b[i], nn);
@@ -969,14 +1011,17 @@ namespace {
 // n_need in w.u) of the tridiagonal T in (w.dg, w.off)
 int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, void* stream) {
     const cudaStream_t s = as_stream(stream);
-    bisect_kernel<<<ceil_div(n_need * 32, 256), 256, 0, s>>>(d, w.dg, w.off, n_need, values, w.e2);
+    // latency-bound chains: two warps per CTA so the n_need warps spread over the
+    // SMs instead of queueing 8 to an SM (12 SMs busy at n_need = 96 before)
+    bisect_kernel<<<ceil_div(n_need * 32, 64), 64, 2 * sizeof(double) * d, s>>>(d, w.dg, w.off, n_need, values,
+                                                                                 w.e2);
     group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
     {
-        const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 4 * 4 * static_cast<size_t>(d));
+        const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 2 * (5 * static_cast<size_t>(d) + (d + 7) / 8));
         static const cudaError_t ai = cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           static_cast<int>(sizeof(double) * 18 * kSyevMaxD));
+                                                           static_cast<int>(sizeof(double) * 14 * kSyevMaxD));
         BK_RET(ai);
-        invit_kernel<<<ceil_div(n_need * 32, 128), 128, ism, s>>>(d, w.dg, w.off, values, n_need, w.u);
+        invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u);
     }
     cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need);
     // clusters -> orthonormal blocks: Gram, per-cluster Cholesky (block-diagonal
