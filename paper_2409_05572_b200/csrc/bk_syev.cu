@@ -378,14 +378,11 @@ __device__ __forceinline__ int sturm_count(int d, const double* __restrict__ dg,
         neg = p < 0.0 || (p == 0.0 && !neg_prev);
         cnt += neg != neg_prev;
     };
-    auto rescale = [&]() {
-        if (fabs(p) > kBig || fabs(pm) > kBig) {
-            p *= kScale;
-            pm *= kScale;
-        } else if (fabs(p) < kScale && fabs(pm) < kScale) {
-            p *= kBig;
-            pm *= kBig;
-        }
+    auto rescale = [&]() {  // branchless: the lanes' probes diverge in magnitude
+        const double ap = fmax(fabs(p), fabs(pm));
+        const double f = ap > kBig ? kScale : (ap < kScale ? kBig : 1.0);
+        p *= f;
+        pm *= f;
     };
     int i = 1;
     if (fast4) {  // ||T|| < 2^25: four steps grow |p| by < 2^204, so rescale every fourth
