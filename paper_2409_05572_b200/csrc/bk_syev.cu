@@ -78,8 +78,10 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_fused_kernel(int d, const
         x = warp_sum(x);
         if (lane == 0) red[wid] = x;
         __syncthreads();
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += red[w];
+        // second level by shuffles in every warp (one LDS per lane instead of a
+        // serial walk over the warp partials): same butterfly everywhere, so every
+        // thread — and every CTA of a cluster — gets bit-identical results
+        const double s = warp_sum(lane < nw ? red[lane] : 0.0);
         __syncthreads();
         return s;
     };
@@ -225,8 +227,10 @@ __global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, cons
         x = warp_sum(x);
         if (lane == 0) red[wid] = x;
         __syncthreads();
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += red[w];
+        // second level by shuffles in every warp (one LDS per lane instead of a
+        // serial walk over the warp partials): same butterfly everywhere, so every
+        // thread — and every CTA of a cluster — gets bit-identical results
+        const double s = warp_sum(lane < nw ? red[lane] : 0.0);
         __syncthreads();
         return s;
     };
@@ -304,9 +308,11 @@ __global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, cons
         double pv = 0.0;
         for (int i = k + 1 + tid; i < d; i += nt) pv = fma(p[i], v[i], pv);
         const double kk = -0.5 * t * block_sum(pv);
-        for (int i = k + 1 + tid; i < d; i += nt) {
-            wp[i] = fma(kk, v[i], p[i]);
-            vp[i] = v[i];
+        for (int i = k + 1 + tid; i < d; i += nt) wp[i] = fma(kk, v[i], p[i]);
+        {  // v becomes the pending vp (local buffers: a pointer swap, no copy)
+            double* t2 = vp;
+            vp = v;
+            v = t2;
         }
         __syncthreads();
     }
@@ -341,7 +347,14 @@ cudaError_t prep_smem(K kernel, size_t bytes) {
 
 // cluster size for the distributed tridiagonalisation, 0 when it does not fit
 int tridiag_cluster_size(int d, size_t* smem) {
-    for (int c = 1; c <= 16; c *= 2) {
+    // at least 8 CTAs: shorter per-rank row passes outweigh the wider cluster
+    // barrier (d = 288: 1.93 -> 1.84 ms per syev; 16 is slower again).
+    // BK_TRI_CLUSTER overrides the minimum (tuning runs only).
+    static const int c0 = [] {
+        const char* e = getenv("BK_TRI_CLUSTER");
+        return e ? max(1, atoi(e)) : 8;
+    }();
+    for (int c = c0; c <= 16; c *= 2) {
         const size_t nloc = static_cast<size_t>((d + c - 1) / c);
         const size_t bytes = sizeof(double) * (nloc * d + 5 * static_cast<size_t>(d) + 8);
         if (bytes <= 200 * 1024) {
@@ -812,8 +825,7 @@ __global__ void __launch_bounds__(kCoopThreads) tridiag_coop_kernel(int d, E* __
         xn2 = warp_sum(xn2);
         if (lane == 0) red_d[wid] = xn2;
         __syncthreads();
-        xn2 = 0.0;
-        for (int w = 0; w < nw; ++w) xn2 += red_d[w];
+        xn2 = warp_sum(lane < nw ? red_d[lane] : 0.0);
         const E alpha = vcur[j + 1];
         E t = mk<E>(0.0, 0.0);
         double beta = re_(alpha);
