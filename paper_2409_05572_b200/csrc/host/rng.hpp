@@ -20,6 +20,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <limits>
+#include <cstring>
 #include <mutex>
 #include <random>
 #include <thread>
@@ -56,11 +57,15 @@ public:
                 avail = produced_ - head_;
             }
             const size_t use = std::min(avail, pairs - done);
-            for (size_t p = 0; p < use; ++p) {
+            // the ring holds (y * mult, x * mult) pairs in output order: copy the
+            // (at most two) contiguous ring segments; an odd block drops the last x
+            for (size_t p = 0; p < use;) {
                 const size_t slot = (head_ + p) % cap_;
+                const size_t seg = std::min(use - p, cap_ - slot);
                 const size_t i = 2 * (done + p);
-                out[i] = ring_[2 * slot];  // y * mult (returned first)
-                if (i + 1 < count) out[i + 1] = ring_[2 * slot + 1];  // cached x * mult
+                const size_t n = std::min(2 * seg, count - i);
+                std::memcpy(out + i, ring_.data() + 2 * slot, n * sizeof(double));
+                p += seg;
             }
             {
                 std::lock_guard<std::mutex> lk(mu_);
