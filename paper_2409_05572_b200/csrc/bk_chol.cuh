@@ -24,6 +24,8 @@ __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__
                                                double* __restrict__ s, int smem_max_a, double* dyn_s,
                                                bool pairs = false) {
     __shared__ int s_unsure, s_bad;
+    __shared__ double s_recip[2];  // 1 / next pivot, computed by thread 0 during the previous step
+    __shared__ int s_recip_ok[2];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
     // shared layout: gd[a] r2[a] piv[a] slot[a] (ints) | Schur complement s (a <= kCholSmemMaxA)
@@ -40,8 +42,11 @@ __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__
     if (tid == 0) {
         s_unsure = 0;
         s_bad = 0;
+        s_recip_ok[0] = s_recip_ok[1] = 0;
     }
     __syncthreads();
+    const double drop2 = drop * drop;
+    constexpr double kLo2 = (1.0 - 1e-4) * (1.0 - 1e-4), kHi2 = (1.0 + 1e-4) * (1.0 + 1e-4);
     // right-looking skip-pivot Cholesky with ONE barrier per pivot: every thread
     // evaluates the (identical) keep decision itself; row j stays unscaled
     // during the step and R is formed in a final pass.
@@ -63,26 +68,38 @@ __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__
             keep = p > 0.0;
             unsure = p <= 1e-8 * gjj;  // pass 2 of CholQR2: basis lost rank
         } else {
-            const double thr = drop * sqrt(r2[j]);
-            if (r2[j] == 0.0 || gjj < thr * thr) {
+            // squared form of "remaining norm >= drop * original norm" (no sqrt on
+            // the sequential path); the uncertainty band |sqrt(p) - thr| < 1e-4 thr
+            // becomes p in ((1-1e-4)^2 thr^2, (1+1e-4)^2 thr^2)
+            const double thr2 = drop2 * r2[j];
+            if (r2[j] == 0.0 || gjj < thr2) {
                 keep = 0;  // certain: the pivot can never exceed the projected norm
             } else {
-                keep = p >= thr * thr;
-                unsure = p < 1e-8 * gjj || fabs(sqrt(fmax(p, 0.0)) - thr) < 1e-4 * thr;
+                keep = p >= thr2;
+                unsure = p < 1e-8 * gjj || (p > kLo2 * thr2 && p < kHi2 * thr2);
             }
         }
+        const int par = j & 1;
+        const double invp = keep ? (s_recip_ok[par] ? s_recip[par] : 1.0 / p) : 0.0;
+        __syncwarp();
         if (tid == 0) {
             if (unsure) s_unsure = 1;
             if (bad) s_bad = 1;
             slot[j] = keep ? kept : -1;
             piv[j] = p;
+            s_recip_ok[par ^ 1] = 0;
         }
         if (keep) {
             ++kept;
-            const double invp = 1.0 / p;
             for (int k = j + 1 + wid; k < a; k += nw) {
                 const double rk = s[j * a + k] * invp;
                 for (int l = k + lane; l < a; l += 32) s[k * a + l] -= rk * s[j * a + l];
+                // thread 0 owns the next pivot s[j+1][j+1] (first row of warp 0,
+                // first element of lane 0): its reciprocal, off the other warps' path
+                if (tid == 0 && k == j + 1) {
+                    s_recip[par ^ 1] = 1.0 / s[k * a + k];
+                    s_recip_ok[par ^ 1] = 1;
+                }
             }
         }
         __syncthreads();
