@@ -16,6 +16,8 @@
 // d/2 disjoint pairs at once, each 2x2 block of H is updated by one thread
 // (rows and columns in one pass), and V accumulates the rotations.  H lives in
 // shared memory up to d = 160 and in global memory (L2-resident) above.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 #include <cstdlib>
 
@@ -34,6 +36,124 @@ __global__ void __launch_bounds__(1024) chol_drop_kernel(int a, const double* __
                                                           int pairs) {
     extern __shared__ double dyn_s[];
     chol_drop_body(a, g, ldg, ref2, drop, m, ldm, info, s, kCholSmemMaxA, dyn_s, pairs != 0);
+}
+
+// Grid-cooperative variant for blocks beyond shared memory (a > kCholSmemMaxA:
+// config 5's 768-wide real embedding of a 384-wide complex Gram, config 3's SI
+// block of 200): the same decisions, operation order and output as
+// chol_drop_body, with the Schur complement in global memory (L2-resident), its
+// rows dealt over every warp of the grid and one grid barrier per pivot.  One
+// CTA walking a 768 x 768 complement through L2 took 40 ms; the grid takes ~2.
+// work layout: s (a x a) | gd, r2, piv (a each) | slot (a ints) | flags (4 ints)
+__global__ void __launch_bounds__(1024) chol_coop_kernel(int a, const double* __restrict__ g, int ldg,
+                                                          const double* __restrict__ ref2, double drop,
+                                                          double* __restrict__ m, int ldm, int* __restrict__ info,
+                                                          double* __restrict__ s, int pairs) {
+    namespace cgr = cooperative_groups;
+    cgr::grid_group grid = cgr::this_grid();
+    double* gd = s + static_cast<size_t>(a) * a;
+    double* r2 = gd + a;
+    double* piv = r2 + a;
+    int* slot = reinterpret_cast<int*>(piv + a);
+    int* flags = slot + a;  // [0] unsure, [1] bad
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
+    const int gw = gtid >> 5, gwarps = gthreads >> 5;
+    const bool lead = gtid == 0;
+    for (size_t e = gtid; e < static_cast<size_t>(a) * a; e += gthreads)
+        s[e] = g[(e / a) * ldg + e % a];
+    for (int j = gtid; j < a; j += gthreads) {
+        gd[j] = g[static_cast<size_t>(j) * ldg + j];
+        r2[j] = ref2 ? ref2[j] : 0.0;
+    }
+    if (lead) flags[0] = flags[1] = 0;
+    grid.sync();
+    const double drop2 = drop * drop;
+    constexpr double kLo2 = (1.0 - 1e-4) * (1.0 - 1e-4), kHi2 = (1.0 + 1e-4) * (1.0 + 1e-4);
+    int kept = 0;
+    for (int j = 0; j < a; ++j) {
+        const double p = s[static_cast<size_t>(j) * a + j];
+        const double gjj = gd[j];
+        int keep;
+        bool unsure = false, bad = false;
+        if (!isfinite(p) || !isfinite(gjj)) {
+            bad = true;
+            keep = 0;
+        } else if (pairs && (j & 1)) {
+            keep = slot[j - 1] >= 0 && p > 0.0;
+            unsure = (slot[j - 1] >= 0) != (p > 0.0);
+        } else if (ref2 == nullptr) {
+            keep = p > 0.0;
+            unsure = p <= 1e-8 * gjj;
+        } else {
+            const double thr2 = drop2 * r2[j];
+            if (r2[j] == 0.0 || gjj < thr2) {
+                keep = 0;
+            } else {
+                keep = p >= thr2;
+                unsure = p < 1e-8 * gjj || (p > kLo2 * thr2 && p < kHi2 * thr2);
+            }
+        }
+        if (lead) {
+            if (unsure) flags[0] = 1;
+            if (bad) flags[1] = 1;
+            slot[j] = keep ? kept : -1;
+            piv[j] = p;
+        }
+        if (keep) {
+            ++kept;
+            const double invp = 1.0 / p;
+            const double* rowj = s + static_cast<size_t>(j) * a;
+            for (int k = j + 1 + gw; k < a; k += gwarps) {
+                const double rk = rowj[k] * invp;
+                double* rowk = s + static_cast<size_t>(k) * a;
+                for (int l = k + lane; l < a; l += 32) rowk[l] -= rk * rowj[l];
+            }
+        }
+        grid.sync();
+    }
+    for (size_t e = gtid; e < static_cast<size_t>(a) * a; e += gthreads) {
+        const int j = static_cast<int>(e / a), l = static_cast<int>(e % a);
+        if (l < j || slot[j] < 0) continue;
+        const double rj = sqrt(piv[j]);
+        s[e] = l == j ? rj : s[e] / rj;
+    }
+    grid.sync();
+    for (size_t e = gtid; e < static_cast<size_t>(a) * a; e += gthreads) {
+        const int j = static_cast<int>(e / a), l = static_cast<int>(e % a);
+        if (l > j && (slot[j] < 0 || slot[l] < 0)) s[e] = 0.0;
+    }
+    grid.sync();
+    for (int i = gtid; i < a; i += gthreads) piv[i] = slot[i] >= 0 ? 1.0 / s[static_cast<size_t>(i) * a + i] : 0.0;
+    grid.sync();
+    for (int c = gw; c < a; c += gwarps) {
+        if (slot[c] < 0) continue;
+        const double* rowc = s + static_cast<size_t>(c) * a;
+        for (int i = c - 1; i >= 0; --i) {
+            if (slot[i] < 0) continue;
+            const double* rowi = s + static_cast<size_t>(i) * a;
+            double acc = 0.0;
+            for (int l = i + 1 + lane; l < c; l += 32) acc = fma(rowi[l], rowc[l], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) s[static_cast<size_t>(c) * a + i] = -(acc + rowi[c] * piv[c]) * piv[i];
+            __syncwarp();
+        }
+    }
+    grid.sync();
+    for (size_t e = gtid; e < static_cast<size_t>(a) * a; e += gthreads)
+        m[(e / a) * ldm + e % a] = 0.0;
+    grid.sync();
+    for (size_t e = gtid; e < static_cast<size_t>(a) * a; e += gthreads) {
+        const int i = static_cast<int>(e / a), c = static_cast<int>(e % a);
+        if (i > c || slot[i] < 0 || slot[c] < 0) continue;
+        const double val = i == c ? piv[c] : s[static_cast<size_t>(c) * a + i];
+        m[static_cast<size_t>(i) * ldm + slot[c]] = val;
+    }
+    if (lead) {
+        info[0] = kept;
+        info[1] = flags[0];
+        info[2] = flags[1];
+    }
 }
 
 // ------------------------------------------------------------------ K5
@@ -221,6 +341,18 @@ int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop
     BK_RET(attr);
     const size_t small = (3 * static_cast<size_t>(a) + (a + 1) / 2) * sizeof(double);
     const size_t smem = small + (a <= kCholSmemMaxA ? static_cast<size_t>(a) * a * sizeof(double) : 0);
+    if (a > kCholSmemMaxA) {
+        // grid-cooperative: one warp per trailing row at most, one CTA per SM at most
+        int per_sm = 0;
+        BK_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, 1024, 0));
+        const int grid = max(1, min(min(ceil_div(a, 32), kSMs), max(per_sm, 1) * kSMs));
+        int aa = a, l1 = ldg, l2 = ldm, pr = pairs ? 1 : 0;
+        void* args[] = {&aa, const_cast<double**>(&g), &l1, const_cast<double**>(&ref2), &drop, &m, &l2, &info, &s,
+                        &pr};
+        BK_RET(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(chol_coop_kernel), dim3(grid), dim3(1024),
+                                           args, 0, st));
+        return 0;
+    }
     // 1024 threads: the per-pivot rank-1 updates are the work (fewer warps measured
     // 1.3-4x slower at a = 96..288)
     chol_drop_kernel<<<1, 1024, smem, st>>>(a, g, ldg, ref2, drop, m, ldm, info, s, pairs ? 1 : 0);

@@ -195,3 +195,19 @@ def test_chol_drop_rule(bk):
     w2 = np.c_[x, x[:, 1] - x[:, 2] + 1e-10 * rng.standard_normal(15)]
     kept2, unsure2, _ = _chol(bk, w2)
     assert unsure2 == 1
+
+
+@pytest.mark.parametrize("a", [150, 200, 520])
+def test_chol_large_blocks(bk, a):
+    # a > 160 runs the grid-cooperative Cholesky (Schur complement in L2); same
+    # drop rule and output layout as the shared-memory kernel
+    rng = np.random.default_rng(a)
+    n = 4 * a
+    w = rng.standard_normal((n, a))
+    w[:, 7] = 0.0                     # certain drop
+    w[:, 11] = w[:, 3] + 1e-3 * w[:, 11]  # kept (well above the 1e-8 threshold)
+    kept, unsure, m = _chol(bk, w)
+    assert (kept, unsure) == (a - 1, 0)
+    assert np.abs(m[7]).max() == 0.0
+    q = w @ m[:, :kept]
+    assert np.abs(q.T @ q - np.eye(kept)).max() < 1e-7  # one CholQR pass (NS polish follows in K4)
