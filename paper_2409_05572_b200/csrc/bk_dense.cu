@@ -160,12 +160,38 @@ struct GramPlan {
     int splits, rows_per_split;
 };
 
-GramPlan gram_plan(int n, int a, int b, int cps = 2, int tk = GTK, int tm = GTM, int tn = GTN) {
-    const int tiles = ceil_div(a, tm) * ceil_div(b, tn);
-    // one wave: cps resident CTAs per SM (register / shared-memory limited), so
-    // tiles x splits must not exceed cps x 148 or a straggler wave doubles the time
-    int splits = max(1, (cps * kSMs) / tiles);
-    splits = max(1, min(splits, ceil_div(n, 256)));  // >= 256 rows per split
+// Split-K partials budget (doubles) for an a x b Gram over n rows: the partial
+// tiles may add at most 1/40 of the input traffic, but never less than two
+// full waves of 96 x 96 tiles' worth (small outputs)
+inline size_t gram_budget(int n, int a, int b) {
+    const size_t floor_elems = 2 * (2 * static_cast<size_t>(kSMs) + 8) * 96 * 96;
+    const size_t traffic = static_cast<size_t>(max(n, 1)) * (max(a, 1) + max(b, 1)) / 40;
+    return std::max(floor_elems, traffic);
+}
+
+// Split count for `tiles` output tiles (partial size a*b per split): enough CTAs
+// for whole waves of cps x 148 resident CTAs — a last wave with a handful of
+// CTAs doubles the time (config 5's Hermitian Rayleigh-Ritz Gram has 300 upper
+// tiles of the 2304-wide real view: one split is 300 CTAs on 296 slots) — within
+// the partials budget and >= 256 rows per split.
+GramPlan gram_plan(int n, int tiles, int a, int b, int cps = 2, int tk = GTK) {
+    const int slots = cps * kSMs;
+    int max_split = max(1, ceil_div(n, 256));
+    const size_t out_elems = static_cast<size_t>(max(a, 1)) * max(b, 1);
+    const size_t by_budget = gram_budget(n, a, b) / out_elems;
+    max_split = static_cast<int>(std::min<size_t>(static_cast<size_t>(max_split), std::max<size_t>(1, by_budget)));
+    int splits = 1;
+    double best = 0.0;
+    for (int sp = 1; sp <= max_split; ++sp) {
+        const int ctas = tiles * sp;
+        const int waves = ceil_div(ctas, slots);
+        const double eff = static_cast<double>(ctas) / (static_cast<double>(waves) * slots);
+        if (eff > best + 0.01) {  // fewest splits within 1 % of the best wave efficiency
+            best = eff;
+            splits = sp;
+        }
+        if (ctas >= 64 * slots) break;
+    }
     int rps = ceil_div(n, splits);
     rps = ceil_div(rps, tk) * tk;
     splits = max(1, ceil_div(n, rps));
@@ -260,13 +286,10 @@ cudaError_t prep(K kernel, size_t smem) {
 using namespace bk;
 
 extern "C" size_t bk_gram_work_bytes(int n, int a, int b) {
-    // partials = splits x a' x b' for any call with a' <= a, b' <= b: splits x
-    // tiles <= 2 x 148 (+ rounding) and a' b' <= tiles x 96^2 (x 2 for the
-    // symmetric variant, which launches only the upper tiles), and splits <=
-    // n / 256 + 1
-    const size_t cap = 2 * (2 * static_cast<size_t>(kSMs) + 8) * GTM * GTN;
+    // partials = splits x a' x b' for any call with a' <= a, b' <= b: at most the
+    // budget of gram_plan (monotone in a, b), and splits <= n / 256 + 1
     const size_t small = (static_cast<size_t>(ceil_div(max(n, 1), 256)) + 1) * max(a, 1) * max(b, 1);
-    return std::min(cap, small) * sizeof(double);
+    return std::min(gram_budget(n, a, b), small) * sizeof(double);
 }
 
 namespace bk {
@@ -285,7 +308,7 @@ int gram_launch_v(int n, const double* x, int ldx, int a, const double* y, int l
     const int nt = ceil_div(a, TM);
     const int tiles = SYM ? nt * (nt + 1) / 2 : nt * ceil_div(b, TN);
     // plan with the number of tiles actually launched
-    const GramPlan p = gram_plan(n, SYM ? tiles * TM : a, SYM ? TN : b, CPS, TK, TM, TN);
+    const GramPlan p = gram_plan(n, tiles, a, b, CPS, TK);
     const dim3 grid(SYM ? tiles : nt, SYM ? 1 : ceil_div(b, TN), p.splits);
     auto w = static_cast<double*>(work);
     const bool direct = p.splits == 1 && !SYM;  // a single split writes C directly
