@@ -330,8 +330,10 @@ int gram_launch_v(int n, const double* x, int ldx, int a, const double* y, int l
 // widths are multiples of n_ex and n_es (96 and 69 at config 2), and a 69-wide
 // block in a 96-wide tile leaves 28 % of the DMMA work idle
 inline bool narrow_tile(int x) {
+    // the 72-wide tiles run ~25 % below the 96-wide ones per tile, so they only
+    // pay when they cut the padding by more than a quarter of the width
     const int w96 = ceil_div(x, 96) * 96 - x, w72 = ceil_div(x, 72) * 72 - x;
-    return w72 < w96;
+    return 4 * (w96 - w72) > x;
 }
 
 // BK_GRAM_VARIANT selects a tile shape for tuning runs (default 0)
@@ -360,15 +362,38 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
                     // 30.3 / 29.6 / 28.8 / 24.4; 72-wide tiles (24-wide warp tiles) for widths
                     // that fit them better
             const bool na = narrow_tile(a), nb = narrow_tile(b);
-            if (SYM) {
-                if (na) return gram_launch_v<GTK, 3, 3, GST, 2, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
-                                                                            run_if);
-            } else if (na && nb) {
-                return gram_launch_v<GTK, 3, 3, GST, 2, false, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
-            } else if (nb) {
-                return gram_launch_v<GTK, 2, 3, GST, 2, false, 96, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
-            } else if (na) {
-                return gram_launch_v<GTK, 3, 2, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+            static const int nv = [] {  // BK_NARROW: warp layout of the 72-wide tiles (tuning runs)
+                const char* e = getenv("BK_NARROW");
+                return e ? atoi(e) : 1;
+            }();
+            if (nv == 0) {
+                if (SYM) {
+                    if (na) return gram_launch_v<GTK, 3, 3, GST, 2, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work,
+                                                                                s, run_if);
+                } else if (na && nb) {
+                    return gram_launch_v<GTK, 3, 3, GST, 2, false, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
+                } else if (nb) {
+                    return gram_launch_v<GTK, 2, 3, GST, 2, false, 96, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
+                } else if (na) {
+                    return gram_launch_v<GTK, 3, 2, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
+                }
+            } else {  // full-width warp tiles along the 72 side: 27 DMMA per 12 fragment loads
+                if (SYM) {
+                    if (na) return gram_launch_v<GTK, 3, 1, GST, 2, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work,
+                                                                                s, run_if);
+                } else if (na && nb) {
+                    return gram_launch_v<GTK, 3, 1, GST, 2, false, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
+                } else if (nb) {
+                    return gram_launch_v<GTK, 4, 1, GST, 2, false, 96, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
+                } else if (na) {
+                    return gram_launch_v<GTK, 1, 4, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
+                }
             }
             return gram_launch_v<GTK, GWM, GWN, GST, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
         }

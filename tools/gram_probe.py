@@ -15,7 +15,7 @@ f.bk_gram_work_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
 f.bk_gram_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, _D, _D]
 a, b = int(sys.argv[1]), int(sys.argv[2])
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 262144
-ld = 344
+ld = max(344, (max(a, b) + 7) // 8 * 8)
 x = torch.randn(n, ld, dtype=torch.float64, device="cuda")
 y = torch.randn(n, ld, dtype=torch.float64, device="cuda")
 c = torch.zeros(a, b, dtype=torch.float64, device="cuda")
