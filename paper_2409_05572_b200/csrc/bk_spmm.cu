@@ -252,7 +252,12 @@ extern "C" int bk_spmm_d(int n, const int32_t* rp, const int32_t* ci, const doub
         BK_LAUNCHED();
     }
     const SpmmShape sh = spmm_shape();
-    const int tg = max(1, min(ceil_div(n, sh.tile), kSMs * sh.cps));
+    // wide blocks (k > 96: 4-6 accumulators per lane, fewer resident warps) run
+    // with twice the CTAs per SM in the sweep: config 4's k = 160 2.39 -> 1.90 ms
+    // (BK_SPMM_CPS overrides; 8 nonzeros in flight per step measured slower at
+    // k = 96 and no better at k = 160)
+    const int cps = getenv("BK_SPMM_CPS") ? sh.cps : (k > 96 ? 8 : 4);
+    const int tg = max(1, min(ceil_div(n, sh.tile), kSMs * cps));
     if (k <= 32)
         spmm_d_kernel<1><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
     else if (k <= 64)
