@@ -92,10 +92,11 @@ __global__ void __launch_bounds__(256) spmm_z_kernel(int n, const int32_t* __res
                                                       const int32_t* __restrict__ ci,
                                                       const double2* __restrict__ val,
                                                       const double2* __restrict__ x, int ldx, int k,
-                                                      double2* __restrict__ y, int ldy) {
-    const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+                                                      double2* __restrict__ y, int ldy, int tile) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // the real kernel's tiled sweep (tile rows per CTA step, resident CTAs)
+    for (int t0 = blockIdx.x * tile; t0 < n; t0 += gridDim.x * tile)
+    for (int row = t0 + warp; row < min(n, t0 + tile); row += nw) {
         const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
         for (int c0 = 0; c0 < k; c0 += 32 * VPL) {
             double2 acc[VPL];
@@ -277,15 +278,27 @@ extern "C" int bk_spmm_z(int n, const int32_t* rp, const int32_t* ci, const doub
                          const double* x, int ldx, int k, double* y, int ldy, void* stream) {
     if (n <= 0 || k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
-    const int grid = spmm_grid(n);
+    const SpmmShape sh = spmm_shape();
+    // wide complex blocks: 128 columns per lane chunk (4 x 16 B), 8 CTAs per SM in
+    // the sweep — config 5's k = 384 SpMM 3.38 -> 2.96 ms (68 % of HBM)
+    const int cps = getenv("BK_SPMM_CPS") ? sh.cps : (k > 96 ? 8 : 4);
+    const int grid = max(1, min(ceil_div(n, sh.tile), kSMs * cps));
     auto v = reinterpret_cast<const double2*>(val);
     auto xx = reinterpret_cast<const double2*>(x);
     auto yy = reinterpret_cast<double2*>(y);
+    static const int vz = [] {  // BK_SPMM_ZV: complex columns per lane for wide k (tuning runs)
+        const char* e = getenv("BK_SPMM_ZV");
+        return e ? atoi(e) : 4;
+    }();
     if (k <= 32)
-        spmm_z_kernel<1><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy);
+        spmm_z_kernel<1><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy, sh.tile);
     else if (k <= 64)
-        spmm_z_kernel<2><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy);
+        spmm_z_kernel<2><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy, sh.tile);
+    else if (k <= 96 || vz == 3)
+        spmm_z_kernel<3><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy, sh.tile);
+    else if (vz == 4)
+        spmm_z_kernel<4><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy, sh.tile);
     else
-        spmm_z_kernel<3><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy);
+        spmm_z_kernel<6><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy, sh.tile);
     BK_LAUNCHED();
 }
