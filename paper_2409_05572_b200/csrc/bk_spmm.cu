@@ -211,6 +211,82 @@ __global__ void __launch_bounds__(256) spmm_d2_kernel(int n, const int32_t* __re
     }
 }
 
+// Half-warp per row, 16-byte X loads (k even, 16-byte aligned rows): two rows
+// per warp in flight, so each lane keeps twice the bytes in flight at the same
+// instruction count (the real kernel is gather-latency bound at k <= 96).
+template <int V2>
+__global__ void __launch_bounds__(256) spmm_d_half_kernel(int n, const int32_t* __restrict__ rp,
+                                                           const int32_t* __restrict__ ci,
+                                                           const double* __restrict__ val,
+                                                           const double* __restrict__ x, int ldx, int k,
+                                                           double* __restrict__ y, int ldy, int tile) {
+    const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+    const int k2 = k >> 1;
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+    const int ldx2 = ldx >> 1, ldy2 = ldy >> 1;
+    double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
+    for (int t0 = blockIdx.x * tile; t0 < n; t0 += gridDim.x * tile)
+        for (int rb = t0 + 2 * warp; rb < min(n, t0 + tile); rb += 2 * nw) {
+            const int row = rb + half;
+            const bool live = row < min(n, t0 + tile);
+            const int s = live ? __ldg(rp + row) : 0, e = live ? __ldg(rp + row + 1) : 0;
+            double2 acc[V2];
+#pragma unroll
+            for (int u = 0; u < V2; ++u) acc[u] = make_double2(0.0, 0.0);
+            for (int pb = s; pb < e; pb += 16) {
+                const int p = pb + hl;
+                int my_c = 0;
+                double my_v = 0.0;
+                if (p < e) {
+                    my_c = __ldg(ci + p);
+                    my_v = __ldg(val + p);
+                }
+                const int cnt = min(16, e - pb);
+                int t = 0;
+                for (; t + 4 <= cnt; t += 4) {
+                    double2 xv[4][V2];
+                    double vv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = __shfl_sync(hmask, my_c, t + q, 16);
+                        vv[q] = __shfl_sync(hmask, my_v, t + q, 16);
+                        const double2* xr = x2 + static_cast<size_t>(c) * ldx2 + hl;
+#pragma unroll
+                        for (int u = 0; u < V2; ++u)
+                            xv[q][u] = hl + 16 * u < k2 ? __ldg(xr + 16 * u) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+#pragma unroll
+                        for (int u = 0; u < V2; ++u) {
+                            acc[u].x = fma(vv[q], xv[q][u].x, acc[u].x);
+                            acc[u].y = fma(vv[q], xv[q][u].y, acc[u].y);
+                        }
+                }
+                for (; t < cnt; ++t) {
+                    const int c = __shfl_sync(hmask, my_c, t, 16);
+                    const double v = __shfl_sync(hmask, my_v, t, 16);
+                    const double2* xr = x2 + static_cast<size_t>(c) * ldx2 + hl;
+#pragma unroll
+                    for (int u = 0; u < V2; ++u)
+                        if (hl + 16 * u < k2) {
+                            const double2 xv = __ldg(xr + 16 * u);
+                            acc[u].x = fma(v, xv.x, acc[u].x);
+                            acc[u].y = fma(v, xv.y, acc[u].y);
+                        }
+                }
+            }
+            if (live) {
+                double2* yr = y2 + static_cast<size_t>(row) * ldy2 + hl;
+#pragma unroll
+                for (int u = 0; u < V2; ++u)
+                    if (hl + 16 * u < k2) yr[16 * u] = acc[u];
+            }
+        }
+}
+
 int spmm_grid(int n) {
     // 8 warps per CTA, one row per warp per grid-stride step; enough CTAs to
     // fill every SM several times over (148 SMs x 8 resident CTAs)
@@ -259,6 +335,21 @@ extern "C" int bk_spmm_d(int n, const int32_t* rp, const int32_t* ci, const doub
     // k = 96 and no better at k = 160)
     const int cps = getenv("BK_SPMM_CPS") ? sh.cps : (k > 96 ? 8 : 4);
     const int tg = max(1, min(ceil_div(n, sh.tile), kSMs * cps));
+    // narrow blocks (k <= 32): half a warp per row with 16-byte loads, two rows per
+    // warp in flight (config 2, k = 26: 0.127 -> 0.082 ms); wider blocks measured
+    // slower that way (BK_SPMM_HALF=1 forces it up to k = 96, tuning runs only)
+    static const bool half_all = getenv("BK_SPMM_HALF") != nullptr;
+    const bool vec16 = (k % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
+                       (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+    if (vec16 && (k <= 32 || (half_all && k <= 96))) {
+        if (k <= 32)
+            spmm_d_half_kernel<1><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
+        else if (k <= 64)
+            spmm_d_half_kernel<2><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
+        else
+            spmm_d_half_kernel<3><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
+        BK_LAUNCHED();
+    }
     if (k <= 32)
         spmm_d_kernel<1><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
     else if (k <= 64)
