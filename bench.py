@@ -155,10 +155,14 @@ def count_launches(solve_once):
 
 
 def ncu_traffic(kernel):
-    """DRAM traffic per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/*_ncu_full.json, tools/ncu_full_summary.py)."""
+    """DRAM traffic per launch of the dominant kernel class from the committed ncu
+    captures (tools/ncu_full_summary.py): the whole-solve per-launch DRAM capture
+    (profiles/*_ncu_dram_all.json, same launches as the class statistics) first,
+    else the steady-state --set full sample (profiles/*_ncu_full.json)."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")), reverse=True):
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_dram_all.json")), reverse=True) + \
+        sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")), reverse=True)
+    for path in paths:
         try:
             with open(path) as f:
                 d = json.load(f)
