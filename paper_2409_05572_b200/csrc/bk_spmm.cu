@@ -7,12 +7,17 @@
 // every row of Y is written exactly once: no atomics, deterministic (fixed
 // column-ascending order per row), one pass over the matrix per call.
 //
-// Mapping: one warp per matrix row (grid-stride).  The warp loads up to 32 of
-// the row's (col, val) pairs with one coalesced load each and broadcasts them
+// Mapping: one warp per matrix row (half a warp with 16-byte loads for k <= 32);
+// rows are dealt in tiles of 64 to the resident CTAs so all SMs sweep the
+// matrix together and the live band of X stays in L2.  The warp loads up to 32
+// of the row's (col, val) pairs with one coalesced load each and broadcasts them
 // by shuffle; lane l accumulates columns l, l+32, ..., so every X-row gather
-// is a coalesced 256-byte transaction per 32 columns.  Accumulators stay in
-// registers (VPL per lane); widths beyond 32*VPL loop over column chunks.
-// HBM-bound: algorithmic bytes = nnz*12 + (n+1)*4 + 2*n*k*8 (real).
+// is a coalesced 256-byte transaction per 32 columns, four nonzeros' gathers in
+// flight per step.  Accumulators stay in registers (VPL per lane); widths
+// beyond 32*VPL loop over column chunks.  Complex: double2 per lane, the same
+// sweep.  HBM-bound: algorithmic bytes = nnz*12 + (n+1)*4 + 2*n*k*8 (real;
+// complex nnz*20 + (n+1)*4 + 2*n*k*16); for wide k and many nonzeros per row
+// the X-row gathers (nnz*k*8) through L1/L2 are the practical bound.
 #include <cstdlib>
 
 #include "bk_common.cuh"
@@ -133,84 +138,6 @@ __global__ void __launch_bounds__(256) spmm_z_kernel(int n, const int32_t* __res
     }
 }
 
-// Vectorised variant for even k and 16-byte aligned X / Y rows: each lane owns
-// pairs of columns (double2), and the (col, val) pairs of up to 8 nonzeros are
-// fetched first so all of a row's X-row gathers are in flight together.
-template <int VPL2>
-__global__ void __launch_bounds__(256) spmm_d2_kernel(int n, const int32_t* __restrict__ rp,
-                                                       const int32_t* __restrict__ ci,
-                                                       const double* __restrict__ val,
-                                                       const double* __restrict__ x, int ldx, int k,
-                                                       double* __restrict__ y, int ldy) {
-    const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    const int k2 = k >> 1;  // column pairs
-    const int ldx2 = ldx >> 1, ldy2 = ldy >> 1;
-    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
-    double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
-    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
-        const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
-        for (int c0 = 0; c0 < k2; c0 += 32 * VPL2) {
-            double2 acc[VPL2];
-#pragma unroll
-            for (int u = 0; u < VPL2; ++u) acc[u] = make_double2(0.0, 0.0);
-            for (int pb = s; pb < e; pb += 32) {
-                const int p = pb + lane;
-                int my_c = 0;
-                double my_v = 0.0;
-                if (p < e) {
-                    my_c = __ldg(ci + p);
-                    my_v = __ldg(val + p);
-                }
-                const int cnt = min(32, e - pb);
-                int t = 0;
-                for (; t + 8 <= cnt; t += 8) {
-                    int cc[8];
-                    double vv[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        cc[q] = __shfl_sync(0xffffffffu, my_c, t + q);
-                        vv[q] = __shfl_sync(0xffffffffu, my_v, t + q);
-                    }
-                    double2 xv[8][VPL2];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-#pragma unroll
-                        for (int u = 0; u < VPL2; ++u) {
-                            const int c = c0 + lane + 32 * u;
-                            xv[q][u] = c < k2 ? __ldg(x2 + static_cast<size_t>(cc[q]) * ldx2 + c) : make_double2(0.0, 0.0);
-                        }
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-#pragma unroll
-                        for (int u = 0; u < VPL2; ++u) {
-                            acc[u].x = fma(vv[q], xv[q][u].x, acc[u].x);
-                            acc[u].y = fma(vv[q], xv[q][u].y, acc[u].y);
-                        }
-                }
-                for (; t < cnt; ++t) {
-                    const int c = __shfl_sync(0xffffffffu, my_c, t);
-                    const double v = __shfl_sync(0xffffffffu, my_v, t);
-#pragma unroll
-                    for (int u = 0; u < VPL2; ++u) {
-                        const int cc2 = c0 + lane + 32 * u;
-                        if (cc2 < k2) {
-                            const double2 xv = __ldg(x2 + static_cast<size_t>(c) * ldx2 + cc2);
-                            acc[u].x = fma(v, xv.x, acc[u].x);
-                            acc[u].y = fma(v, xv.y, acc[u].y);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < VPL2; ++u) {
-                const int c = c0 + lane + 32 * u;
-                if (c < k2) y2[static_cast<size_t>(row) * ldy2 + c] = acc[u];
-            }
-        }
-    }
-}
-
 // Half-warp per row, 16-byte X loads (k even, 16-byte aligned rows): two rows
 // per warp in flight, so each lane keeps twice the bytes in flight at the same
 // instruction count (the real kernel is gather-latency bound at k <= 96).
@@ -287,13 +214,6 @@ __global__ void __launch_bounds__(256) spmm_d_half_kernel(int n, const int32_t* 
         }
 }
 
-int spmm_grid(int n) {
-    // 8 warps per CTA, one row per warp per grid-stride step; enough CTAs to
-    // fill every SM several times over (148 SMs x 8 resident CTAs)
-    const int want = ceil_div(n, 8);
-    return max(1, min(want, kSMs * 16));
-}
-
 // tile rows per CTA step and resident CTAs per SM for spmm_d_kernel
 // (BK_SPMM_TILE / BK_SPMM_CPS override, for tuning runs only)
 struct SpmmShape {
@@ -318,16 +238,6 @@ extern "C" int bk_spmm_d(int n, const int32_t* rp, const int32_t* ci, const doub
                          const double* x, int ldx, int k, double* y, int ldy, void* stream) {
     if (n <= 0 || k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
-    const int grid = spmm_grid(n);
-    const bool vec = (k % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
-                     (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
-    if (vec && k >= 16 && false) {  // measured slower (register pressure); kept for reference
-        if (k <= 64)
-            spmm_d2_kernel<1><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
-        else
-            spmm_d2_kernel<2><<<grid, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy);
-        BK_LAUNCHED();
-    }
     const SpmmShape sh = spmm_shape();
     // wide blocks (k > 96: 4-6 accumulators per lane, fewer resident warps) run
     // with twice the CTAs per SM in the sweep: config 4's k = 160 2.39 -> 1.90 ms
