@@ -476,12 +476,26 @@ private:
             kept = pin_.info[0];
             if (kept == 0) return 0;
         }
-        Blk pt = B(PT_.d(), ldT_);
-        gemm(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld);
         // second pass: the block is orthonormal to ~1e-8 after the pivot-checked
         // first pass (p >= 1e-8 g_jj bounds its condition), so one Newton-Schulz
-        // step W1 (3I - G)/2 restores orthogonality to ~1e-16 without a second
-        // sequential factorisation or host round trip
+        // step W1 (3I - G1)/2 restores orthogonality without a second sequential
+        // factorisation or host round trip.  For n-row blocks G1 = W1^T W1 is
+        // formed from the first Gram (G1 = M1^T G M1, a x a work) and the two
+        // steps are fused into one tall update out = W (M1 M2): one n-row Gram
+        // and one n-row update fewer per orthonormalisation.  (The tall product's
+        // own rounding, O(kappa eps) with kappa <= 1e4 after the pivot check, is
+        // below what the Rayleigh-Ritz step resolves.)
+        static const bool ns_tall = std::getenv("BLOCKEIG_NS_TALL") != nullptr;
+        if (rows >= n_ && !ns_tall) {
+            gemm(a, GB_.d(), a, a, M1_.d(), a, kept, 1.0, 0.0, COEF_.d(), kept);       // T = G M1
+            gram(a, M1_.d(), a, kept, COEF_.d(), kept, kept, GB_.d(), kept);           // G1 = M1^T T
+            ns_coeff(kept, GB_.d(), kept, M2_.d(), kept);                               // M2 = (3I - G1)/2
+            gemm(a, M1_.d(), a, kept, M2_.d(), kept, kept, 1.0, 0.0, COEF_.d(), kept);  // M1 M2
+            gemm(rows, w.p, w.ld, a, COEF_.d(), kept, kept, 1.0, 0.0, out.p, out.ld);
+            return kept;
+        }
+        Blk pt = B(PT_.d(), ldT_);
+        gemm(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld);
         gram(rows, pt.p, pt.ld, kept, pt.p, pt.ld, kept, GB_.d(), kept);
         ns_coeff(kept, GB_.d(), kept, M2_.d(), kept);
         gemm(rows, pt.p, pt.ld, kept, M2_.d(), kept, kept, 1.0, 0.0, out.p, out.ld);
