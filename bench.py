@@ -202,7 +202,7 @@ def run_reference(args, world, rank, dist):
     """--impl reference: the CPU oracle (port of the reference algorithm), all host threads."""
     if rank != 0:
         return
-    w = W.config2("fix", n_ex=96)
+    w = W.config2(args.strategy, n_ex=96, side=args.side)
     threads = os.cpu_count() or 1
     vals = []
     for i in range(args.warmup + args.steps):
@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--strategy", default="fix")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    # lattice side of the workload (64 = BASELINE configs[1]); smaller only for tests
+    ap.add_argument("--side", type=int, default=64)
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
     if args.impl == "reference":
@@ -245,7 +247,7 @@ def main():
     from paper_2409_05572_b200 import load
     torch.cuda.set_device(local)
     L = load()
-    w = W.config2(args.strategy, n_ex=96)
+    w = W.config2(args.strategy, n_ex=96, side=args.side)
     cfg = dict(w.cfg)
     strat = L.strategy_config(w.strategy)
     ext = L.solve_ext(device=local, profile=1)
@@ -278,7 +280,7 @@ def main():
     t_step = reduce_max(dist, float(np.mean(times)))
     launches_per_solve, launch_names = count_launches(solve_once)
     vals = res.values
-    ref = W.lap3d_eigs(64, 64)
+    ref = W.lap3d_eigs(args.side, 64)
     max_rel = float(np.max(np.abs(vals - ref) / ref))
 
     # ---- e2e through the public API from host buffers
