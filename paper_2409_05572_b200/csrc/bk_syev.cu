@@ -1255,6 +1255,10 @@ extern "C" size_t bk_syev_work_bytes(int d) {
 
 extern "C" int bk_syev_d(int d, double* h, int ldh, int n_need, double* values, double* z, int ldz, void* work,
                          int* info, void* stream) {
-    if (d <= kSyevJacobiMaxD) return bk_syev_jacobi_d(d, h, ldh, values, z, ldz, work, info, stream);
+    static const int jmax = [] {  // BK_SYEV_JACOBI_MAX: Jacobi/tridiagonal switch (tuning runs)
+        const char* e = getenv("BK_SYEV_JACOBI_MAX");
+        return e ? atoi(e) : kSyevJacobiMaxD;
+    }();
+    if (d <= jmax) return bk_syev_jacobi_d(d, h, ldh, values, z, ldz, work, info, stream);
     return bk_syev_tri_d(d, h, ldh, n_need, values, z, ldz, work, info, stream);
 }
