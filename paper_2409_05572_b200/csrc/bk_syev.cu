@@ -712,6 +712,54 @@ __global__ void __launch_bounds__(256) backtr_reg_kernel(int d, int n_need, cons
         }
 }
 
+// Variant without shared-memory staging: each warp streams the reflectors
+// from L1/L2 itself (the CTA's warps share them through L1), prefetching
+// reflector k-1 while applying k, so there is no CTA barrier on the chain.
+template <int NPL>
+__global__ void __launch_bounds__(256) backtr_g_kernel(int d, int n_need, const double* __restrict__ vref,
+                                                        const double* __restrict__ tau,
+                                                        const double* __restrict__ u, double* __restrict__ z,
+                                                        int ldz) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int c = blockIdx.x * nwb + wib;
+    if (c >= n_need) return;
+    double x[NPL], vn[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int r = lane + 32 * q;
+        x[q] = r < d ? u[static_cast<size_t>(c) * d + r] : 0.0;
+    }
+    auto load_v = [&](int k, double (&v)[NPL]) {
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int r = lane + 32 * q;
+            v[q] = (k >= 0 && r > k && r < d) ? __ldg(vref + static_cast<size_t>(k) * d + (r - k - 1)) : 0.0;
+        }
+    };
+    load_v(d - 3, vn);
+    double tn = d >= 3 ? __ldg(tau + d - 3) : 0.0;
+    for (int k = d - 3; k >= 0; --k) {
+        double vc[NPL];
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) vc[q] = vn[q];
+        const double t = tn;
+        load_v(k - 1, vn);
+        tn = k > 0 ? __ldg(tau + k - 1) : 0.0;
+        if (t == 0.0) continue;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) s = fma(vc[q], x[q], s);
+        s = warp_sum(s) * t;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) x[q] = fma(-s, vc[q], x[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int r = lane + 32 * q;
+        if (r < d) z[static_cast<size_t>(r) * ldz + c] = x[q];
+    }
+}
+
 // u (column-major d x k) -> row-major scratch, and back
 __global__ void cm_to_rm_small(int d, int k, const double* __restrict__ cm, double* __restrict__ rm, int ldr) {
     const int64_t total = static_cast<int64_t>(d) * k;
@@ -1199,7 +1247,25 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         BK_RET(ab8);
         BK_RET(ab12);
         BK_RET(ab16);
-        if (d <= 128)
+        // streaming variant (no staging barrier): d = 288 syev 1.89 -> 1.79 ms.
+        // BK_BACKTR_STAGED=1 selects the staged kernel, BK_BACKTR_WARPS the warps
+        // (columns) per CTA (tuning runs)
+        static const bool staged = getenv("BK_BACKTR_STAGED") != nullptr;
+        static const int bw = [] {
+            const char* e = getenv("BK_BACKTR_WARPS");
+            return e ? max(1, min(8, atoi(e))) : 2;
+        }();
+        const int gblocks = ceil_div(n_need, bw);
+        if (!staged && d <= 512) {
+            if (d <= 128)
+                backtr_g_kernel<4><<<gblocks, 32 * bw, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+            else if (d <= 256)
+                backtr_g_kernel<8><<<gblocks, 32 * bw, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+            else if (d <= 384)
+                backtr_g_kernel<12><<<gblocks, 32 * bw, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+            else
+                backtr_g_kernel<16><<<gblocks, 32 * bw, 0, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
+        } else if (d <= 128)
             backtr_reg_kernel<4><<<blocks, 256, bs, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
         else if (d <= 256)
             backtr_reg_kernel<8><<<blocks, 256, bs, s>>>(d, n_need, w.vref, w.tau, w.u, z, ldz);
