@@ -14,149 +14,154 @@
 
 namespace bk {
 
+// indexable view of the extern shared array: S[i] stays in the shared window
+struct SmemRef {
+    double* base;
+    __device__ __forceinline__ double& operator[](int i) const { return base[i]; }
+};
+
 // one-CTA launch of the routine below (bk_small.cu); pairs: see above
 int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop, double* m, int ldm, int* info,
                 void* work, cudaStream_t st, bool pairs);
+
+// Shared-memory layout (dyn_s): gd[a] thr2[a] piv[a] slot[a] (ints) | S (a x a, a <= smem_max_a).
+// S holds the Schur complement in its upper triangle and, in its strict lower
+// triangle, the unit-lower elimination matrix E (E G = D L^T), so R^{-1} =
+// E^T D^{-1/2} comes out of the same sweep: no separate triangular inversion
+// (whose per-column warp walks cost half the kernel).  One barrier per pivot;
+// the keep decision of pivot j+1 is taken by thread 0 right after its warp
+// (warp 0, which owns row j+1 alone) has updated S[j+1][j+1], and published
+// through shared memory — the other warps never run the decision logic.
+template <class Ptr>
+__device__ __forceinline__ void chol_drop_core(int a, const double* __restrict__ g, int ldg,
+                                               const double* __restrict__ ref2, double drop,
+                                               double* __restrict__ m, int ldm, int* __restrict__ info, Ptr S,
+                                               double* gd, double* thr2, double* piv, int* slot, bool pairs) {
+    __shared__ int s_keep[2];
+    __shared__ double s_invp[2];
+    __shared__ int s_kept, s_flags;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    for (int e = tid; e < a * a; e += nt) {
+        const int k = e / a, l = e - k * a;
+        S[e] = l >= k ? g[static_cast<size_t>(k) * ldg + l] : 0.0;
+    }
+    const double drop2 = drop * drop;
+    for (int j = tid; j < a; j += nt) {
+        const double d = g[static_cast<size_t>(j) * ldg + j];
+        gd[j] = d;
+        // thr2 < 0: no reference norm (pass 2 of CholQR2); +inf: certain drop
+        double t = -1.0;
+        if (ref2) {
+            const double r = ref2[j], t2 = drop2 * r;
+            t = (r == 0.0 || d < t2) ? INFINITY : t2;
+        }
+        thr2[j] = t;
+    }
+    __syncthreads();
+    constexpr double kLo2 = (1.0 - 1e-4) * (1.0 - 1e-4), kHi2 = (1.0 + 1e-4) * (1.0 + 1e-4);
+    // thread 0's running state: decisions, flags, kept count
+    int kept = 0, flags = 0;  // flags: 1 unsure, 2 bad
+    auto decide = [&](int j, double p) {
+        const double gjj = gd[j], t2 = thr2[j];
+        int keep;
+        if (!isfinite(p) || !isfinite(gjj)) {
+            flags |= 2;
+            keep = 0;
+        } else if (pairs && (j & 1)) {
+            // real embedding of a complex Gram: index 2c+1 is the imaginary twin
+            // of 2c (same pivot in exact arithmetic) and follows its decision
+            keep = slot[j - 1] >= 0 && p > 0.0;
+            if ((slot[j - 1] >= 0) != (p > 0.0)) flags |= 1;
+        } else if (t2 < 0.0) {
+            keep = p > 0.0;
+            if (p <= 1e-8 * gjj) flags |= 1;  // pass 2 of CholQR2: basis lost rank
+        } else if (t2 == INFINITY) {
+            keep = 0;  // certain: the pivot can never exceed the projected norm
+        } else {
+            // squared form of "remaining norm >= drop * original norm"; the
+            // uncertainty band |sqrt(p) - thr| < 1e-4 thr in squared form
+            keep = p >= t2;
+            if (p < 1e-8 * gjj || (p > kLo2 * t2 && p < kHi2 * t2)) flags |= 1;
+        }
+        slot[j] = keep ? kept : -1;
+        piv[j] = p;
+        kept += keep;
+        s_keep[j & 1] = keep;
+        s_invp[j & 1] = keep ? 1.0 / p : 0.0;
+    };
+    if (tid == 0) decide(0, S[0]);
+    __syncthreads();
+    for (int j = 0; j < a; ++j) {
+        const int par = j & 1;
+        if (s_keep[par]) {
+            const double invp = s_invp[par];
+            const int e_len = j + 1;  // E part of a row: l in [0, j]
+            // warp 0: row j+1 alone (its diagonal is the next pivot); other warps: rows j+2..
+            // (a single warp takes every row)
+            const int k_begin = j + 1 + wid;
+            const int k_step = nw == 1 ? 1 : (wid == 0 ? a : nw - 1);
+            for (int k = k_begin; k < a; k += k_step) {
+                const double f = S[j * a + k] * invp;
+                const int up = a - k;  // Schur part: l in [k, a)
+                for (int q = lane; q < up + e_len; q += 32) {
+                    if (q < up) {
+                        const int l = k + q;
+                        S[k * a + l] -= f * S[j * a + l];
+                    } else {
+                        const int l = q - up;
+                        S[k * a + l] = l == j ? -f : S[k * a + l] - f * S[j * a + l];
+                    }
+                }
+            }
+        }
+        if (tid == 0 && j + 1 < a) decide(j + 1, S[(j + 1) * a + j + 1]);
+        __syncthreads();
+    }
+    if (tid == 0) {
+        s_kept = kept;
+        s_flags = flags;
+    }
+    // slot^{-1} (column of M -> original index), reusing gd
+    int* inv = reinterpret_cast<int*>(gd);
+    for (int j = tid; j < a; j += nt)
+        if (slot[j] >= 0) inv[slot[j]] = j;
+    __syncthreads();
+    // M[i][slot[c]] = E[c][i] / sqrt(p_c) for kept i <= c (E[c][c] = 1); zero elsewhere
+    const int nk = s_kept;
+    for (int e = tid; e < a * a; e += nt) {
+        const int i = e / a, col = e - i * a;
+        double v = 0.0;
+        if (col < nk && slot[i] >= 0) {
+            const int c = inv[col];
+            if (i <= c) v = (i == c ? 1.0 : S[c * a + i]) / sqrt(piv[c]);
+        }
+        m[static_cast<size_t>(i) * ldm + col] = v;
+    }
+    if (tid == 0) {
+        info[0] = nk;
+        info[1] = s_flags & 1;
+        info[2] = (s_flags >> 1) & 1;
+    }
+}
 
 __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__ g, int ldg,
                                                const double* __restrict__ ref2, double drop,
                                                double* __restrict__ m, int ldm, int* __restrict__ info,
                                                double* __restrict__ s, int smem_max_a, double* dyn_s,
                                                bool pairs = false) {
-    __shared__ int s_unsure, s_bad;
-    __shared__ double s_recip[2];  // 1 / next pivot, computed by thread 0 during the previous step
-    __shared__ int s_recip_ok[2];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-    // shared layout: gd[a] r2[a] piv[a] slot[a] (ints) | Schur complement s (a <= kCholSmemMaxA)
     double* gd = dyn_s;
-    double* r2 = dyn_s + a;
+    double* thr2 = dyn_s + a;
     double* piv = dyn_s + 2 * a;
     int* slot = reinterpret_cast<int*>(dyn_s + 3 * a);
-    if (a <= smem_max_a) s = dyn_s + 3 * a + (a + 1) / 2;  // working Schur complement in shared memory
-    for (int e = tid; e < a * a; e += nt) s[e] = g[static_cast<size_t>(e / a) * ldg + e % a];
-    for (int j = tid; j < a; j += nt) {
-        gd[j] = g[static_cast<size_t>(j) * ldg + j];
-        r2[j] = ref2 ? ref2[j] : 0.0;
-    }
-    if (tid == 0) {
-        s_unsure = 0;
-        s_bad = 0;
-        s_recip_ok[0] = s_recip_ok[1] = 0;
-    }
-    __syncthreads();
-    const double drop2 = drop * drop;
-    constexpr double kLo2 = (1.0 - 1e-4) * (1.0 - 1e-4), kHi2 = (1.0 + 1e-4) * (1.0 + 1e-4);
-    // right-looking skip-pivot Cholesky with ONE barrier per pivot: every thread
-    // evaluates the (identical) keep decision itself; row j stays unscaled
-    // during the step and R is formed in a final pass.
-    int kept = 0;
-    for (int j = 0; j < a; ++j) {
-        const double p = s[j * a + j];
-        const double gjj = gd[j];
-        int keep;
-        bool unsure = false, bad = false;
-        if (!isfinite(p) || !isfinite(gjj)) {
-            bad = true;
-            keep = 0;
-        } else if (pairs && (j & 1)) {
-            // real embedding of a complex Gram: index 2c+1 is the imaginary twin
-            // of 2c (same pivot in exact arithmetic) and follows its decision
-            keep = slot[j - 1] >= 0 && p > 0.0;
-            unsure = (slot[j - 1] >= 0) != (p > 0.0);
-        } else if (ref2 == nullptr) {
-            keep = p > 0.0;
-            unsure = p <= 1e-8 * gjj;  // pass 2 of CholQR2: basis lost rank
-        } else {
-            // squared form of "remaining norm >= drop * original norm" (no sqrt on
-            // the sequential path); the uncertainty band |sqrt(p) - thr| < 1e-4 thr
-            // becomes p in ((1-1e-4)^2 thr^2, (1+1e-4)^2 thr^2)
-            const double thr2 = drop2 * r2[j];
-            if (r2[j] == 0.0 || gjj < thr2) {
-                keep = 0;  // certain: the pivot can never exceed the projected norm
-            } else {
-                keep = p >= thr2;
-                unsure = p < 1e-8 * gjj || (p > kLo2 * thr2 && p < kHi2 * thr2);
-            }
-        }
-        const int par = j & 1;
-        const double invp = keep ? (s_recip_ok[par] ? s_recip[par] : 1.0 / p) : 0.0;
-        __syncwarp();
-        if (tid == 0) {
-            if (unsure) s_unsure = 1;
-            if (bad) s_bad = 1;
-            slot[j] = keep ? kept : -1;
-            piv[j] = p;
-            s_recip_ok[par ^ 1] = 0;
-        }
-        if (keep) {
-            ++kept;
-            for (int k = j + 1 + wid; k < a; k += nw) {
-                const double rk = s[j * a + k] * invp;
-                for (int l = k + lane; l < a; l += 32) s[k * a + l] -= rk * s[j * a + l];
-                // thread 0 owns the next pivot s[j+1][j+1] (first row of warp 0,
-                // first element of lane 0): its reciprocal, off the other warps' path
-                if (tid == 0 && k == j + 1) {
-                    s_recip[par ^ 1] = 1.0 / s[k * a + k];
-                    s_recip_ok[par ^ 1] = 1;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    // R rows: R[j][l] = s[j][l] / sqrt(p_j), R[j][j] = sqrt(p_j)
-    for (int e = tid; e < a * a; e += nt) {
-        const int j = e / a, l = e % a;
-        if (l < j || slot[j] < 0) continue;
-        const double rj = sqrt(piv[j]);
-        s[e] = l == j ? rj : s[e] / rj;
-    }
-    __syncthreads();
-    // R^{-1} = M (upper triangular over the kept indices), computed row by row
-    // from the bottom: for each kept i (descending, one barrier per row) all
-    // kept c > i in parallel:  M[i][c] = -(sum_{i<l<=c} R[i][l] M[l][c]) / R[i][i].
-    // R lives in the upper triangle of s; M is stored transposed in the strict
-    // lower triangle (M[l][c] at s[c*a + l]) and its diagonal in m's diagonal
-    // slot, so both stay in shared memory.
-    // dropped indices hold no R entries: zero their row of R (upper part) so the
-    // dot products below need no per-element test
-    for (int e = tid; e < a * a; e += nt) {
-        const int j = e / a, l = e % a;
-        if (l > j && (slot[j] < 0 || slot[l] < 0)) s[e] = 0.0;
-    }
-    __syncthreads();
-    // 1/R[i][i] once (piv[] no longer needed)
-    for (int i = tid; i < a; i += nt) piv[i] = slot[i] >= 0 ? 1.0 / s[i * a + i] : 0.0;
-    __syncthreads();
-    // Column c of M depends only on itself: one warp per column walks i
-    // downward (lanes split each dot product), no CTA barrier needed.
-    for (int c = wid; c < a; c += nw) {
-        if (slot[c] < 0) continue;
-        for (int i = c - 1; i >= 0; --i) {
-            if (slot[i] < 0) continue;
-            double acc = 0.0;
-            for (int l = i + 1 + lane; l < c; l += 32) acc = fma(s[i * a + l], s[c * a + l], acc);
-            acc = warp_sum(acc);
-            if (lane == 0) s[c * a + i] = -(acc + s[i * a + c] * piv[c]) * piv[i];  // M[i][c]
-            __syncwarp();
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < a * a; e += nt) {
-        const int j = e / a, c = e % a;  // output row j (original column), column c (slot)
-        m[static_cast<size_t>(j) * ldm + c] = 0.0;
-    }
-    __syncthreads();
-    for (int e = tid; e < a * a; e += nt) {
-        const int i = e / a, c = e % a;  // M[i][c], original indices i <= c
-        if (i > c || slot[i] < 0 || slot[c] < 0) continue;
-        const double val = i == c ? piv[c] : s[c * a + i];
-        m[static_cast<size_t>(i) * ldm + slot[c]] = val;
-    }
-    if (tid == 0) {
-        info[0] = kept;
-        info[1] = s_unsure;
-        info[2] = s_bad;
+    if (a <= smem_max_a) {
+        // the Schur complement in shared memory: the specialised instantiation
+        // keeps every access an LDS/STS (a generic pointer compiles to LD/ST)
+        extern __shared__ double chol_smem[];
+        SmemRef S{chol_smem + 3 * a + (a + 1) / 2};
+        chol_drop_core(a, g, ldg, ref2, drop, m, ldm, info, S, gd, thr2, piv, slot, pairs);
+    } else {
+        chol_drop_core(a, g, ldg, ref2, drop, m, ldm, info, s, gd, thr2, piv, slot, pairs);
     }
 }
 

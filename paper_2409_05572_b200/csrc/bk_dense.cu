@@ -140,6 +140,8 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
 
 // C[i][j] = sum_s work[s][i][j] in split order; with `sym`, entries of the
 // strictly-lower tiles (never computed) are mirrored from the upper ones
+// (tile-level: an element-wise mirror reads the partials with stride b — one
+// 69 x 69 Gram over 293 splits 137 -> 230 us)
 __global__ void gram_reduce(int splits, int a, int b, const double* __restrict__ work, double* __restrict__ c,
                             int ldc, int sym, int tile, const int* __restrict__ run_if) {
     if (run_if && *run_if == 0) return;
@@ -199,7 +201,7 @@ GramPlan gram_plan(int n, int tiles, int a, int b, int cps = 2, int tk = GTK) {
 }
 
 // ------------------------------------------------------------------ update
-template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16>
+template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16, bool V16C>
 __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(int n, const double* __restrict__ x, int ldx, int d,
                                                              const double* __restrict__ cm, int ldc, int k,
                                                              double alpha, double beta, double* __restrict__ y,
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(int n, const double*
     auto load_stage = [&](int kt, int st) {
         const int k0 = kt * TK;
         load_rows<V16>(xs + st * TM * PX, PX, x, ldx, r0, n, k0, d, TM, TK, tid, NT);
-        load_rows<false>(cs + st * TK * PC, PC, cm, ldc, k0, d, c0, k, TK, TN, tid, NT);
+        load_rows<V16C>(cs + st * TK * PC, PC, cm, ldc, k0, d, c0, k, TK, TN, tid, NT);
     };
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
@@ -362,9 +364,12 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
                     // 30.3 / 29.6 / 28.8 / 24.4; 72-wide tiles (24-wide warp tiles) for widths
                     // that fit them better
             const bool na = narrow_tile(a), nb = narrow_tile(b);
-            static const int nv = [] {  // BK_NARROW: warp layout of the 72-wide tiles (tuning runs)
+            // BK_NARROW: warp layout of the 72-wide tiles (tuning runs).  Default 2:
+            // 72 x 72 tiles at 4 CTAs per SM, n = 262144 (tools/dense_probe.py):
+            // 138 x 69 18.8 -> 21.1 TF/s, symmetric 207 14.8 -> 17.9 TF/s
+            static const int nv = [] {
                 const char* e = getenv("BK_NARROW");
-                return e ? atoi(e) : 1;
+                return e ? atoi(e) : 2;
             }();
             if (nv == 0) {
                 if (SYM) {
@@ -380,6 +385,22 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
                     return gram_launch_v<GTK, 3, 2, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
                                                                           run_if);
                 }
+            } else if (nv == 2 || nv == 3) {
+                // 72 x 72 tiles of 3 warps at 4 (nv 2: 8-deep k steps) or 3 (nv 3) CTAs
+                // per SM, so the 4 SM sub-partitions carry equal warp counts
+                if (na && (SYM || nb)) {
+                    if (nv == 2)
+                        return gram_launch_v<8, 3, 1, 4, 4, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                        run_if);
+                    return gram_launch_v<16, 3, 1, 3, 3, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                     run_if);
+                }
+                if (!SYM && nb)
+                    return gram_launch_v<GTK, 4, 1, GST, 2, false, 96, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
+                if (!SYM && na)
+                    return gram_launch_v<GTK, 1, 4, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
+                                                                          run_if);
             } else {  // full-width warp tiles along the 72 side: 27 DMMA per 12 fragment loads
                 if (SYM) {
                     if (na) return gram_launch_v<GTK, 3, 1, GST, 2, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work,
@@ -457,6 +478,123 @@ __global__ void __launch_bounds__(256) xc_kernel(int n, const double* __restrict
         }
     }
 }
+// ------------------------------------------------------------------ short-axis forms
+// Contractions over a short axis (n <= kSmallN: the coefficient-space Grams and
+// lifts of the HL trick and of K5's cluster orthonormalisation, n = d <= 3k) are a
+// few MFLOP: a DMMA tile walks the rows serially on one or two SMs (~27 us for
+// 207 x 69 x 69).  Here 32 x 32 output tiles per CTA, the contraction axis in
+// 32-deep chunks staged through shared memory (the next chunk prefetched into
+// registers while the current one is consumed), each thread 4 outputs summed
+// in a fixed order (deterministic).
+constexpr int kSmallN = 512;
+
+// C[i][j] = sum_r X[r][i] Y[r][j]; sym: tiles below the diagonal skipped, the
+// upper triangle mirrored (exactly symmetric)
+__global__ void __launch_bounds__(256) gram_small_kernel(int n, const double* __restrict__ x, int ldx, int a,
+                                                          const double* __restrict__ y, int ldy, int b,
+                                                          double* __restrict__ c, int ldc, int sym,
+                                                          const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    if (sym && i0 > j0) return;
+    __shared__ double xs[32][33], ys[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const bool xi = i0 + tx < a, yj = j0 + tx < b;
+    double px[4], py[4], acc[4] = {0.0, 0.0, 0.0, 0.0};
+    auto fetch = [&](int r0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = r0 + ty + 8 * q;
+            px[q] = r < n && xi ? x[static_cast<size_t>(r) * ldx + i0 + tx] : 0.0;
+            py[q] = r < n && yj ? y[static_cast<size_t>(r) * ldy + j0 + tx] : 0.0;
+        }
+    };
+    fetch(0);
+    for (int r0 = 0; r0 < n; r0 += 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            xs[ty + 8 * q][tx] = px[q];
+            ys[ty + 8 * q][tx] = py[q];
+        }
+        __syncthreads();
+        if (r0 + 32 < n) fetch(r0 + 32);
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+            const double yv = ys[rr][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(xs[rr][ty + 8 * q], yv, acc[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ty + 8 * q, j = j0 + tx;
+        if (i < a && j < b && (!sym || i <= j)) {
+            c[static_cast<size_t>(i) * ldc + j] = acc[q];
+            if (sym && i != j) c[static_cast<size_t>(j) * ldc + i] = acc[q];
+        }
+    }
+}
+
+// Y[r][j] = alpha sum_q X[r][q] C[q][j] + beta Y[r][j]
+__global__ void __launch_bounds__(256) gemm_small_kernel(int n, const double* __restrict__ x, int ldx, int d,
+                                                          const double* __restrict__ cm, int ldc, int k,
+                                                          double alpha, double beta, double* __restrict__ y,
+                                                          int ldy, const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
+    const int r0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    __shared__ double xs[32][33], cs[32][33];  // xs[q][row], cs[q][col]
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    double px[4], pc[4], acc[4] = {0.0, 0.0, 0.0, 0.0};
+    auto fetch = [&](int q0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int rr = ty + 8 * u;  // X: row r0 + rr, column q0 + tx (coalesced along q)
+            px[u] = r0 + rr < n && q0 + tx < d ? x[static_cast<size_t>(r0 + rr) * ldx + q0 + tx] : 0.0;
+            // C: row q0 + rr, column j0 + tx
+            pc[u] = q0 + rr < d && j0 + tx < k ? cm[static_cast<size_t>(q0 + rr) * ldc + j0 + tx] : 0.0;
+        }
+    };
+    fetch(0);
+    for (int q0 = 0; q0 < d; q0 += 32) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            xs[tx][ty + 8 * u] = px[u];
+            cs[ty + 8 * u][tx] = pc[u];
+        }
+        __syncthreads();
+        if (q0 + 32 < d) fetch(q0 + 32);
+#pragma unroll 8
+        for (int qq = 0; qq < 32; ++qq) {
+            const double cv = cs[qq][tx];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(xs[qq][ty + 8 * u], cv, acc[u]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int r = r0 + ty + 8 * u, j = j0 + tx;
+        if (r < n && j < k) {
+            double* yr = y + static_cast<size_t>(r) * ldy + j;
+            *yr = beta == 0.0 ? alpha * acc[u] : fma(alpha, acc[u], beta * *yr);
+        }
+    }
+}
+
+int gram_small(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc, bool sym,
+               cudaStream_t s, const int* run_if) {
+    gram_small_kernel<<<dim3(ceil_div(b, 32), ceil_div(a, 32)), 256, 0, s>>>(n, x, ldx, a, y, ldy, b, c, ldc,
+                                                                             sym ? 1 : 0, run_if);
+    BK_LAUNCHED();
+}
+
+int gemm_small(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
+               double* y, int ldy, cudaStream_t s, const int* run_if) {
+    gemm_small_kernel<<<dim3(ceil_div(k, 32), ceil_div(n, 32)), 256, 0, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta,
+                                                                             y, ldy, run_if);
+    BK_LAUNCHED();
+}
 }  // namespace
 }  // namespace bk
 
@@ -468,6 +606,7 @@ extern "C" int bk_gram_d(int n, const double* x, int ldx, int a, const double* y
         for (int i = 0; i < a; ++i) BK_RET(cudaMemsetAsync(c + static_cast<size_t>(i) * ldc, 0, sizeof(double) * b, s));
         return 0;
     }
+    if (n <= kSmallN) return gram_small(n, x, ldx, a, y, ldy, b, c, ldc, false, s, nullptr);
     if (b == 1 && n >= 4096) {  // X^T v (work: row blocks x a <= bk_gram_work_bytes(n, a, 1))
         const int nb = max(1, min(ceil_div(n, kGvRows), kGvMaxBlocks));
         auto partial = static_cast<double*>(work);
@@ -483,6 +622,7 @@ extern "C" int bk_gram_sym_d(int n, const double* x, int ldx, const double* y, i
     if (d <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
     if (n <= 0) return bk_gram_d(n, x, ldx, d, y, ldy, d, c, ldc, work, stream);
+    if (n <= kSmallN) return gram_small(n, x, ldx, d, y, ldy, d, c, ldc, true, s, nullptr);
     return gram_launch<true>(n, x, ldx, d, y, ldy, d, c, ldc, work, s);
 }
 
@@ -492,14 +632,20 @@ template <int TM, int TN, int TK, int WM, int WN, int ST>
 int gemm_launch_v(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
                   double* y, int ldy, cudaStream_t s, const int* run_if) {
     constexpr size_t smem = sizeof(double) * ST * (TM * (TK + 4) + TK * (TN + 4));
-    auto k16 = gemm_kernel<TM, TN, TK, WM, WN, ST, true>;
-    auto k8 = gemm_kernel<TM, TN, TK, WM, WN, ST, false>;
+    auto k16 = gemm_kernel<TM, TN, TK, WM, WN, ST, true, false>;
+    auto k16c = gemm_kernel<TM, TN, TK, WM, WN, ST, true, true>;
+    auto k8 = gemm_kernel<TM, TN, TK, WM, WN, ST, false, false>;
     static const cudaError_t a1 = prep(k16, smem);
     static const cudaError_t a2 = prep(k8, smem);
+    static const cudaError_t a3 = prep(k16c, smem);
     BK_RET(a1);
     BK_RET(a2);
+    BK_RET(a3);
     const dim3 grid(ceil_div(n, TM), ceil_div(k, TN));
-    if (aligned16(x, ldx))
+    // 16-byte copies of C too when its view allows them (fewer copy instructions)
+    if (aligned16(x, ldx) && aligned16(c, ldc))
+        k16c<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
+    else if (aligned16(x, ldx))
         k16<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
     else
         k8<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);
@@ -524,8 +670,25 @@ int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc
         case 4:  // 8 warps of 32 x 48 (the round-1 first shape): 27.8 / 27.4 / 26.0 / 22.5
             return gemm_launch_v<128, 96, 16, 4, 2, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
         default:  // 4 warps of 64 x 48: 28.3 / 28.1 / 26.3 / 22.2; 72-wide output tiles when they fit k better
-            if (narrow_tile(k))
+            if (narrow_tile(k)) {
+                // BK_GEMM_NARROW: 72-wide tile shape (tuning runs).  Default: 64-row
+                // tiles at 4 CTAs per SM for short contractions (d <= 144: 138 -> 69
+                // with beta = 1 373 -> 338 us, 69 -> 69 144 -> 130 us), 128-row tiles
+                // otherwise (207 -> 138: 613 vs 618 us)
+                static const int nv_env = [] {
+                    const char* e = getenv("BK_GEMM_NARROW");
+                    return e ? atoi(e) : 0;
+                }();
+                const int nv = nv_env ? nv_env : (d <= 144 ? 4 : 1);
+                if (nv == 2)  // 8-deep k steps, 4 stages: 3 CTAs per SM
+                    return gemm_launch_v<128, 72, 8, 2, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+                if (nv == 3)  // 256-row tiles of 12 warps
+                    return gemm_launch_v<256, 72, 16, 4, 3, 2>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
+                                                               run_if);
+                if (nv == 4)  // 64-row tiles of 3 warps, 8-deep, 4 stages: 4 CTAs per SM
+                    return gemm_launch_v<64, 72, 8, 1, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
                 return gemm_launch_v<128, 72, 16, 2, 3, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+            }
             return gemm_launch_v<UTM, UTN, UTK, UWM, UWN, UST>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
                                                                run_if);
     }
@@ -540,6 +703,7 @@ extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c
         if (beta == 1.0) return 0;
         return bk_axpby_d(n, k, 0.0, y, ldy, beta, y, ldy, stream);
     }
+    if (n <= kSmallN) return gemm_small(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, as_stream(stream), nullptr);
     if (k == 1 && n >= 4096) {  // X c for one column: a GEMV
         xc_kernel<<<max(1, min(ceil_div(n, 8), kSMs * 16)), 256, 0, as_stream(stream)>>>(n, x, ldx, d, c, ldc, alpha,
                                                                                          beta, y, ldy);
@@ -553,11 +717,13 @@ extern "C" int bk_gemm_d(int n, const double* x, int ldx, int d, const double* c
 extern "C" int bk_gram_if_d(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
                             int ldc, void* work, const int* run_if, void* stream) {
     if (a <= 0 || b <= 0 || n <= 0) return 0;
+    if (n <= kSmallN) return gram_small(n, x, ldx, a, y, ldy, b, c, ldc, false, as_stream(stream), run_if);
     return gram_launch<false>(n, x, ldx, a, y, ldy, b, c, ldc, work, as_stream(stream), run_if);
 }
 
 extern "C" int bk_gemm_if_d(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
                             double beta, double* y, int ldy, const int* run_if, void* stream) {
     if (n <= 0 || k <= 0 || d <= 0) return 0;
+    if (n <= kSmallN) return gemm_small(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, as_stream(stream), run_if);
     return gemm_launch(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, as_stream(stream), run_if);
 }

@@ -355,7 +355,11 @@ int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop
     }
     // 1024 threads: the per-pivot rank-1 updates are the work (fewer warps measured
     // 1.3-4x slower at a = 96..288)
-    chol_drop_kernel<<<1, 1024, smem, st>>>(a, g, ldg, ref2, drop, m, ldm, info, s, pairs ? 1 : 0);
+    static const int threads = [] {  // BK_CHOL_THREADS: CTA size (tuning runs only)
+        const char* e = getenv("BK_CHOL_THREADS");
+        return e ? max(32, min(1024, atoi(e) / 32 * 32)) : 1024;
+    }();
+    chol_drop_kernel<<<1, threads, smem, st>>>(a, g, ldg, ref2, drop, m, ldm, info, s, pairs ? 1 : 0);
     BK_LAUNCHED();
 }
 }  // namespace bk

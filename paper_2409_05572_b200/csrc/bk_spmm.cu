@@ -25,12 +25,20 @@
 namespace bk {
 namespace {
 
-template <int VPL>
-__global__ void __launch_bounds__(256) spmm_d_kernel(int n, const int32_t* __restrict__ rp,
+// X-row load; `far` rows (|col - row| beyond the tile's neighbourhood) bypass L1
+// allocation so the near band of the tile stays cached for its other rows
+__device__ __forceinline__ double ldx_na(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+template <int VPL, bool NA = false>
+__global__ void __launch_bounds__(512) spmm_d_kernel(int n, const int32_t* __restrict__ rp,
                                                       const int32_t* __restrict__ ci,
                                                       const double* __restrict__ val,
                                                       const double* __restrict__ x, int ldx, int k,
-                                                      double* __restrict__ y, int ldy, int tile) {
+                                                      double* __restrict__ y, int ldy, int tile, int near_h = 0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     // Rows are dealt out in tiles of `tile` consecutive rows, tile t to CTA
     // t mod grid (grid = resident CTAs), so all SMs sweep the matrix together:
@@ -66,8 +74,15 @@ __global__ void __launch_bounds__(256) spmm_d_kernel(int n, const int32_t* __res
                         const int c = __shfl_sync(0xffffffffu, my_c, t + q);
                         vv[q] = __shfl_sync(0xffffffffu, my_v, t + q);
                         const double* xr = x + static_cast<size_t>(c) * ldx + c0 + lane;
+                        if (NA && abs(c - row) > near_h) {
 #pragma unroll
-                        for (int u = 0; u < VPL; ++u) xv[q][u] = c0 + lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
+                            for (int u = 0; u < VPL; ++u)
+                                xv[q][u] = c0 + lane + 32 * u < k ? ldx_na(xr + 32 * u) : 0.0;
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < VPL; ++u)
+                                xv[q][u] = c0 + lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
+                        }
                     }
 #pragma unroll
                     for (int q = 0; q < G; ++q)
@@ -258,6 +273,36 @@ extern "C" int bk_spmm_d(int n, const int32_t* rp, const int32_t* ci, const doub
             spmm_d_half_kernel<2><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
         else
             spmm_d_half_kernel<3><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
+        BK_LAUNCHED();
+    }
+    // BK_SPMM_L1=<threads>: one CTA per SM of that many threads, L1-preferred carve-out,
+    // far X rows (|col - row| > BK_SPMM_H) loaded without L1 allocation (tuning runs)
+    static const int l1_threads = [] {
+        const char* e = getenv("BK_SPMM_L1");
+        return e ? atoi(e) : 0;
+    }();
+    if (l1_threads > 0 && k <= 96) {
+        static const int near_h = [] {
+            const char* e = getenv("BK_SPMM_H");
+            return e ? atoi(e) : 128;
+        }();
+        static const int cps_l1 = getenv("BK_SPMM_CPS") ? sh.cps : 1;
+        static const cudaError_t c1 = cudaFuncSetAttribute(spmm_d_kernel<1, true>,
+                                                           cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        static const cudaError_t c2 = cudaFuncSetAttribute(spmm_d_kernel<2, true>,
+                                                           cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        static const cudaError_t c3 = cudaFuncSetAttribute(spmm_d_kernel<3, true>,
+                                                           cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        BK_RET(c1);
+        BK_RET(c2);
+        BK_RET(c3);
+        const int g1 = max(1, min(ceil_div(n, sh.tile), kSMs * cps_l1));
+        if (k <= 32)
+            spmm_d_kernel<1, true><<<g1, l1_threads, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile, near_h);
+        else if (k <= 64)
+            spmm_d_kernel<2, true><<<g1, l1_threads, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile, near_h);
+        else
+            spmm_d_kernel<3, true><<<g1, l1_threads, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile, near_h);
         BK_LAUNCHED();
     }
     if (k <= 32)

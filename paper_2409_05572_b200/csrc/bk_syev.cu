@@ -340,6 +340,188 @@ __global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, cons
     }
 }
 
+// Packed single-CTA variant (d <= kPackedMaxD, config 2's shrunk d = 3 x 69 =
+// 207): the lower triangle (d(d+1)/2 doubles, 171 KB at d = 207) stays in one
+// SM's shared memory for the whole reduction, so a step costs CTA barriers
+// (~100 cycles) instead of cluster barriers and DSMEM round trips.  The fused
+// pass reads and writes each trailing lower element once: lane l owns columns
+// j = k+1+l+32m (their v / vp / wp in registers for the step), warp w owns rows
+// i = k+1+w+16r; an element x_ij (j <= i) adds x_ij v_j to row i's sum (lane
+// partials in rowacc[r], reduced once per row at the end of the pass) and, off
+// the diagonal, x_ij v_i to column j's sum (colacc[m], combined over warps in a
+// fixed order) — the symmetric matvec without storing the upper triangle.
+constexpr int kPkThreads = 512, kPkWarps = kPkThreads / 32;
+constexpr int kPkM = 7, kPkR = 14;  // column chunks per lane, rows per warp (<= 16): d - 1 <= 224
+constexpr int kPackedMaxD = 218;    // d(d+1)/2 + 22 d doubles <= 227 KB
+// launched up to d = 160: one SM's issue rate bounds the fused pass, and above
+// ~165 the 8-CTA cluster kernel is faster (tools/syev_probe.py, syev incl.
+// bisection etc.: d = 100 480 vs 522 us, 160 815 vs 818, 207 1160 vs 1076)
+constexpr int kPackedUseMaxD = 160;
+
+inline size_t packed_smem_bytes(int d) {
+    return sizeof(double) * (static_cast<size_t>(d) * (d + 1) / 2 + static_cast<size_t>(6 + kPkWarps) * d);
+}
+
+__global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, const double* __restrict__ h, int ldh,
+                                                                        double* __restrict__ vref,
+                                                                        double* __restrict__ tau,
+                                                                        double* __restrict__ diag,
+                                                                        double* __restrict__ off) {
+    extern __shared__ double sm[];
+    __shared__ double red[kPkWarps];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int nt = kPkThreads, nw = kPkWarps;
+    double* A = sm;  // row i of the lower triangle at A + i(i+1)/2
+    double* v = A + static_cast<size_t>(d) * (d + 1) / 2;
+    double* vp = v + d;
+    double* wp = vp + d;
+    double* col = wp + d;  // column k after the pending update
+    double* rp = col + d;  // row parts of p
+    double* p = rp + d;
+    double* cp = p + d;  // [nw][d] column partials
+    auto rowp = [&](int i) { return A + (static_cast<size_t>(i) * (i + 1) >> 1); };
+    for (int i = wid; i < d; i += nw) {
+        double* r = rowp(i);
+        for (int j = lane; j <= i; j += 32)
+            r[j] = 0.5 * (h[static_cast<size_t>(i) * ldh + j] + h[static_cast<size_t>(j) * ldh + i]);
+    }
+    for (int i = tid; i < d; i += nt) {
+        vp[i] = 0.0;
+        wp[i] = 0.0;
+    }
+    auto block_sum = [&](double x) {  // same butterfly in every thread: bit-identical results
+        x = warp_sum(x);
+        if (lane == 0) red[wid] = x;
+        __syncthreads();
+        const double s = warp_sum(lane < nw ? red[lane] : 0.0);
+        __syncthreads();
+        return s;
+    };
+    __syncthreads();
+    for (int k = 0; k + 2 < d; ++k) {
+        // (1) column k (rows r >= k) with the pending update applied; reflector norm
+        const double vpk = vp[k], wpk = wp[k];
+        double xs = 0.0;
+        for (int r = k + tid; r < d; r += nt) {
+            const double x = rowp(r)[k] - (vp[r] * wpk + wp[r] * vpk);
+            col[r] = x;
+            if (r >= k + 2) xs = fma(x, x, xs);
+        }
+        const double xnorm2 = block_sum(xs);  // barrier inside: col[] visible
+        const double alpha = col[k + 1];
+        double t = 0.0, beta = alpha, scal = 0.0;
+        if (xnorm2 > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+            t = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int r = k + 1 + tid; r < d; r += nt) {
+            const double vr = r == k + 1 ? 1.0 : col[r] * scal;
+            v[r] = vr;
+            vref[static_cast<size_t>(k) * d + (r - k - 1)] = vr;
+        }
+        if (tid == 0) {
+            diag[k] = col[k];
+            off[k] = beta;
+            tau[k] = t;
+        }
+        __syncthreads();
+        // (2) fused pass over the trailing lower triangle (rows, cols >= j0)
+        const int j0 = k + 1;
+        double vj[kPkM], vpj[kPkM], wpj[kPkM], cacc[kPkM];
+#pragma unroll
+        for (int m = 0; m < kPkM; ++m) {
+            const int j = j0 + lane + 32 * m;
+            const bool ok = j < d;
+            vj[m] = ok ? v[j] : 0.0;
+            vpj[m] = ok ? vp[j] : 0.0;
+            wpj[m] = ok ? wp[j] : 0.0;
+            cacc[m] = 0.0;
+        }
+        // loops leave by warp-uniform breaks: the trailing triangle shrinks with k,
+        // and guarded-but-unrolled bodies would be predicated, not skipped
+        double racc[kPkR];
+#pragma unroll
+        for (int r = 0; r < kPkR; ++r) racc[r] = 0.0;
+#pragma unroll
+        for (int r = 0; r < kPkR; ++r) {
+            const int i = j0 + wid + nw * r;
+            if (i >= d) break;
+            double* row = rowp(i);
+            const double vi = v[i], vpi = vp[i], wpi = wp[i];
+            const int mhi = (i - j0) >> 5;  // last chunk holding a j <= i
+#pragma unroll
+            for (int m = 0; m < kPkM; ++m) {
+                if (m > mhi) break;
+                const int j = j0 + lane + 32 * m;
+                if (j <= i) {
+                    const double x = row[j] - (vpi * wpj[m] + wpi * vpj[m]);
+                    row[j] = x;
+                    racc[r] = fma(x, vj[m], racc[r]);
+                    if (j < i) cacc[m] = fma(x, vi, cacc[m]);
+                }
+            }
+        }
+        // the 16 row sums of the warp by one reduce-scatter across the lanes
+        // (16 shuffles instead of 16 warp_sums' 80); lane pair (2q, 2q+1) ends
+        // with row q's sum, the butterfly order fixed (deterministic)
+        {
+            double v8[8], v4[4], v2[2];
+            const bool h1 = lane & 16, h2 = lane & 8, h3 = lane & 4, h4 = lane & 2;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double lo8 = q < kPkR ? racc[q] : 0.0, hi8 = q + 8 < kPkR ? racc[q + 8] : 0.0;
+                v8[q] = (h1 ? hi8 : lo8) + __shfl_xor_sync(0xffffffffu, h1 ? lo8 : hi8, 16);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                v4[q] = (h2 ? v8[q + 4] : v8[q]) + __shfl_xor_sync(0xffffffffu, h2 ? v8[q] : v8[q + 4], 8);
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                v2[q] = (h3 ? v4[q + 2] : v4[q]) + __shfl_xor_sync(0xffffffffu, h3 ? v4[q] : v4[q + 2], 4);
+            double v1 = (h4 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? v2[0] : v2[1], 2);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+            const int r = (h1 ? 8 : 0) + (h2 ? 4 : 0) + (h3 ? 2 : 0) + (h4 ? 1 : 0);
+            const int i = j0 + wid + nw * r;
+            if (!(lane & 1) && i < d) rp[i] = v1;
+        }
+#pragma unroll
+        for (int m = 0; m < kPkM; ++m) {
+            const int j = j0 + lane + 32 * m;
+            if (j < d) cp[wid * d + j] = cacc[m];
+        }
+        __syncthreads();
+        // (3) p = t (row part + column parts, fixed warp order); w = p - (t/2)(p^T v) v
+        double pv = 0.0;
+        for (int j = j0 + tid; j < d; j += nt) {
+            double s = rp[j];
+#pragma unroll
+            for (int w = 0; w < nw; ++w) s += cp[w * d + j];
+            const double pj = t * s;
+            p[j] = pj;
+            pv = fma(pj, v[j], pv);
+        }
+        const double kk = -0.5 * t * block_sum(pv);
+        for (int j = j0 + tid; j < d; j += nt) wp[j] = fma(kk, v[j], p[j]);
+        {  // v becomes the pending vp (pointer swap)
+            double* t2 = vp;
+            vp = v;
+            v = t2;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const int k = d - 2;
+        auto at = [&](int i, int j) { return rowp(i)[j] - (vp[i] * wp[j] + wp[i] * vp[j]); };
+        diag[k] = at(k, k);
+        off[k] = at(k + 1, k);
+        diag[k + 1] = at(k + 1, k + 1);
+        off[k + 1] = 0.0;
+        tau[k] = 0.0;
+        tau[k + 1] = 0.0;
+    }
+}
+
 template <class K>
 cudaError_t prep_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
@@ -466,6 +648,68 @@ __global__ void __launch_bounds__(256) bisect_kernel(int d, const double* __rest
         hi = new_hi;
     }
     if (lane == 0) lam[j] = 0.5 * (lo + hi);
+}
+
+// One CTA of W warps per eigenvalue index j: (32W + 1)-way multisection, so a
+// round shrinks the bracket 257-fold at W = 8 (8 rounds to full precision
+// instead of 12-13 at 33-fold) and the eigenvalues' CTAs fill the SMs' sub-
+// partitions instead of one warp each.  Probe t sits at lo + width (t+1)/(N+1),
+// a formula every thread evaluates identically, so the new bracket needs no
+// exchange of probe values — only the first probe index above j (ballot per
+// warp, minimum over warps).
+template <int W>
+__global__ void __launch_bounds__(32 * W) bisect_multi_kernel(int d, const double* __restrict__ dg,
+                                                              const double* __restrict__ off, int n_need,
+                                                              double* __restrict__ lam) {
+    constexpr int N = 32 * W;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int j = blockIdx.x;
+    extern __shared__ double bsm_t[];
+    __shared__ int s_first[2][W];
+    double* sdg = bsm_t;
+    double* se2 = bsm_t + d;
+    for (int i = tid; i < d; i += N) {
+        sdg[i] = dg[i];
+        se2[i] = i + 1 < d ? off[i] * off[i] : 0.0;
+    }
+    __syncthreads();
+    if (j >= n_need) return;
+    double lo = INFINITY, hi = -INFINITY, emax2 = 0.0;
+    for (int i = lane; i < d; i += 32) {
+        const double r = (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0);
+        lo = fmin(lo, dg[i] - r);
+        hi = fmax(hi, dg[i] + r);
+        if (i + 1 < d) emax2 = fmax(emax2, off[i] * off[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+    }
+    const double tnorm = fmax(fabs(lo), fabs(hi));
+    const double pivmin = DBL_MIN * fmax(1.0, emax2);
+    const double slack = 2.0 * DBL_EPSILON * tnorm + pivmin;
+    lo -= slack;
+    hi += slack;
+    const bool fast4 = tnorm < 0x1p+25;
+    for (int it = 0; it < 40; ++it) {
+        const double width = hi - lo;
+        if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
+        const double x = lo + width * (tid + 1) / static_cast<double>(N + 1);
+        const int c = sturm_count(d, sdg, se2, x, pivmin, fast4);
+        const unsigned above = __ballot_sync(0xffffffffu, c > j);
+        if (lane == 0) s_first[it & 1][wid] = above ? wid * 32 + __ffs(above) - 1 : N;
+        __syncthreads();
+        int first = N;
+#pragma unroll
+        for (int w = 0; w < W; ++w) first = min(first, s_first[it & 1][w]);
+        const double new_lo = first == 0 ? lo : lo + width * first / static_cast<double>(N + 1);
+        const double new_hi = first == N ? hi : lo + width * (first + 1) / static_cast<double>(N + 1);
+        if (new_lo == lo && new_hi == hi) break;
+        lo = new_lo;
+        hi = new_hi;
+    }
+    if (tid == 0) lam[j] = 0.5 * (lo + hi);
 }
 
 // ------------------------------------------------------------------ 3. inverse iteration
@@ -1070,8 +1314,19 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
     const cudaStream_t s = as_stream(stream);
     // latency-bound chains: two warps per CTA so the n_need warps spread over the
     // SMs instead of queueing 8 to an SM (12 SMs busy at n_need = 96 before)
-    bisect_kernel<<<ceil_div(n_need * 32, 64), 64, 2 * sizeof(double) * d, s>>>(d, w.dg, w.off, n_need, values,
-                                                                                 w.e2);
+    // one CTA of 8 warps per eigenvalue (257-way multisection); BK_BISECT_W = 0
+    // selects the warp-per-eigenvalue kernel, 4 a 129-way CTA (tuning runs)
+    static const int bw = [] {
+        const char* e = getenv("BK_BISECT_W");
+        return e ? atoi(e) : 8;
+    }();
+    const size_t bsm = 2 * sizeof(double) * d;
+    if (bw == 4)
+        bisect_multi_kernel<4><<<n_need, 128, bsm, s>>>(d, w.dg, w.off, n_need, values);
+    else if (bw == 8)
+        bisect_multi_kernel<8><<<n_need, 256, bsm, s>>>(d, w.dg, w.off, n_need, values);
+    else
+        bisect_kernel<<<ceil_div(n_need * 32, 64), 64, bsm, s>>>(d, w.dg, w.off, n_need, values, w.e2);
     group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
     {
         const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 2 * (5 * static_cast<size_t>(d) + (d + 7) / 8));
@@ -1195,7 +1450,17 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     const int C = tridiag_cluster_size(d, &csmem);
     bool launched = false;
     static const bool force_coop = getenv("BK_SYEV_COOP") != nullptr;  // tuning runs only
-    if (C > 0 && !force_coop) {
+    static const bool no_packed = getenv("BK_TRI_NO_PACKED") != nullptr;  // tuning runs only
+    if (d <= kPackedUseMaxD && !force_coop && !no_packed) {
+        static const cudaError_t ap = cudaFuncSetAttribute(tridiag_packed_kernel,
+                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            static_cast<int>(packed_smem_bytes(kPackedMaxD)));
+        BK_RET(ap);
+        tridiag_packed_kernel<<<1, kPkThreads, packed_smem_bytes(d), s>>>(d, h, ldh, w.vref, w.tau, w.dg, w.off);
+        BK_RET(cudaGetLastError());
+        launched = true;
+    }
+    if (!launched && C > 0 && !force_coop) {
         static const cudaError_t a1 = cudaFuncSetAttribute(tridiag_cluster_kernel,
                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 8192);
         static const cudaError_t a2 =

@@ -122,7 +122,8 @@ public:
         T2_.alloc(n * ldT_ * es);
         PT_.alloc(n * ldT_ * es);
         VEC_.alloc(n * es);
-        const size_t dc = static_cast<size_t>(dcap_) + tcap_;
+        // coefficient blocks: 64-byte rows (16-byte copies of update coefficients)
+        const size_t dc = static_cast<size_t>(round8(dcap_ + tcap_));
         ldH_ = static_cast<int>(dc);
         H_.alloc(dc * dc * es);
         Z_.alloc(dc * dc * es);

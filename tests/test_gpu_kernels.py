@@ -26,6 +26,7 @@ def bk(product):
     f.bk_gram_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, _D, _D]
     f.bk_gemm_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int, C.c_double, C.c_double, _D,
                             C.c_int, _D]
+    f.bk_gram_sym_d.argtypes = [C.c_int, _D, C.c_int, _D, C.c_int, C.c_int, _D, C.c_int, _D, _D]
     f.bk_syev_work_bytes.restype = C.c_size_t
     f.bk_syev_work_bytes.argtypes = [C.c_int]
     f.bk_syev_d.argtypes = [C.c_int, _D, C.c_int, C.c_int, _D, _D, C.c_int, _D, _D, _D]
@@ -86,7 +87,7 @@ def test_spmm_vs_oracle(bk, oracle, k):
 
 
 @pytest.mark.parametrize("n,a,b", [(1000, 13, 70), (262144, 96, 96), (5000, 288, 288), (77, 1, 1),
-                                   (100000, 95, 1)])
+                                   (100000, 95, 1), (207, 69, 69), (512, 138, 69), (262144, 138, 69)])
 def test_gram_vs_numpy(bk, n, a, b):
     rng = np.random.default_rng(n + a)
     x, y = rng.standard_normal((n, a)), rng.standard_normal((n, b))
@@ -101,7 +102,8 @@ def test_gram_vs_numpy(bk, n, a, b):
 
 
 @pytest.mark.parametrize("n,d,k,beta", [(1000, 40, 40, 0.0), (262144, 288, 96, 0.0), (5000, 96, 7, 1.0), (33, 5, 3, -1.0),
-                                        (100000, 70, 1, 1.0)])
+                                        (100000, 70, 1, 1.0), (207, 207, 138, 0.0), (288, 96, 69, 1.0),
+                                        (262144, 138, 69, 1.0), (262144, 69, 69, 0.0)])
 def test_gemm_vs_numpy(bk, n, d, k, beta):
     rng = np.random.default_rng(d + k)
     x, cm, y0 = rng.standard_normal((n, d)), rng.standard_normal((d, k)), rng.standard_normal((n, k))
@@ -110,6 +112,25 @@ def test_gemm_vs_numpy(bk, n, d, k, beta):
     torch.cuda.synchronize()
     want = -x @ cm + beta * y0
     assert np.abs(yd.cpu().numpy() - want).max() <= 1e-13 * d * np.abs(want).max()
+
+
+@pytest.mark.parametrize("n,d,same", [(207, 69, True), (207, 207, False), (262144, 69, True), (262144, 207, False)])
+def test_gram_sym_vs_numpy(bk, n, d, same):
+    """Symmetric Gram (upper tiles computed, the strict lower triangle mirrored)."""
+    rng = np.random.default_rng(n + d)
+    x = rng.standard_normal((n, d))
+    a = rng.standard_normal((n, n)) if n <= 512 else None
+    y = x if same else ((a + a.T) @ x if a is not None else x * rng.uniform(0.5, 2.0, (n, 1)))
+    xd = dev(x)
+    yd = xd if same else dev(y)
+    c = torch.zeros((d, d), dtype=torch.float64, device="cuda")
+    ws = torch.empty(bk.bk_gram_work_bytes(n, d, d) // 8 + 1, dtype=torch.float64, device="cuda")
+    assert bk.bk_gram_sym_d(n, ptr(xd), d, ptr(yd), d, d, ptr(c), d, ptr(ws), stream()) == 0
+    torch.cuda.synchronize()
+    got, want = c.cpu().numpy(), x.T @ y
+    if n <= 512:  # short-axis kernel: upper triangle computed and mirrored
+        assert np.array_equal(got, got.T)
+    assert np.abs(got - want).max() <= 1e-13 * np.sqrt(n) * np.abs(want).max() + 1e-12
 
 
 def clustered_sym(d, seed, cluster=(3, 0.5)):
@@ -121,7 +142,7 @@ def clustered_sym(d, seed, cluster=(3, 0.5)):
 
 
 @pytest.mark.parametrize("path", ["jacobi", "tri", "dispatch"])
-@pytest.mark.parametrize("d", [2, 5, 40, 97, 288])
+@pytest.mark.parametrize("d", [2, 5, 40, 97, 207, 218, 219, 288])
 def test_syev_vs_reference(bk, oracle, path, d):
     if path == "jacobi" and d > 160:
         pytest.skip("one-CTA Jacobi is used for small d only")

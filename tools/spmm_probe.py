@@ -49,7 +49,8 @@ def main():
     vv = torch.as_tensor(full.data.view(np.float64) if cplx else full.data, device=dev)
     nnz = full.nnz
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    out = {"workload": w.name, "n": w.n, "nnz_full": nnz, "complex": bool(cplx)}
+    out = {"workload": w.name, "n": w.n, "nnz_full": nnz, "complex": bool(cplx),
+           "env": {k: v for k, v in os.environ.items() if k.startswith("BK_")}}
     es = 16 if cplx else 8
     for k in args.k:
         ld = (k + 7) // 8 * 8

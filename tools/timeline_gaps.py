@@ -51,6 +51,21 @@ def main():
                       "idle_ms": (span - busy) / 1e3, "kernels": len(k)}))
     for key, g in gaps.most_common(15):
         print(f"{g / 1e3:9.2f} ms  {count[key]:6d}x  {key}")
+    # one steady-state iteration (between two tridiagonalisations), launch by launch
+    tri = [i for i, e in enumerate(k) if "tridiag" in e["name"]]
+    if len(tri) > 101:
+        for e in k[tri[100]:tri[101] + 1]:
+            a = e.get("args", {})
+            print(f"  {short(e['name'])[-24:]:24s} {str(a.get('grid')):>16s} {str(a.get('block')):>14s} {e['dur']:9.1f} us"
+                  f"  {e['name'].split('(')[0][-60:] if 'kernel<' in e['name'] else ''}")
+    # device time per kernel (CUPTI durations, concurrent-free stream)
+    per = collections.defaultdict(lambda: [0, 0.0])
+    for e in k:
+        per[short(e["name"])][0] += 1
+        per[short(e["name"])][1] += e["dur"]
+    print(f"{'kernel':32s} {'launches':>8s} {'total_ms':>9s} {'avg_us':>8s}")
+    for name, (c, d) in sorted(per.items(), key=lambda x: -x[1][1])[:30]:
+        print(f"{name[-32:]:32s} {c:8d} {d / 1e3:9.2f} {d / c:8.2f}")
 
 
 if __name__ == "__main__":
