@@ -34,6 +34,14 @@ extern "C" {
 /* ---- K1 SpMM: Y = A X  (replaces spmv / spmv_block, proj/src/kernel.cpp:8-33) ---- */
 BK_API int bk_spmm_d(int n, const int32_t* row_ptr, const int32_t* col, const double* val,
                      const double* x, int ldx, int k, double* y, int ldy, void* stream);
+/* Cluster-tiled form (same Y, bit-identical): rows regrouped into tiles of `tile`
+ * graph-local rows (rowid[i]: original row of ordered row i; rp2 / val2: the
+ * full CSR in that order, each row's nonzeros in their original order); code[p]
+ * = column, or -(slot + 1) when the column is row rowid[t*tile + slot] of the
+ * same tile t — those X rows are read from the tile's shared-memory copy. */
+BK_API int bk_spmm_tiled_d(int n, int tile, const int32_t* rp2, const int32_t* code, const double* val2,
+                           const int32_t* rowid, const double* x, int ldx, int k, double* y, int ldy,
+                           void* stream);
 /* complex Hermitian twin: x, y, val interleaved (re, im); ld in complex elements */
 BK_API int bk_spmm_z(int n, const int32_t* row_ptr, const int32_t* col, const double* val,
                      const double* x, int ldx, int k, double* y, int ldy, void* stream);
@@ -86,6 +94,12 @@ BK_API int bk_residual_d(int n, const double* v, int ldv, const double* av, int 
                          const double* lambda, int k, double* r, int ldr, const double* t,
                          double* w, int ldw, int w_from, double* rn2, double* vn2, void* work,
                          void* stream);
+/* ... and the squared column norms of W (columns >= w_from) into wn2 (k - w_from
+ * doubles; nullptr: none) — K4's reference norms without re-reading W */
+BK_API int bk_residual_w_d(int n, const double* v, int ldv, const double* av, int ldav,
+                           const double* lambda, int k, double* r, int ldr, const double* t,
+                           double* w, int ldw, int w_from, double* rn2, double* vn2, double* wn2,
+                           void* work, void* stream);
 
 /* convergence finish (replaces assess_convergence, proj/src/rr.cpp:22-38):
  * per_pair[i] = sqrt(rn2)/(norm_a*sqrt(vn2) + sqrt(vn2)*|lambda|), overall =
@@ -207,6 +221,9 @@ BK_API size_t bk_residual_z_work_bytes(int n, int k);
 BK_API int bk_residual_z(int n, const double* v, int ldv, const double* av, int ldav, const double* lambda,
                          int k, double* r, int ldr, const double* t, double* w, int ldw, int w_from,
                          double* rn2, double* vn2, void* work, void* stream);
+BK_API int bk_residual_w_z(int n, const double* v, int ldv, const double* av, int ldav, const double* lambda,
+                           int k, double* r, int ldr, const double* t, double* w, int ldw, int w_from,
+                           double* rn2, double* vn2, double* wn2, void* work, void* stream);
 BK_API int bk_ns_coeff_z(int a, const double* g, int ldg, double* m, int ldm, void* stream);
 BK_API size_t bk_chol_z_work_bytes(int a);
 BK_API int bk_chol_drop_z(int a, const double* g, int ldg, const double* ref2, double drop, double* m,

@@ -237,24 +237,33 @@ extern "C" int bk_coldot_z(int n, const double* x, int ldx, const double* y, int
 }
 
 extern "C" size_t bk_residual_z_work_bytes(int n, int k) {
-    return align256(bk_residual_work_bytes(n, 2 * k)) + align256(6 * static_cast<size_t>(k > 0 ? k : 1) * sizeof(double));
+    return align256(bk_residual_work_bytes(n, 2 * k)) + align256(8 * static_cast<size_t>(k > 0 ? k : 1) * sizeof(double));
 }
 
-extern "C" int bk_residual_z(int n, const double* v, int ldv, const double* av, int ldav, const double* lambda, int k,
-                             double* r, int ldr, const double* t, double* w, int ldw, int w_from, double* rn2,
-                             double* vn2, void* work, void* stream) {
+extern "C" int bk_residual_w_z(int n, const double* v, int ldv, const double* av, int ldav, const double* lambda,
+                               int k, double* r, int ldr, const double* t, double* w, int ldw, int w_from,
+                               double* rn2, double* vn2, double* wn2, void* work, void* stream) {
     if (k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
     double* lam2 = reinterpret_cast<double*>(static_cast<char*>(work) + align256(bk_residual_work_bytes(n, 2 * k)));
     double* rn2r = lam2 + 2 * k;
     double* vn2r = rn2r + 2 * k;
+    double* wn2r = vn2r + 2 * k;
     dup_kernel<<<ceil_div(k, 256), 256, 0, s>>>(k, lambda, lam2);
-    int rc = bk_residual_d(n, v, 2 * ldv, av, 2 * ldav, lam2, 2 * k, r, 2 * ldr, t, w, 2 * ldw, 2 * w_from, rn2r,
-                           vn2r, work, stream);
+    int rc = bk_residual_w_d(n, v, 2 * ldv, av, 2 * ldav, lam2, 2 * k, r, 2 * ldr, t, w, 2 * ldw, 2 * w_from, rn2r,
+                             vn2r, wn2 ? wn2r : nullptr, work, stream);
     if (rc) return rc;
     pairsum_kernel<<<ceil_div(k, 256), 256, 0, s>>>(k, rn2r, rn2);
     pairsum_kernel<<<ceil_div(k, 256), 256, 0, s>>>(k, vn2r, vn2);
+    if (wn2 && w && k > w_from) pairsum_kernel<<<ceil_div(k - w_from, 256), 256, 0, s>>>(k - w_from, wn2r, wn2);
     BK_LAUNCHED();
+}
+
+extern "C" int bk_residual_z(int n, const double* v, int ldv, const double* av, int ldav, const double* lambda, int k,
+                             double* r, int ldr, const double* t, double* w, int ldw, int w_from, double* rn2,
+                             double* vn2, void* work, void* stream) {
+    return bk_residual_w_z(n, v, ldv, av, ldav, lambda, k, r, ldr, t, w, ldw, w_from, rn2, vn2, nullptr, work,
+                           stream);
 }
 
 extern "C" int bk_ns_coeff_z(int a, const double* g, int ldg, double* m, int ldm, void* stream) {

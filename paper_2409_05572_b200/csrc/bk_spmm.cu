@@ -25,20 +25,12 @@
 namespace bk {
 namespace {
 
-// X-row load; `far` rows (|col - row| beyond the tile's neighbourhood) bypass L1
-// allocation so the near band of the tile stays cached for its other rows
-__device__ __forceinline__ double ldx_na(const double* p) {
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-
-template <int VPL, bool NA = false>
-__global__ void __launch_bounds__(512) spmm_d_kernel(int n, const int32_t* __restrict__ rp,
+template <int VPL>
+__global__ void __launch_bounds__(256) spmm_d_kernel(int n, const int32_t* __restrict__ rp,
                                                       const int32_t* __restrict__ ci,
                                                       const double* __restrict__ val,
                                                       const double* __restrict__ x, int ldx, int k,
-                                                      double* __restrict__ y, int ldy, int tile, int near_h = 0) {
+                                                      double* __restrict__ y, int ldy, int tile) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     // Rows are dealt out in tiles of `tile` consecutive rows, tile t to CTA
     // t mod grid (grid = resident CTAs), so all SMs sweep the matrix together:
@@ -74,28 +66,42 @@ __global__ void __launch_bounds__(512) spmm_d_kernel(int n, const int32_t* __res
                         const int c = __shfl_sync(0xffffffffu, my_c, t + q);
                         vv[q] = __shfl_sync(0xffffffffu, my_v, t + q);
                         const double* xr = x + static_cast<size_t>(c) * ldx + c0 + lane;
-                        if (NA && abs(c - row) > near_h) {
 #pragma unroll
-                            for (int u = 0; u < VPL; ++u)
-                                xv[q][u] = c0 + lane + 32 * u < k ? ldx_na(xr + 32 * u) : 0.0;
-                        } else {
-#pragma unroll
-                            for (int u = 0; u < VPL; ++u)
-                                xv[q][u] = c0 + lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
-                        }
+                        for (int u = 0; u < VPL; ++u) xv[q][u] = c0 + lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
                     }
 #pragma unroll
                     for (int q = 0; q < G; ++q)
 #pragma unroll
                         for (int u = 0; u < VPL; ++u) acc[u] = fma(vv[q], xv[q][u], acc[u]);
                 }
-                for (; t < cnt; ++t) {
-                    const int c = __shfl_sync(0xffffffffu, my_c, t);
-                    const double v = __shfl_sync(0xffffffffu, my_v, t);
-                    const double* xr = x + static_cast<size_t>(c) * ldx + c0 + lane;
+                // tail (< G nonzeros): for narrow blocks all its gathers issued
+                // together too (wide ones: one at a time, registers)
+                if (VPL > 3) {
+                    for (; t < cnt; ++t) {
+                        const int c = __shfl_sync(0xffffffffu, my_c, t);
+                        const double v = __shfl_sync(0xffffffffu, my_v, t);
+                        const double* xr = x + static_cast<size_t>(c) * ldx + c0 + lane;
 #pragma unroll
-                    for (int u = 0; u < VPL; ++u)
-                        if (c0 + lane + 32 * u < k) acc[u] = fma(v, __ldg(xr + 32 * u), acc[u]);
+                        for (int u = 0; u < VPL; ++u)
+                            if (c0 + lane + 32 * u < k) acc[u] = fma(v, __ldg(xr + 32 * u), acc[u]);
+                    }
+                } else if (t < cnt) {
+                    double xv[G][VPL], vv[G];
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const bool live = t + q < cnt;
+                        const int c = __shfl_sync(0xffffffffu, my_c, live ? t + q : t);
+                        vv[q] = __shfl_sync(0xffffffffu, my_v, live ? t + q : t);
+                        const double* xr = x + static_cast<size_t>(c) * ldx + c0 + lane;
+#pragma unroll
+                        for (int u = 0; u < VPL; ++u)
+                            xv[q][u] = live && c0 + lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < G; ++q)
+                        if (t + q < cnt)
+#pragma unroll
+                            for (int u = 0; u < VPL; ++u) acc[u] = fma(vv[q], xv[q][u], acc[u]);
                 }
             }
             double* yr = y + static_cast<size_t>(row) * ldy + c0 + lane;
@@ -207,17 +213,27 @@ __global__ void __launch_bounds__(256) spmm_d_half_kernel(int n, const int32_t* 
                             acc[u].y = fma(vv[q], xv[q][u].y, acc[u].y);
                         }
                 }
-                for (; t < cnt; ++t) {
-                    const int c = __shfl_sync(hmask, my_c, t, 16);
-                    const double v = __shfl_sync(hmask, my_v, t, 16);
-                    const double2* xr = x2 + static_cast<size_t>(c) * ldx2 + hl;
+                if (t < cnt) {  // tail: its gathers issued together
+                    double2 xv[4][V2];
+                    double vv[4];
 #pragma unroll
-                    for (int u = 0; u < V2; ++u)
-                        if (hl + 16 * u < k2) {
-                            const double2 xv = __ldg(xr + 16 * u);
-                            acc[u].x = fma(v, xv.x, acc[u].x);
-                            acc[u].y = fma(v, xv.y, acc[u].y);
-                        }
+                    for (int q = 0; q < 4; ++q) {
+                        const bool lv = t + q < cnt;
+                        const int c = __shfl_sync(hmask, my_c, lv ? t + q : t, 16);
+                        vv[q] = __shfl_sync(hmask, my_v, lv ? t + q : t, 16);
+                        const double2* xr = x2 + static_cast<size_t>(c) * ldx2 + hl;
+#pragma unroll
+                        for (int u = 0; u < V2; ++u)
+                            xv[q][u] = lv && hl + 16 * u < k2 ? __ldg(xr + 16 * u) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (t + q < cnt)
+#pragma unroll
+                            for (int u = 0; u < V2; ++u) {
+                                acc[u].x = fma(vv[q], xv[q][u].x, acc[u].x);
+                                acc[u].y = fma(vv[q], xv[q][u].y, acc[u].y);
+                            }
                 }
             }
             if (live) {
@@ -227,6 +243,105 @@ __global__ void __launch_bounds__(256) spmm_d_half_kernel(int n, const int32_t* 
                     if (hl + 16 * u < k2) yr[16 * u] = acc[u];
             }
         }
+}
+
+// Cluster-tiled SpMM (bk_spmm_tiled_d): the rows are regrouped into tiles of
+// T graph-local rows (host-side BFS clustering, host/matrix.cpp), so most
+// nonzeros of a tile's rows point at rows of the same tile.  A CTA copies the
+// tile's own X rows into shared memory once (cp.async, double-buffered: the
+// next tile's copy overlaps this tile's products) and reads in-tile nonzeros
+// from there; only the rest are gathered from L2/HBM.  Config 2's 7-point
+// stencil: ~5 L2 row-gathers per row with the plain kernel (L1 hit 26 %),
+// ~1 + the boundary fraction here.  Per row the arithmetic and its order are
+// the plain kernel's (nonzeros in their original order), so Y is bit-identical.
+template <int VPL>
+__global__ void __launch_bounds__(256) spmm_d_tile_kernel(int n, int T, int ntiles, const int32_t* __restrict__ rp2,
+                                                           const int32_t* __restrict__ code,
+                                                           const double* __restrict__ val,
+                                                           const int32_t* __restrict__ rowid,
+                                                           const double* __restrict__ x, int ldx, int k, int kp,
+                                                           bool v16, double* __restrict__ y, int ldy) {
+    extern __shared__ __align__(16) double win[];  // 2 x T x kp
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    auto stage = [&](int t, int b) {
+        double* w = win + static_cast<size_t>(b) * T * kp;
+        const int r0 = t * T, nr = min(T, n - r0);
+        if (v16) {
+            const int cpr = kp >> 1;
+            for (int e = tid; e < nr * cpr; e += blockDim.x) {
+                const int sl = e / cpr, c2 = (e - sl * cpr) << 1;
+                const int row = __ldg(rowid + r0 + sl);
+                cp_async16(w + sl * kp + c2, x + static_cast<size_t>(row) * ldx + c2, true);
+            }
+        } else {
+            for (int e = tid; e < nr * k; e += blockDim.x) {
+                const int sl = e / k, c = e - sl * k;
+                const int row = __ldg(rowid + r0 + sl);
+                cp_async8(w + sl * kp + c, x + static_cast<size_t>(row) * ldx + c, true);
+            }
+        }
+        cp_async_commit();
+    };
+    int t = blockIdx.x, b = 0;
+    if (t < ntiles) stage(t, 0);
+    for (; t < ntiles; t += gridDim.x, b ^= 1) {
+        const int tn = t + gridDim.x;
+        if (tn < ntiles) stage(tn, b ^ 1);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* w = win + static_cast<size_t>(b) * T * kp;
+        const int r0 = t * T, nr = min(T, n - r0);
+        for (int sl = warp; sl < nr; sl += nw) {
+            const int i = r0 + sl;
+            const int orow = __ldg(rowid + i);
+            const int s = __ldg(rp2 + i), e = __ldg(rp2 + i + 1);
+            double acc[VPL];
+#pragma unroll
+            for (int u = 0; u < VPL; ++u) acc[u] = 0.0;
+            for (int pb = s; pb < e; pb += 32) {
+                const int p = pb + lane;
+                int my_c = 0;
+                double my_v = 0.0;
+                if (p < e) {
+                    my_c = __ldg(code + p);
+                    my_v = __ldg(val + p);
+                }
+                const int cnt = min(32, e - pb);
+                constexpr int G = 4;
+                for (int q0 = 0; q0 < cnt; q0 += G) {
+                    double xv[G][VPL], vv[G];
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const bool live = q0 + q < cnt;
+                        const int c = __shfl_sync(0xffffffffu, my_c, live ? q0 + q : q0);
+                        vv[q] = __shfl_sync(0xffffffffu, my_v, live ? q0 + q : q0);
+                        if (c < 0) {  // in-tile row: shared memory
+                            const double* xr = w + (-c - 1) * kp + lane;
+#pragma unroll
+                            for (int u = 0; u < VPL; ++u) xv[q][u] = live && lane + 32 * u < k ? xr[32 * u] : 0.0;
+                        } else {
+                            const double* xr = x + static_cast<size_t>(c) * ldx + lane;
+#pragma unroll
+                            for (int u = 0; u < VPL; ++u)
+                                xv[q][u] = live && lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < G; ++q)
+                        if (q0 + q < cnt)
+#pragma unroll
+                            for (int u = 0; u < VPL; ++u) acc[u] = fma(vv[q], xv[q][u], acc[u]);
+                }
+            }
+            double* yr = y + static_cast<size_t>(orow) * ldy + lane;
+#pragma unroll
+            for (int u = 0; u < VPL; ++u)
+                if (lane + 32 * u < k) yr[32 * u] = acc[u];
+        }
+        __syncthreads();  // buffer b is restaged two tiles on
+    }
+    cp_async_wait<0>();
 }
 
 // tile rows per CTA step and resident CTAs per SM for spmm_d_kernel
@@ -275,36 +390,6 @@ extern "C" int bk_spmm_d(int n, const int32_t* rp, const int32_t* ci, const doub
             spmm_d_half_kernel<3><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
         BK_LAUNCHED();
     }
-    // BK_SPMM_L1=<threads>: one CTA per SM of that many threads, L1-preferred carve-out,
-    // far X rows (|col - row| > BK_SPMM_H) loaded without L1 allocation (tuning runs)
-    static const int l1_threads = [] {
-        const char* e = getenv("BK_SPMM_L1");
-        return e ? atoi(e) : 0;
-    }();
-    if (l1_threads > 0 && k <= 96) {
-        static const int near_h = [] {
-            const char* e = getenv("BK_SPMM_H");
-            return e ? atoi(e) : 128;
-        }();
-        static const int cps_l1 = getenv("BK_SPMM_CPS") ? sh.cps : 1;
-        static const cudaError_t c1 = cudaFuncSetAttribute(spmm_d_kernel<1, true>,
-                                                           cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        static const cudaError_t c2 = cudaFuncSetAttribute(spmm_d_kernel<2, true>,
-                                                           cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        static const cudaError_t c3 = cudaFuncSetAttribute(spmm_d_kernel<3, true>,
-                                                           cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        BK_RET(c1);
-        BK_RET(c2);
-        BK_RET(c3);
-        const int g1 = max(1, min(ceil_div(n, sh.tile), kSMs * cps_l1));
-        if (k <= 32)
-            spmm_d_kernel<1, true><<<g1, l1_threads, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile, near_h);
-        else if (k <= 64)
-            spmm_d_kernel<2, true><<<g1, l1_threads, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile, near_h);
-        else
-            spmm_d_kernel<3, true><<<g1, l1_threads, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile, near_h);
-        BK_LAUNCHED();
-    }
     if (k <= 32)
         spmm_d_kernel<1><<<tg, 256, 0, s>>>(n, rp, ci, val, x, ldx, k, y, ldy, sh.tile);
     else if (k <= 64)
@@ -347,4 +432,50 @@ extern "C" int bk_spmm_z(int n, const int32_t* rp, const int32_t* ci, const doub
     else
         spmm_z_kernel<6><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy, sh.tile);
     BK_LAUNCHED();
+}
+
+extern "C" int bk_spmm_tiled_d(int n, int tile, const int32_t* rp2, const int32_t* code, const double* val2,
+                               const int32_t* rowid, const double* x, int ldx, int k, double* y, int ldy,
+                               void* stream) {
+    if (n <= 0 || k <= 0) return 0;
+    if (tile <= 0 || tile > 256) return static_cast<int>(cudaErrorInvalidValue);
+    const cudaStream_t s = as_stream(stream);
+    // widths beyond 96 run as column chunks of <= 96 (the tile copy holds one chunk)
+    for (int c0 = 0; c0 < k; c0 += 96) {
+        const int kc = min(96, k - c0);
+        const double* xc = x + c0;
+        double* yc = y + c0;
+        const bool v16 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(xc) % 16 == 0);
+        // 16-byte copies take an even width; the extra column is inside the row (ld even > k)
+        const int kp = v16 ? (kc + 1) / 2 * 2 : kc;
+        if (v16 && kp > ldx - c0) return static_cast<int>(cudaErrorInvalidValue);
+        const size_t smem = 2 * sizeof(double) * static_cast<size_t>(tile) * kp;
+        const int ntiles = ceil_div(n, tile);
+        static const int cps = [] {  // BK_SPMM_TILED_CPS: CTAs per SM (tuning runs)
+            const char* e = getenv("BK_SPMM_TILED_CPS");
+            return e ? max(1, atoi(e)) : 1;
+        }();
+        const int grid = max(1, min(ntiles, kSMs * cps));
+        if (kc <= 32) {
+            static const cudaError_t a = cudaFuncSetAttribute(spmm_d_tile_kernel<1>,
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            BK_RET(a);
+            spmm_d_tile_kernel<1><<<grid, 256, smem, s>>>(n, tile, ntiles, rp2, code, val2, rowid, xc, ldx, kc, kp,
+                                                          v16, yc, ldy);
+        } else if (kc <= 64) {
+            static const cudaError_t a = cudaFuncSetAttribute(spmm_d_tile_kernel<2>,
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            BK_RET(a);
+            spmm_d_tile_kernel<2><<<grid, 256, smem, s>>>(n, tile, ntiles, rp2, code, val2, rowid, xc, ldx, kc, kp,
+                                                          v16, yc, ldy);
+        } else {
+            static const cudaError_t a = cudaFuncSetAttribute(spmm_d_tile_kernel<3>,
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            BK_RET(a);
+            spmm_d_tile_kernel<3><<<grid, 256, smem, s>>>(n, tile, ntiles, rp2, code, val2, rowid, xc, ldx, kc, kp,
+                                                          v16, yc, ldy);
+        }
+        BK_RET(cudaGetLastError());
+    }
+    return 0;
 }

@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_fused_kernel(int d, const
 // scalars are bit-identical.
 constexpr int kClThreads = 512;
 
-__global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, const double* __restrict__ h, int ldh,
+template <int NT = kClThreads>
+__global__ void __launch_bounds__(NT) tridiag_cluster_kernel(int d, const double* __restrict__ h, int ldh,
                                                                       double* __restrict__ vref,
                                                                       double* __restrict__ tau,
                                                                       double* __restrict__ diag,
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kClThreads) tridiag_cluster_kernel(int d, cons
     const int C = static_cast<int>(cl.num_blocks());
     const int rank = static_cast<int>(cl.block_rank());
     extern __shared__ double sm[];
-    __shared__ double red[kClThreads / 32];
+    __shared__ double red[NT / 32];
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
     const int nloc = (d + C - 1) / C;
     double* A = sm;                       // local rows: A[t*d + j] is row rank + C*t
@@ -1461,15 +1462,25 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         launched = true;
     }
     if (!launched && C > 0 && !force_coop) {
-        static const cudaError_t a1 = cudaFuncSetAttribute(tridiag_cluster_kernel,
-                                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 8192);
-        static const cudaError_t a2 =
-            cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        // CTA size of the cluster kernel: 256 threads (fewer warps repeat the
+        // replicated reflector / reduction work; syev d = 207 1076 -> 1009 us,
+        // d = 288 1563 -> 1508 us); BK_TRI_THREADS = 128 / 512 for tuning runs
+        static const int tthreads = [] {
+            const char* e = getenv("BK_TRI_THREADS");
+            const int v = e ? atoi(e) : 256;
+            return v == 128 || v == 512 ? v : 256;
+        }();
+        auto kern = tthreads == 256   ? tridiag_cluster_kernel<256>
+                    : tthreads == 128 ? tridiag_cluster_kernel<128>
+                                      : tridiag_cluster_kernel<kClThreads>;
+        static const cudaError_t a1 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            200 * 1024 + 8192);
+        static const cudaError_t a2 = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         BK_RET(a1);
         BK_RET(a2);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(C, 1, 1);
-        cfg.blockDim = dim3(kClThreads, 1, 1);
+        cfg.blockDim = dim3(tthreads, 1, 1);
         cfg.dynamicSmemBytes = csmem;
         cfg.stream = s;
         cudaLaunchAttribute attr_c[1];
@@ -1479,7 +1490,7 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
         attr_c[0].val.clusterDim.z = 1;
         cfg.attrs = attr_c;
         cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, d, h, ldh, w.vref, w.tau, w.dg, w.off);
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, d, h, ldh, w.vref, w.tau, w.dg, w.off);
         if (e == cudaSuccess) launched = true;
         else (void)cudaGetLastError();  // cluster not schedulable: fall back below
     }

@@ -62,55 +62,69 @@ __global__ void sum_partials(int nb, int k, const double* __restrict__ partial, 
 }
 
 // R = AV - V diag(lambda); W = t .* R (columns >= w_from); norms of R and V
+// (and, with pw, of W: the reference norms of K4's drop rule, fused here so
+// the preconditioned block is not read again)
 __global__ void __launch_bounds__(256) residual_partial(int n, const double* __restrict__ v, int ldv,
                                                          const double* __restrict__ av, int ldav,
                                                          const double* __restrict__ lambda, int k,
                                                          double* __restrict__ r, int ldr,
                                                          const double* __restrict__ t,
                                                          double* __restrict__ w, int ldw, int w_from,
-                                                         double* __restrict__ pr, double* __restrict__ pv) {
+                                                         double* __restrict__ pr, double* __restrict__ pv,
+                                                         double* __restrict__ pw) {
     __shared__ double red_r[8][33];
     __shared__ double red_v[8][33];
+    __shared__ double red_w[8][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int c = blockIdx.y * 32 + tx;
     const int nb = gridDim.x;
     const int r0 = static_cast<int>((static_cast<int64_t>(n) * blockIdx.x) / nb);
     const int r1 = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.x + 1)) / nb);
-    double ar = 0.0, avv = 0.0;
+    double ar = 0.0, avv = 0.0, aw = 0.0;
     if (c < k) {
         const double lam = lambda[c];
         for (int i = r0 + ty; i < r1; i += 8) {
             const double vv = v[static_cast<size_t>(i) * ldv + c];
             const double rr = av[static_cast<size_t>(i) * ldav + c] - lam * vv;
             if (r) r[static_cast<size_t>(i) * ldr + c] = rr;
-            if (w && c >= w_from) w[static_cast<size_t>(i) * ldw + (c - w_from)] = t ? t[i] * rr : rr;
+            if (w && c >= w_from) {
+                const double ww = t ? t[i] * rr : rr;
+                w[static_cast<size_t>(i) * ldw + (c - w_from)] = ww;
+                aw = fma(ww, ww, aw);
+            }
             ar = fma(rr, rr, ar);
             avv = fma(vv, vv, avv);
         }
     }
     red_r[ty][tx] = ar;
     red_v[ty][tx] = avv;
+    red_w[ty][tx] = aw;
     __syncthreads();
     if (ty == 0 && c < k) {
-        double s = 0.0, sv = 0.0;
+        double s = 0.0, sv = 0.0, sw = 0.0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             s += red_r[i][tx];
             sv += red_v[i][tx];
+            sw += red_w[i][tx];
         }
         pr[static_cast<size_t>(blockIdx.x) * k + c] = s;
         pv[static_cast<size_t>(blockIdx.x) * k + c] = sv;
+        if (pw) pw[static_cast<size_t>(blockIdx.x) * k + c] = sw;
     }
 }
 
 __global__ void residual_finish(int nb, int k, const double* __restrict__ pr, const double* __restrict__ pv,
-                                double* __restrict__ rn2, double* __restrict__ vn2) {
+                                const double* __restrict__ pw, int w_from, double* __restrict__ rn2,
+                                double* __restrict__ vn2, double* __restrict__ wn2) {
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (c >= k) return;
     const double s = warp_colsum(nb, k, pr, c), sv = warp_colsum(nb, k, pv, c);
+    const double sw = pw && c >= w_from ? warp_colsum(nb, k, pw, c) : 0.0;
     if ((threadIdx.x & 31) == 0) {
         rn2[c] = s;
         vn2[c] = sv;
+        if (pw && c >= w_from) wn2[c - w_from] = sw;
     }
 }
 
@@ -355,21 +369,30 @@ extern "C" int bk_colnorm2_d(int n, const double* x, int ldx, int k, double* out
     BK_LAUNCHED();
 }
 
-extern "C" size_t bk_residual_work_bytes(int n, int k) { return 2 * bk_colnorm2_work_bytes(n, k); }
+extern "C" size_t bk_residual_work_bytes(int n, int k) { return 3 * bk_colnorm2_work_bytes(n, k); }
 
-extern "C" int bk_residual_d(int n, const double* v, int ldv, const double* av, int ldav,
-                             const double* lambda, int k, double* r, int ldr, const double* t,
-                             double* w, int ldw, int w_from, double* rn2, double* vn2, void* work,
-                             void* stream) {
+extern "C" int bk_residual_w_d(int n, const double* v, int ldv, const double* av, int ldav,
+                               const double* lambda, int k, double* r, int ldr, const double* t,
+                               double* w, int ldw, int w_from, double* rn2, double* vn2, double* wn2,
+                               void* work, void* stream) {
     if (k <= 0) return 0;
     const cudaStream_t s = as_stream(stream);
     const int nb = row_blocks(n);
     auto pr = static_cast<double*>(work);
     auto pv = pr + static_cast<size_t>(nb) * k;
+    double* pw = w && wn2 ? pv + static_cast<size_t>(nb) * k : nullptr;
     residual_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(
-        n, v, ldv, av, ldav, lambda, k, r, ldr, t, w, ldw, w_from, pr, pv);
-    residual_finish<<<ceil_div(k, 8), 256, 0, s>>>(nb, k, pr, pv, rn2, vn2);
+        n, v, ldv, av, ldav, lambda, k, r, ldr, t, w, ldw, w_from, pr, pv, pw);
+    residual_finish<<<ceil_div(k, 8), 256, 0, s>>>(nb, k, pr, pv, pw, w_from, rn2, vn2, wn2);
     BK_LAUNCHED();
+}
+
+extern "C" int bk_residual_d(int n, const double* v, int ldv, const double* av, int ldav,
+                             const double* lambda, int k, double* r, int ldr, const double* t,
+                             double* w, int ldw, int w_from, double* rn2, double* vn2, void* work,
+                             void* stream) {
+    return bk_residual_w_d(n, v, ldv, av, ldav, lambda, k, r, ldr, t, w, ldw, w_from, rn2, vn2, nullptr, work,
+                           stream);
 }
 
 extern "C" int bk_convergence_d(int k, const double* rn2, const double* vn2, const double* lambda,

@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <thread>
+#include <vector>
 
 #include "host.hpp"
 #include "rng.hpp"
@@ -284,7 +286,10 @@ private:
     void spmm(Blk x, int k, Blk y) {
         if (k <= 0) return;
         auto t = prof_begin();
-        if (cw_ == 1)
+        if (cw_ == 1 && csr_->tile > 0)
+            BKC(bk_spmm_tiled_d(n_, csr_->tile, csr_->rp2.as<int32_t>(), csr_->code.as<int32_t>(), csr_->val2.d(),
+                                csr_->rowid.as<int32_t>(), x.p, x.ld, k, y.p, y.ld, st()));
+        else if (cw_ == 1)
             BKC(bk_spmm_d(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
                           y.ld, st()));
         else
@@ -385,6 +390,24 @@ private:
             }
         }
     };
+    // host-side copy between user memory and a pinned chunk on up to 8 threads
+    // (one thread moves ~8-10 GB/s; the DMA of the other chunk runs meanwhile)
+    static void par_memcpy(void* dst, const void* src, size_t bytes) {
+        static const int nthr = std::max(1, std::min(8, static_cast<int>(std::thread::hardware_concurrency()) / 2));
+        if (bytes < (size_t(4) << 20) || nthr == 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::vector<std::thread> th;
+        const size_t part = (bytes / nthr + 63) & ~size_t(63);
+        for (int t = 1; t < nthr; ++t) {
+            const size_t o = std::min(bytes, part * t), e = std::min(bytes, o + part);
+            if (o < e)
+                th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, e - o); });
+        }
+        std::memcpy(dst, src, std::min(bytes, part));
+        for (auto& x : th) x.join();
+    }
     static PinnedChunks& chunks() {
         static thread_local PinnedChunks* c = new PinnedChunks;
         return *c;
@@ -417,7 +440,7 @@ private:
                 const int b = static_cast<int>((i - 1) & 1);
                 const size_t off = (i - 1) * kChunk, len = std::min(kChunk, count - off);
                 BKC(cudaEventSynchronize(c.ev[b]));
-                std::memcpy(dst + off, c.buf[b], len * sizeof(double));
+                par_memcpy(dst + off, c.buf[b], len * sizeof(double));
             }
         }
     }
@@ -426,7 +449,10 @@ private:
     void upload_colmajor(const double* h, int cols, Blk dst) {
         const size_t bytes = static_cast<size_t>(n_) * cols * sizeof(double) * cw_;
         if (stage_.bytes() < bytes) stage_.alloc(bytes);
-        BKC(cudaMemcpyAsync(stage_.d(), h, bytes, cudaMemcpyHostToDevice, stream_));
+        // pinned double-buffered chunks filled on several host threads (a pageable
+        // cudaMemcpy of config 2's 201 MB X0 ran at ~9 GB/s)
+        chunked_h2d(stage_.d(), bytes / sizeof(double),
+                    [&](double* buf, size_t off, size_t len) { par_memcpy(buf, h + off, len * sizeof(double)); });
         if (cw_ == 1) BKC(bk_cm_to_rm_d(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
         else BKC(bk_cm_to_rm_z(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
         sync();  // the host buffer may be released by the caller
@@ -438,10 +464,12 @@ private:
     // slot >= 0: speculative — no host round trip; the caller proceeds as if all
     // a columns were kept and verifies the Cholesky info at the next record
     // readback (spec_ok), redoing the iteration synchronously if not.
-    int proj_ortho(int rows, Blk w, int a, Blk q, int m, Blk out, int slot = -1) {
+    int proj_ortho(int rows, Blk w, int a, Blk q, int m, Blk out, int slot = -1, const double* pre_ref2 = nullptr) {
         if (a <= 0) return 0;
         double* ref2 = SMALL_.d();  // a doubles
-        colnorm2(rows, w, a, ref2);
+        // column norms of w: precomputed by the kernel that wrote w (residual_kernel), else here
+        if (pre_ref2) BKC(cudaMemcpyAsync(ref2, pre_ref2, a * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+        else colnorm2(rows, w, a, ref2);
         // [0..2] Cholesky info, [3] DGKS flag; speculative calls use their own slot
         int* info = INFO_.as<int>() + (slot >= 0 ? 40 + 4 * slot : 0);
         int* info_host = pin_.info + (slot >= 0 ? 16 + 4 * slot : 0);
@@ -637,15 +665,30 @@ private:
     }
     void restore_residual(Blk v, int k) {
         spmm(v, k, AS());
+        residual_kernel(v, k, VALS_BAK_.d());
+    }
+    // LOBPCG consumes the residual only as W = T R (solvers.cpp:98-107): the
+    // residual kernel writes T R straight into T1 (all n_now columns; the tail
+    // takes T1(:, lock:)), R itself is not stored — one read and one write of an
+    // n x k block fewer per iteration than R, then scale_rows
+    bool fused_w() const { return kind_ == SolverKind::lobpcg; }
+    void residual_kernel(Blk v, int k, const double* lam) {
         double* rn2 = SMALL_.d();
         double* vn2 = SMALL_.d() + dcap_ + tcap_;
+        const bool f = fused_w();
+        double* r = f ? nullptr : R_.d();
+        const double* t = f && TD_.bytes() ? TD_.d() : nullptr;
+        double* w = f ? T1_.d() : nullptr;
+        double* wn2 = f ? w_norms() : nullptr;
         if (cw_ == 1)
-            BKC(bk_residual_d(n_, v.p, v.ld, AS_.d(), ldS_, VALS_BAK_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0,
-                              rn2, vn2, WORK_.p(), st()));
+            BKC(bk_residual_w_d(n_, v.p, v.ld, AS_.d(), ldS_, lam, k, r, ldT_, t, w, ldT_, 0, rn2, vn2, wn2,
+                                WORK_.p(), st()));
         else
-            BKC(bk_residual_z(n_, v.p, v.ld, AS_.d(), ldS_, VALS_BAK_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0,
-                              rn2, vn2, WORK_.p(), st()));
+            BKC(bk_residual_w_z(n_, v.p, v.ld, AS_.d(), ldS_, lam, k, r, ldT_, t, w, ldT_, 0, rn2, vn2, wn2,
+                                WORK_.p(), st()));
     }
+    // squared column norms of W = T R (all n_now columns), written by residual_kernel
+    double* w_norms() { return SMALL_.d() + 4 * (dcap_ + tcap_); }
     Rep residual(Blk v, int k, int n_ev, bool tolerate_nonfinite = false) {
         meter_.w.spmv_cols += k;
         if (debug_) std::fprintf(stderr, "[blockeig] iteration %zu k=%d\n", out_.history.size() + 1, k);
@@ -653,12 +696,7 @@ private:
         double* rn2 = SMALL_.d();
         double* vn2 = SMALL_.d() + dcap_ + tcap_;
         auto tr = prof_begin();
-        if (cw_ == 1)
-            BKC(bk_residual_d(n_, v.p, v.ld, AS_.d(), ldS_, VALS_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0, rn2,
-                              vn2, WORK_.p(), st()));
-        else
-            BKC(bk_residual_z(n_, v.p, v.ld, AS_.d(), ldS_, VALS_.d(), k, R_.d(), ldT_, nullptr, nullptr, 0, 0, rn2,
-                              vn2, WORK_.p(), st()));
+        residual_kernel(v, k, VALS_.d());
         double* rec = SMALL_.d() + 2 * (dcap_ + tcap_);
         BKC(bk_convergence_d(k, rn2, vn2, VALS_.d(), norm_a_, n_ev, cfg_.tol, nullptr, rec, st()));
         prof_end(tr, K_RESID, 24.0 * cw_ * n_ * k, 6.0 * cw_ * n_ * k);
@@ -1069,7 +1107,6 @@ void Engine::solve_lobpcg() {
     int n_now = n_ex, np = 0, prev_lock = 0;
     BlockSizer sizer(strategy_);
     const Blk xd = B(XD_.d(), ldT_);
-    const double* td = TD_.bytes() ? TD_.d() : nullptr;
     const Blk zc = B(ZC_.d(), ldH_), cz = B(CZ_.d(), ldH_), z = B(Z_.d(), ldH_);
     static const bool spec_off = std::getenv("BLOCKEIG_NO_SPEC") != nullptr;
 
@@ -1077,12 +1114,11 @@ void Engine::solve_lobpcg() {
     auto tail = [&](int j, const Rep& rep, int lock, Decision d, bool spec) -> bool {
         Blk s = S(cur_);
         const int active = n_now - lock;
-        // W = T R(:, lock:) orthonormalised against [X, P]
-        scale_rows(n_, active, td, B(R_.d(), ldT_).at(lock), T1());
+        // W = T R(:, lock:) (written by the residual kernel) orthonormalised against [X, P]
         int m = n_now + np;
         meter_.proj_ortho(n_, active, m);
         mark(0);
-        const int kw = proj_ortho(n_, T1(), active, s, m, s.at(m), spec ? 0 : -1);
+        const int kw = proj_ortho(n_, T1().at(lock), active, s, m, s.at(m), spec ? 0 : -1, w_norms() + lock);
         mark(2);
         if (kw == 0) {
             push(j, rep.overall, n_now, Event::none, lock);

@@ -114,6 +114,11 @@ struct DeviceCsr {
     int64_t nnz_full = 0;
     DevMem row_ptr, col, val;
     bool negated = false;
+    // cluster-tiled copy for bk_spmm_tiled_d (tile == 0: not built, the graph has
+    // too little locality); see cluster_rows() in host/matrix.cpp
+    int tile = 0;
+    double in_tile_frac = 0.0;
+    DevMem rp2, code, val2, rowid;
 };
 
 class SparseSym {

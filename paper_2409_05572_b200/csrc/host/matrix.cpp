@@ -236,6 +236,53 @@ double SparseSym::norm_est() const {
     return est;
 }
 
+namespace {
+// Graph-local row order for the cluster-tiled SpMM: rows are grouped into tiles
+// of `tile` rows grown breadth-first over the sparsity graph, each tile seeded
+// from the oldest unplaced row the previous tiles reached (so consecutive tiles
+// are neighbours and their boundary rows stay L2-resident together).  Returns
+// the order (ordered index -> row) and the fraction of nonzeros whose column
+// lies in the row's own tile.
+double cluster_rows(int n, const std::vector<int32_t>& rp, const std::vector<int32_t>& col, int tile,
+                    std::vector<int32_t>& order) {
+    order.clear();
+    order.reserve(n);
+    std::vector<int32_t> tile_of(static_cast<size_t>(n), -1);
+    std::vector<int32_t> frontier;  // global FIFO of reached rows (may repeat)
+    size_t fhead = 0;
+    int next_seed = 0;
+    std::vector<int32_t> q;
+    while (static_cast<int>(order.size()) < n) {
+        const int t = static_cast<int>(order.size()) / tile;
+        const size_t start = order.size();
+        q.clear();
+        size_t qh = 0;
+        auto seed = [&]() {
+            while (fhead < frontier.size() && tile_of[frontier[fhead]] >= 0) ++fhead;
+            if (fhead < frontier.size()) return frontier[fhead++];
+            while (next_seed < n && tile_of[next_seed] >= 0) ++next_seed;
+            return next_seed < n ? next_seed : -1;
+        };
+        while (order.size() - start < static_cast<size_t>(tile)) {
+            while (qh < q.size() && tile_of[q[qh]] >= 0) ++qh;
+            int u;
+            if (qh < q.size()) u = q[qh++];
+            else if ((u = seed()) < 0) break;
+            tile_of[u] = t;
+            order.push_back(u);
+            for (int32_t p = rp[u]; p < rp[u + 1]; ++p)
+                if (tile_of[col[p]] < 0) q.push_back(col[p]);
+        }
+        for (; qh < q.size(); ++qh)
+            if (tile_of[q[qh]] < 0) frontier.push_back(q[qh]);
+    }
+    int64_t in = 0;
+    for (int r = 0; r < n; ++r)
+        for (int32_t p = rp[r]; p < rp[r + 1]; ++p) in += tile_of[col[p]] == tile_of[r];
+    return rp[n] ? static_cast<double>(in) / rp[n] : 0.0;
+}
+}  // namespace
+
 // Expand the lower triangle to full CSR (int32) and upload once per
 // (device, sign); the upper entries are the mirrored (conjugated) lower ones.
 const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
@@ -291,6 +338,44 @@ const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
     if (nnz) {
         cuda_check(cudaMemcpy(e->col.as<void>(), fcol.data(), sizeof(int32_t) * fcol.size(), cudaMemcpyHostToDevice), "upload");
         cuda_check(cudaMemcpy(e->val.as<void>(), fval.data(), sizeof(double) * fval.size(), cudaMemcpyHostToDevice), "upload");
+    }
+    // cluster-tiled copy (real matrices; BLOCKEIG_SPMM_TILE = rows per tile).  Off by
+    // default: measured 3x slower than the plain K1 on config 2 (one 143 KB CTA per
+    // SM holds 8 warps, too few to cover the remaining gathers and the per-row
+    // index loads; the plain kernel keeps 32 warps per SM in flight)
+    static const int tile = [] {
+        const char* v = std::getenv("BLOCKEIG_SPMM_TILE");
+        return v ? std::max(0, std::min(256, std::atoi(v))) : 0;
+    }();
+    if (!complex_ && tile > 0 && n_ >= 8 * tile && nnz) {
+        std::vector<int32_t> order;
+        const double frac = cluster_rows(n_, frp, fcol, tile, order);
+        if (frac >= 0.5) {  // enough locality to pay for the shared-memory copy
+            std::vector<int32_t> pos(static_cast<size_t>(n_));
+            for (int i = 0; i < n_; ++i) pos[order[i]] = i;
+            std::vector<int32_t> rp2(static_cast<size_t>(n_) + 1, 0), code(static_cast<size_t>(nnz));
+            std::vector<double> val2(static_cast<size_t>(nnz));
+            int64_t q = 0;
+            for (int i = 0; i < n_; ++i) {
+                const int r = order[i];
+                for (int32_t p = frp[r]; p < frp[r + 1]; ++p, ++q) {
+                    const int c = fcol[p];
+                    code[q] = pos[c] / tile == i / tile ? -(pos[c] % tile) - 1 : c;
+                    val2[q] = fval[p];
+                }
+                rp2[i + 1] = static_cast<int32_t>(q);
+            }
+            e->tile = tile;
+            e->in_tile_frac = frac;
+            e->rp2.alloc(sizeof(int32_t) * rp2.size());
+            e->code.alloc(sizeof(int32_t) * code.size());
+            e->val2.alloc(sizeof(double) * val2.size());
+            e->rowid.alloc(sizeof(int32_t) * order.size());
+            cuda_check(cudaMemcpy(e->rp2.as<void>(), rp2.data(), sizeof(int32_t) * rp2.size(), cudaMemcpyHostToDevice), "upload");
+            cuda_check(cudaMemcpy(e->code.as<void>(), code.data(), sizeof(int32_t) * code.size(), cudaMemcpyHostToDevice), "upload");
+            cuda_check(cudaMemcpy(e->val2.as<void>(), val2.data(), sizeof(double) * val2.size(), cudaMemcpyHostToDevice), "upload");
+            cuda_check(cudaMemcpy(e->rowid.as<void>(), order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice), "upload");
+        }
     }
     cudaSetDevice(prev);
     dev_->entries.push_back(std::move(e));

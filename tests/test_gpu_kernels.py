@@ -86,6 +86,45 @@ def test_spmm_vs_oracle(bk, oracle, k):
     assert torch.equal(y2[:, :k], yd[:, :k])
 
 
+@pytest.mark.parametrize("k", [7, 40, 69, 96, 138])
+@pytest.mark.parametrize("perm", [False, True])
+def test_spmm_tiled_bit_identical(bk, k, perm):
+    """Cluster-tiled K1 (in-tile X rows from shared memory) == plain K1, bit for bit,
+    for any row order: each row's nonzeros keep their order."""
+    from paper_2409_05572_b200.workloads import grid_laplacian, full_from_lower
+    rp, col, val = grid_laplacian((12, 11, 10))
+    n = 12 * 11 * 10
+    full = full_from_lower(n, rp, col, val)
+    frp, fcol, fval = full.indptr.astype(np.int32), full.indices.astype(np.int32), full.data
+    tile = 64
+    order = np.random.default_rng(k).permutation(n).astype(np.int32) if perm else np.arange(n, dtype=np.int32)
+    pos = np.empty(n, dtype=np.int64)
+    pos[order] = np.arange(n)
+    rp2, code, val2 = [0], [], []
+    for i, r in enumerate(order):
+        for p in range(frp[r], frp[r + 1]):
+            c = fcol[p]
+            code.append(-(pos[c] % tile) - 1 if pos[c] // tile == i // tile else c)
+            val2.append(fval[p])
+        rp2.append(len(code))
+    ld = (k + 7) // 8 * 8 + 8
+    x = torch.randn(n, ld, dtype=torch.float64, device="cuda")
+    y1 = torch.zeros_like(x)
+    y2 = torch.zeros_like(x)
+    f = bk
+    f.bk_spmm_tiled_d.argtypes = [C.c_int, C.c_int] + [_D] * 5 + [C.c_int, C.c_int, _D, C.c_int, _D]
+    t_rp, t_c, t_v = dev(frp), dev(fcol), dev(fval)
+    assert f.bk_spmm_d(n, ptr(t_rp), ptr(t_c), ptr(t_v), ptr(x), ld, k, ptr(y1), ld, stream()) == 0
+    r2 = dev(np.array(rp2, dtype=np.int32))
+    c2 = dev(np.array(code, dtype=np.int32))
+    v2 = dev(np.array(val2))
+    oid = dev(order)
+    assert f.bk_spmm_tiled_d(n, tile, ptr(r2), ptr(c2), ptr(v2), ptr(oid), ptr(x), ld, k, ptr(y2), ld,
+                             stream()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(y1[:, :k], y2[:, :k])
+
+
 @pytest.mark.parametrize("n,a,b", [(1000, 13, 70), (262144, 96, 96), (5000, 288, 288), (77, 1, 1),
                                    (100000, 95, 1), (207, 69, 69), (512, 138, 69), (262144, 138, 69)])
 def test_gram_vs_numpy(bk, n, a, b):
