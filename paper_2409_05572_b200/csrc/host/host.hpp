@@ -136,6 +136,14 @@ public:
     double norm_est() const;                                  // estimate_norm2, cached
     // full (both triangles) CSR on `device`, optionally with negated values (M = -A)
     const DeviceCsr& device_csr(int device, bool negate) const;
+    // full (both triangles) CSR: per row the lower entries then the mirrored
+    // (conjugated) upper ones, columns ascending; built once per handle and
+    // shared by the norm estimate and the device uploads
+    struct FullCsr {
+        std::vector<int32_t> rp, col;
+        std::vector<double> val;  // interleaved when complex
+    };
+    const FullCsr& full_csr() const;
 
 private:
     int n_;
@@ -147,6 +155,9 @@ private:
     struct DevCache {
         std::mutex mu;
         std::vector<std::unique_ptr<DeviceCsr>> entries;
+        std::mutex full_mu;
+        bool full_ready = false;
+        FullCsr full;
     };
     std::shared_ptr<DevCache> dev_;
 };

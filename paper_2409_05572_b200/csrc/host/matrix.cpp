@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <thread>
 #include <vector>
 #include <fstream>
 #include <sstream>
@@ -220,9 +221,34 @@ double SparseSym::norm_est() const {
     if (nrm == 0.0) return 0.0;
     for (auto& x : v) x /= nrm;
     std::vector<double> w, t;
+    // real: the full (both triangles) CSR, each row [lower entries, then the
+    // mirrored upper ones, columns ascending] summed left to right from 0 —
+    // exactly the order in which host_spmv's row scan and scatter build y[r]
+    // (acc over the lower row, then y[r] += v x[r'] for each later row r'), so
+    // the rows can be split over threads and the estimate stays bit-identical
+    const bool par = !complex_ && n_ >= 65536;
+    const FullCsr* full = par ? &full_csr() : nullptr;
+    auto spmv = [&](const std::vector<double>& x, std::vector<double>& y) {
+        if (!par) return host_spmv(*this, x, y);
+        y.resize(x.size());
+        const int nthr = std::max(1, std::min(8, static_cast<int>(std::thread::hardware_concurrency())));
+        auto rows = [&](int r0, int r1) {
+            for (int r = r0; r < r1; ++r) {
+                double acc = 0.0;
+                for (int32_t p = full->rp[r]; p < full->rp[r + 1]; ++p) acc += full->val[p] * x[full->col[p]];
+                y[r] = acc;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int i = 1; i < nthr; ++i)
+            th.emplace_back(rows, static_cast<int>(static_cast<int64_t>(n_) * i / nthr),
+                            static_cast<int>(static_cast<int64_t>(n_) * (i + 1) / nthr));
+        rows(0, static_cast<int>(static_cast<int64_t>(n_) / nthr));
+        for (auto& x2 : th) x2.join();
+    };
     for (int it = 0; it < 30; ++it) {
-        host_spmv(*this, v, t);
-        host_spmv(*this, t, w);
+        spmv(v, t);
+        spmv(t, w);
         nrm = host_nrm2(w, complex_);
         if (nrm == 0.0) {
             norm_cache_->store(0.0, std::memory_order_relaxed);
@@ -230,7 +256,7 @@ double SparseSym::norm_est() const {
         }
         for (size_t i = 0; i < v.size(); ++i) v[i] = w[i] / nrm;
     }
-    host_spmv(*this, v, t);
+    spmv(v, t);
     const double est = host_nrm2(t, complex_);
     norm_cache_->store(est, std::memory_order_relaxed);
     return est;
@@ -285,10 +311,13 @@ double cluster_rows(int n, const std::vector<int32_t>& rp, const std::vector<int
 
 // Expand the lower triangle to full CSR (int32) and upload once per
 // (device, sign); the upper entries are the mirrored (conjugated) lower ones.
-const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
-    std::lock_guard<std::mutex> lk(dev_->mu);
-    for (auto& e : dev_->entries)
-        if (e->device == device && e->negated == negate) return *e;
+const SparseSym::FullCsr& SparseSym::full_csr() const {
+    std::lock_guard<std::mutex> lk(dev_->full_mu);
+    if (dev_->full_ready) return dev_->full;
+    auto& frp = dev_->full.rp;
+    auto& fcol = dev_->full.col;
+    auto& fval = dev_->full.val;
+    const double sgn = 1.0;
     const int per = complex_ ? 2 : 1;
     std::vector<int32_t> cnt(static_cast<size_t>(n_) + 1, 0);
     for (int r = 0; r < n_; ++r)
@@ -298,10 +327,10 @@ const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
         }
     for (int r = 0; r < n_; ++r) cnt[r + 1] += cnt[r];
     const int64_t nnz = cnt[n_];
-    std::vector<int32_t> frp(cnt), fcol(static_cast<size_t>(nnz));
-    std::vector<double> fval(static_cast<size_t>(nnz) * per);
+    frp = cnt;
+    fcol.assign(static_cast<size_t>(nnz), 0);
+    fval.assign(static_cast<size_t>(nnz) * per, 0.0);
     std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
-    const double sgn = negate ? -1.0 : 1.0;
     // rows in order: upper-part entries (c > r) come from later rows' lower
     // entries, so fill by scanning rows and appending both mirror images;
     // columns end up sorted because both scans are in increasing order.
@@ -323,6 +352,24 @@ const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
             ++q;
         }
     }
+    dev_->full_ready = true;
+    return dev_->full;
+}
+
+const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
+    std::lock_guard<std::mutex> lk(dev_->mu);
+    for (auto& e : dev_->entries)
+        if (e->device == device && e->negated == negate) return *e;
+    const FullCsr& full = full_csr();
+    const std::vector<int32_t>& frp = full.rp;
+    const std::vector<int32_t>& fcol = full.col;
+    std::vector<double> neg;
+    if (negate) {  // M = -A (largest eigenpairs)
+        neg.resize(full.val.size());
+        for (size_t i = 0; i < neg.size(); ++i) neg[i] = -full.val[i];
+    }
+    const std::vector<double>& fval = negate ? neg : full.val;
+    const int64_t nnz = frp[n_];
     auto e = std::make_unique<DeviceCsr>();
     e->device = device;
     e->n = n_;

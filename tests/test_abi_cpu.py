@@ -132,3 +132,15 @@ def test_theory_checks_out_of_scope(prod):
     assert prod.lib.beig_theory_example3x3(None) == B.ERR_INVALID
     assert prod.lib.beig_theory_example3x3(C.byref(ex)) == B.ERR_INVALID
     assert "scope" in prod.last_error()
+
+
+@pytest.mark.parametrize("side", [64, 41])
+def test_threaded_norm_estimate_bit_identical(prod, oracle, side):
+    """The product's host norm estimate splits the full-CSR rows over threads for
+    n >= 65536; each row is summed in the reference scatter order, so the value is
+    bit-identical to the oracle's serial estimate_norm2 (kernel.cpp:174-196)."""
+    from paper_2409_05572_b200.workloads import grid_laplacian
+    rp, col, val = grid_laplacian((side, side, side))
+    n = side ** 3
+    val = val * (1.0 + 0.1 * np.sin(np.arange(val.size)))  # break the stencil's symmetry of values
+    assert prod.from_csr(n, rp, col, val).norm_est() == oracle.from_csr(n, rp, col, val).norm_est()
