@@ -523,6 +523,163 @@ __global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, co
     }
 }
 
+// One-barrier cluster variant: the reflector of step k+1 needs column k+1,
+// which by symmetry is row k+1 — owned by one rank, and final for step k+1 as
+// soon as step k's fused pass has updated it.  So that pass also broadcasts the
+// stored row k+1 (DSMEM, double-buffered by step parity) next to the p slices,
+// and after the one cluster barrier every rank applies the pending rank-2 update
+// to it locally and forms the reflector redundantly: one cluster barrier per
+// step instead of two (the column scatter and its barrier are gone).  Column k
+// is read from the stored row k instead of the stored column (equal up to the
+// rounding of the contracted rank-2 update), otherwise the arithmetic is the
+// two-barrier kernel's.
+template <int NT>
+__global__ void __launch_bounds__(NT) tridiag_cluster1_kernel(int d, const double* __restrict__ h, int ldh,
+                                                              double* __restrict__ vref, double* __restrict__ tau,
+                                                              double* __restrict__ diag, double* __restrict__ off) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = static_cast<int>(cl.num_blocks());
+    const int rank = static_cast<int>(cl.block_rank());
+    extern __shared__ double sm[];
+    __shared__ double red[NT / 32];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    const int nloc = (d + C - 1) / C;
+    double* A = sm;  // local rows: A[t*d + j] is row rank + C*t
+    double* v = A + static_cast<size_t>(nloc) * d;
+    double* vp = v + d;
+    double* wp = vp + d;
+    double* col = wp + d;
+    double* pb[2] = {col + d, col + 2 * d};     // p slices, by step parity
+    double* rb[2] = {col + 3 * d, col + 4 * d};  // broadcast stored row k, by step parity
+    for (int e = tid; e < nloc * d; e += nt) {
+        const int t = e / d, j = e - t * d;
+        const int i = rank + C * t;
+        if (i < d) A[e] = 0.5 * (h[static_cast<size_t>(i) * ldh + j] + h[static_cast<size_t>(j) * ldh + i]);
+    }
+    for (int i = tid; i < d; i += nt) {
+        vp[i] = 0.0;
+        wp[i] = 0.0;
+    }
+    auto block_sum = [&](double x) {
+        x = warp_sum(x);
+        if (lane == 0) red[wid] = x;
+        __syncthreads();
+        const double s = warp_sum(lane < nw ? red[lane] : 0.0);
+        __syncthreads();
+        return s;
+    };
+    cl.sync();  // every rank's rows are loaded before row 0 is read remotely
+    if (rank == 0)  // row 0 (rank 0's local row 0), symmetrised above, to every rank
+        for (int j = tid; j < d; j += nt) {
+            const double x = A[j];
+            for (int q = 0; q < C; ++q) cl.map_shared_rank(rb[0], q)[j] = x;
+        }
+    cl.sync();
+    for (int k = 0; k + 2 < d; ++k) {
+        // (1) column k = stored row k with the pending update applied (replicated)
+        const double* rk = rb[k & 1];
+        const double vpk = vp[k], wpk = wp[k];
+        double xs = 0.0;
+        for (int r = k + tid; r < d; r += nt) {
+            const double x = rk[r] - (vp[r] * wpk + wp[r] * vpk);
+            col[r] = x;
+            if (r >= k + 2) xs = fma(x, x, xs);
+        }
+        const double xnorm2 = block_sum(xs);
+        const double alpha = col[k + 1];
+        double t = 0.0, beta = alpha, scal = 0.0;
+        if (xnorm2 > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+            t = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int r = k + 1 + tid; r < d; r += nt) {
+            const double vr = r == k + 1 ? 1.0 : col[r] * scal;
+            v[r] = vr;
+            if (rank == 0) vref[static_cast<size_t>(k) * d + (r - k - 1)] = vr;
+        }
+        if (rank == 0 && tid == 0) {
+            diag[k] = col[k];
+            off[k] = beta;
+            tau[k] = t;
+        }
+        __syncthreads();
+        // (2) fused pending update + p = t A22 v on local rows i >= k+1; the
+        // owner of row k+1 also broadcasts it (its stored values for step k+1)
+        double* p = pb[k & 1];
+        double* rn = rb[(k + 1) & 1];
+        const int t1 = k + 1 <= rank ? 0 : (k + 1 - rank + C - 1) / C;
+        for (int tb = t1 + 4 * wid; tb < nloc; tb += 4 * nw) {
+            int ii[4];
+            double* rows[4];
+            double vpi[4], wpi[4], sacc[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int tt = tb + q;
+                ii[q] = rank + C * tt;
+                const bool ok = tt < nloc && ii[q] < d;
+                rows[q] = ok ? A + static_cast<size_t>(tt) * d : nullptr;
+                vpi[q] = ok ? vp[ii[q]] : 0.0;
+                wpi[q] = ok ? wp[ii[q]] : 0.0;
+                sacc[q] = 0.0;
+            }
+            const int bq = ii[0] == k + 1 ? 0 : -1;  // row k+1 is the first local row it can be
+            for (int j = k + 1 + lane; j < d; j += 32) {
+                const double vj = v[j], vpj = vp[j], wpj = wp[j];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (rows[q]) {
+                        const double x = rows[q][j] - (vpi[q] * wpj + wpi[q] * vpj);
+                        rows[q][j] = x;
+                        sacc[q] = fma(x, vj, sacc[q]);
+                        if (q == bq)
+                            for (int r = 0; r < C; ++r) cl.map_shared_rank(rn, r)[j] = x;
+                    }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sacc[q] = warp_sum(sacc[q]) * t;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (rows[q] && lane < C) cl.map_shared_rank(p, lane)[ii[q]] = sacc[q];
+        }
+        cl.sync();
+        // (3) w = p - (t/2)(p^T v) v becomes the pending update (replicated)
+        double pv = 0.0;
+        for (int i = k + 1 + tid; i < d; i += nt) pv = fma(p[i], v[i], pv);
+        const double kk = -0.5 * t * block_sum(pv);
+        for (int i = k + 1 + tid; i < d; i += nt) wp[i] = fma(kk, v[i], p[i]);
+        {
+            double* t2 = vp;
+            vp = v;
+            v = t2;
+        }
+        __syncthreads();
+    }
+    // last 2 x 2 block: owners of rows d-2, d-1 publish their entries to rank 0
+    if (d >= 2) {
+        const int k = d - 2;
+        for (int r = k + tid; r < d; r += nt) {
+            if (r % C != rank) continue;
+            const int t = r / C;
+            const double* row = A + static_cast<size_t>(t) * d;
+            double* c0 = cl.map_shared_rank(col, 0);
+            c0[r] = row[k] - (vp[r] * wp[k] + wp[r] * vp[k]);
+            if (r == d - 1) c0[d] = row[d - 1] - (vp[r] * wp[d - 1] + wp[r] * vp[d - 1]);
+        }
+    }
+    cl.sync();
+    if (rank == 0 && tid == 0) {
+        const int k = d - 2;
+        diag[k] = col[k];
+        off[k] = col[k + 1];
+        diag[k + 1] = col[d];
+        off[k + 1] = 0.0;
+        tau[k] = 0.0;
+        tau[k + 1] = 0.0;
+    }
+}
+
 template <class K>
 cudaError_t prep_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
@@ -539,7 +696,8 @@ int tridiag_cluster_size(int d, size_t* smem) {
     }();
     for (int c = c0; c <= 16; c *= 2) {
         const size_t nloc = static_cast<size_t>((d + c - 1) / c);
-        const size_t bytes = sizeof(double) * (nloc * d + 5 * static_cast<size_t>(d) + 8);
+        // + 3 d: the one-barrier kernel's second p buffer and two row buffers
+        const size_t bytes = sizeof(double) * (nloc * d + 8 * static_cast<size_t>(d) + 8);
         if (bytes <= 200 * 1024) {
             *smem = bytes;
             return c;
@@ -1470,9 +1628,14 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
             const int v = e ? atoi(e) : 256;
             return v == 128 || v == 512 ? v : 256;
         }();
-        auto kern = tthreads == 256   ? tridiag_cluster_kernel<256>
-                    : tthreads == 128 ? tridiag_cluster_kernel<128>
-                                      : tridiag_cluster_kernel<kClThreads>;
+        // one cluster barrier per step (BK_TRI_2BAR: the two-barrier kernel, tuning runs)
+        static const bool two_bar = getenv("BK_TRI_2BAR") != nullptr;
+        auto kern = two_bar ? (tthreads == 256   ? tridiag_cluster_kernel<256>
+                               : tthreads == 128 ? tridiag_cluster_kernel<128>
+                                                 : tridiag_cluster_kernel<kClThreads>)
+                            : (tthreads == 256   ? tridiag_cluster1_kernel<256>
+                               : tthreads == 128 ? tridiag_cluster1_kernel<128>
+                                                 : tridiag_cluster1_kernel<kClThreads>);
         static const cudaError_t a1 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                             200 * 1024 + 8192);
         static const cudaError_t a2 = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
