@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
     const int r_begin = split * rows_per_split;
     const int r_end = min(n, r_begin + rows_per_split);
     const int wm = (warp / WN) * (TM / WM), wn = (warp % WN) * (TN / WN);
+    // X^T X on a diagonal tile of the symmetric Gram (CholQR's W^T W): the Y
+    // tile is the X tile — staged once, read through both fragment paths
+    const bool same = SYM && ti == tj && x == y && ldx == ldy;
 
     double acc[FM][FN][2];
 #pragma unroll
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
     auto load_stage = [&](int kt, int st) {
         const int r0 = r_begin + kt * TK;
         load_rows<V16>(xs + st * TK * PX, PX, x, ldx, r0, r_end, i0, a, TK, TM, tid, NT);
-        load_rows<V16>(ys + st * TK * PY, PY, y, ldy, r0, r_end, j0, b, TK, TN, tid, NT);
+        if (!same) load_rows<V16>(ys + st * TK * PY, PY, y, ldy, r0, r_end, j0, b, TK, TN, tid, NT);
     };
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
         if (nxt < nk) load_stage(nxt, nxt % STAGES);
         cp_async_commit();
         const double* xd = xs + (kt % STAGES) * TK * PX;
-        const double* yd = ys + (kt % STAGES) * TK * PY;
+        const double* yd = same ? xd : ys + (kt % STAGES) * TK * PY;
 #pragma unroll
         for (int k4 = 0; k4 < TK; k4 += 4) {
             double af[FM], bf[FN];
@@ -138,21 +141,41 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
         }
 }
 
-// C[i][j] = sum_s work[s][i][j] in split order; with `sym`, entries of the
+// C[i][j] = sum_s work[s][i][j] in a fixed order; with `sym`, entries of the
 // strictly-lower tiles (never computed) are mirrored from the upper ones
 // (tile-level: an element-wise mirror reads the partials with stride b — one
 // 69 x 69 Gram over 293 splits 137 -> 230 us)
-__global__ void gram_reduce(int splits, int a, int b, const double* __restrict__ work, double* __restrict__ c,
-                            int ldc, int sym, int tile, const int* __restrict__ run_if) {
+__global__ void __launch_bounds__(256) gram_reduce(int splits, int a, int b, const double* __restrict__ work,
+                                                    double* __restrict__ c, int ldc, int sym, int tile,
+                                                    const int* __restrict__ run_if) {
+    // 32 outputs per CTA (coalesced along the partial tiles), the splits dealt
+    // to 8 fixed contiguous groups summed in split order, the group sums added
+    // in group order: deterministic, and 8 loads in flight per output instead
+    // of one serial chain over all splits
     if (run_if && *run_if == 0) return;
+    __shared__ double red[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t total = static_cast<int64_t>(a) * b;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(e / b), j = static_cast<int>(e % b);
-        const int64_t src = sym && i / tile > j / tile ? static_cast<int64_t>(j) * b + i : e;
-        double s = 0.0;
-        for (int p = 0; p < splits; ++p) s += work[static_cast<size_t>(p) * total + src];
-        c[static_cast<size_t>(i) * ldc + j] = s;
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+    int i = 0, j = 0;
+    int64_t src = 0;
+    if (e < total) {
+        i = static_cast<int>(e / b);
+        j = static_cast<int>(e % b);
+        src = sym && i / tile > j / tile ? static_cast<int64_t>(j) * b + i : e;
+    }
+    const int p0 = static_cast<int>(static_cast<int64_t>(splits) * ty / 8);
+    const int p1 = static_cast<int>(static_cast<int64_t>(splits) * (ty + 1) / 8);
+    double sacc = 0.0;
+    if (e < total)
+        for (int p = p0; p < p1; ++p) sacc += work[static_cast<size_t>(p) * total + src];
+    red[ty][tx] = sacc;
+    __syncthreads();
+    if (ty == 0 && e < total) {
+        double t = red[0][tx];
+#pragma unroll
+        for (int g = 1; g < 8; ++g) t += red[g][tx];
+        c[static_cast<size_t>(i) * ldc + j] = t;
     }
 }
 
@@ -322,7 +345,7 @@ int gram_launch_v(int n, const double* x, int ldx, int a, const double* y, int l
         k8<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, a, y, ldy, b, dst, ldo, p.rows_per_split, run_if);
     if (!direct) {
         const int64_t total = static_cast<int64_t>(a) * b;
-        gram_reduce<<<static_cast<int>(std::min<int64_t>(ceil_div64(total, 256), 4 * kSMs)), 256, 0, s>>>(
+        gram_reduce<<<static_cast<int>(ceil_div64(total, 32)), 256, 0, s>>>(
             p.splits, a, b, w, c, ldc, SYM ? 1 : 0, TM, run_if);
     }
     BK_LAUNCHED();
