@@ -88,7 +88,7 @@ __device__ __forceinline__ void chol_drop_core(int a, const double* __restrict__
         piv[j] = p;
         kept += keep;
         s_keep[j & 1] = keep;
-        s_invp[j & 1] = keep ? 1.0 / p : 0.0;
+        s_invp[j & 1] = keep ? __drcp_rn(p) : 0.0;  // reciprocal without the division routine
     };
     if (tid == 0) decide(0, S[0]);
     __syncthreads();

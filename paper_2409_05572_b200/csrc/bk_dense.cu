@@ -710,6 +710,14 @@ int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc
                                                                run_if);
                 if (nv == 4)  // 64-row tiles of 3 warps, 8-deep, 4 stages: 4 CTAs per SM
                     return gemm_launch_v<64, 72, 8, 1, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+                if (nv == 5)  // 64-row tiles of 6 warps of 32 x 24 (half the accumulators per thread)
+                    return gemm_launch_v<64, 72, 8, 2, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+                if (nv == 6)  // 128-row tiles of 12 warps of 32 x 24
+                    return gemm_launch_v<128, 72, 8, 4, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
+                                                              run_if);
+                if (nv == 7)  // 64-row tiles of 6 warps, 16-deep, 3 stages
+                    return gemm_launch_v<64, 72, 16, 2, 3, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
+                                                              run_if);
                 return gemm_launch_v<128, 72, 16, 2, 3, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
             }
             return gemm_launch_v<UTM, UTN, UTK, UWM, UWN, UST>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
