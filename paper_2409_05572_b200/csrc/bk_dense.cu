@@ -383,6 +383,10 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
             return gram_launch_v<16, 2, 4, 3, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
         case 4:  // 4 warps of 48 x 48, 32-deep, 3 stages, 1 CTA / SM: 24.6 / 24.5 / 24.3 / 22.2
             return gram_launch_v<32, 2, 2, 3, 1, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+        case 5:  // 6 warps of 32 x 48, 8-deep, 4 stages, 3 CTAs / SM
+            return gram_launch_v<8, 3, 2, 4, 3, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
+        case 6:  // 6 warps of 32 x 48, 16-deep, 4 stages, 2 CTAs / SM
+            return gram_launch_v<16, 3, 2, 4, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
         default: {  // 4 warps of 48 x 48 (36 DMMA per 12 fragment loads), 4 stages, 2 CTAs / SM:
                     // 30.3 / 29.6 / 28.8 / 24.4; 72-wide tiles (24-wide warp tiles) for widths
                     // that fit them better
@@ -408,6 +412,9 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
                     return gram_launch_v<GTK, 3, 2, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
                                                                           run_if);
                 }
+            } else if (nv == 4 && na && (SYM || nb)) {
+                // 72 x 72 tiles of 9 warps of 24 x 24 (18 accumulators per thread), 8-deep, 4 CTAs per SM
+                return gram_launch_v<8, 3, 3, 4, 4, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
             } else if (nv == 2 || nv == 3) {
                 // 72 x 72 tiles of 3 warps at 4 (nv 2: 8-deep k steps) or 3 (nv 3) CTAs
                 // per SM, so the 4 SM sub-partitions carry equal warp counts
@@ -702,7 +709,10 @@ int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc
                     const char* e = getenv("BK_GEMM_NARROW");
                     return e ? atoi(e) : 0;
                 }();
-                const int nv = nv_env ? nv_env : (d <= 144 ? 4 : 1);
+                // default: 64-row tiles of 6 warps of 32 x 24 (24 accumulators per
+                // thread, ~70 registers: 4 CTAs = 24 warps per SM); 138 -> 69 with
+                // beta = 1 313 -> 238 us, 207 -> 138 572 -> 556 us (dense_probe)
+                const int nv = nv_env ? nv_env : 5;
                 if (nv == 2)  // 8-deep k steps, 4 stages: 3 CTAs per SM
                     return gemm_launch_v<128, 72, 8, 2, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
                 if (nv == 3)  // 256-row tiles of 12 warps
@@ -719,6 +729,25 @@ int gemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc
                     return gemm_launch_v<64, 72, 16, 2, 3, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
                                                               run_if);
                 return gemm_launch_v<128, 72, 16, 2, 3, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+            }
+            {
+                // BK_GEMM_WIDE: 96-wide tile shape (tuning runs).  Default: 64-row tiles
+                // of 6 warps of 32 x 32 for short contractions (192 -> 96 with beta = 1
+                // 555 -> 419 us, 96 -> 96 214 -> 192 us), 128-row tiles of 4 warps of
+                // 64 x 48 for long ones (288 -> 192: 996 vs 1023 us)
+                static const int wv_env = [] {
+                    const char* e = getenv("BK_GEMM_WIDE");
+                    return e ? atoi(e) : 0;
+                }();
+                const int wv = wv_env ? wv_env : (d <= 200 ? 2 : 1);
+                if (wv == 2)  // 64-row tiles of 6 warps of 32 x 32
+                    return gemm_launch_v<64, 96, 8, 2, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+                if (wv == 3)  // 128-row tiles of 12 warps of 32 x 32
+                    return gemm_launch_v<128, 96, 8, 4, 3, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
+                                                              run_if);
+                if (wv == 4)  // 64-row tiles of 6 warps, 16-deep, 3 stages
+                    return gemm_launch_v<64, 96, 16, 2, 3, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
+                                                              run_if);
             }
             return gemm_launch_v<UTM, UTN, UTK, UWM, UWN, UST>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s,
                                                                run_if);
