@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, co
         double t = 0.0, beta = alpha, scal = 0.0;
         if (xnorm2 > 0.0) {
             beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
-            t = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
+            t = (beta - alpha) * __drcp_rn(beta);  // reciprocals: no division routine on the step's chain
+            scal = __drcp_rn(alpha - beta);
         }
         for (int r = k + 1 + tid; r < d; r += nt) {
             const double vr = r == k + 1 ? 1.0 : col[r] * scal;
@@ -591,8 +591,8 @@ __global__ void __launch_bounds__(NT) tridiag_cluster1_kernel(int d, const doubl
         double t = 0.0, beta = alpha, scal = 0.0;
         if (xnorm2 > 0.0) {
             beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
-            t = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
+            t = (beta - alpha) * __drcp_rn(beta);  // reciprocals: no division routine on the step's chain
+            scal = __drcp_rn(alpha - beta);
         }
         for (int r = k + 1 + tid; r < d; r += nt) {
             const double vr = r == k + 1 ? 1.0 : col[r] * scal;
@@ -905,11 +905,14 @@ __device__ void tri_factor(int d, const double* __restrict__ dg, const double* _
         const double sub = off[i];  // A(i+1, i)
         const double nd = dg[i + 1] - lam;
         const double ns = i + 2 < d ? off[i + 1] : 0.0;
+        // one reciprocal per step on the dependent chain, the multiplier from it
+        // (two IEEE divisions per step bounded the factorisation)
         if (fabs(sub) > fabs(diag_cur)) {  // swap rows i and i+1
-            const double m = diag_cur / sub;
+            const double r = __drcp_rn(sub);
+            const double m = diag_cur * r;
             mult[i] = m;
             swp[i] = 1;
-            rinv[i] = 1.0 / sub;
+            rinv[i] = r;
             u1[i] = nd;
             u2[i] = ns;
             diag_cur = sup_cur - m * nd;
@@ -917,10 +920,11 @@ __device__ void tri_factor(int d, const double* __restrict__ dg, const double* _
             sup2_cur = 0.0;
         } else {
             const double p0 = guard(diag_cur);
-            const double m = sub / p0;
+            const double r = __drcp_rn(p0);
+            const double m = sub * r;
             mult[i] = m;
             swp[i] = 0;
-            rinv[i] = 1.0 / p0;
+            rinv[i] = r;
             u1[i] = sup_cur;
             u2[i] = sup2_cur;
             diag_cur = nd - m * sup_cur;
