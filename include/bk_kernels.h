@@ -38,10 +38,11 @@ BK_API int bk_spmm_d(int n, const int32_t* row_ptr, const int32_t* col, const do
  * graph-local rows (rowid[i]: original row of ordered row i; rp2 / val2: the
  * full CSR in that order, each row's nonzeros in their original order); code[p]
  * = column, or -(slot + 1) when the column is row rowid[t*tile + slot] of the
- * same tile t — those X rows are read from the tile's shared-memory copy. */
-BK_API int bk_spmm_tiled_d(int n, int tile, const int32_t* rp2, const int32_t* code, const double* val2,
-                           const int32_t* rowid, const double* x, int ldx, int k, double* y, int ldy,
-                           void* stream);
+ * same tile t — those X rows are read from the tile's shared-memory copy; nzmax >= the
+ * largest nonzero count of a tile (its index slice is staged on chip too). */
+BK_API int bk_spmm_tiled_d(int n, int tile, int nzmax, const int32_t* rp2, const int32_t* code,
+                           const double* val2, const int32_t* rowid, const double* x, int ldx, int k, double* y,
+                           int ldy, void* stream);
 /* complex Hermitian twin: x, y, val interleaved (re, im); ld in complex elements */
 BK_API int bk_spmm_z(int n, const int32_t* row_ptr, const int32_t* col, const double* val,
                      const double* x, int ldx, int k, double* y, int ldy, void* stream);

@@ -38,6 +38,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pre
     const int sz = pred ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
+// 4-byte variant
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
 // 16-byte variant (cp.async.cg, L2 only); both addresses 16-byte aligned
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

@@ -383,10 +383,6 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
             return gram_launch_v<16, 2, 4, 3, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
         case 4:  // 4 warps of 48 x 48, 32-deep, 3 stages, 1 CTA / SM: 24.6 / 24.5 / 24.3 / 22.2
             return gram_launch_v<32, 2, 2, 3, 1, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
-        case 5:  // 6 warps of 32 x 48, 8-deep, 4 stages, 3 CTAs / SM
-            return gram_launch_v<8, 3, 2, 4, 3, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
-        case 6:  // 6 warps of 32 x 48, 16-deep, 4 stages, 2 CTAs / SM
-            return gram_launch_v<16, 3, 2, 4, 2, SYM>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
         default: {  // 4 warps of 48 x 48 (36 DMMA per 12 fragment loads), 4 stages, 2 CTAs / SM:
                     // 30.3 / 29.6 / 28.8 / 24.4; 72-wide tiles (24-wide warp tiles) for widths
                     // that fit them better
@@ -412,9 +408,6 @@ int gram_launch(int n, const double* x, int ldx, int a, const double* y, int ldy
                     return gram_launch_v<GTK, 3, 2, GST, 2, false, 72, 96>(n, x, ldx, a, y, ldy, b, c, ldc, work, s,
                                                                           run_if);
                 }
-            } else if (nv == 4 && na && (SYM || nb)) {
-                // 72 x 72 tiles of 9 warps of 24 x 24 (18 accumulators per thread), 8-deep, 4 CTAs per SM
-                return gram_launch_v<8, 3, 3, 4, 4, SYM, 72, 72>(n, x, ldx, a, y, ldy, b, c, ldc, work, s, run_if);
             } else if (nv == 2 || nv == 3) {
                 // 72 x 72 tiles of 3 warps at 4 (nv 2: 8-deep k steps) or 3 (nv 3) CTAs
                 // per SM, so the 4 SM sub-partitions carry equal warp counts

@@ -247,101 +247,91 @@ __global__ void __launch_bounds__(256) spmm_d_half_kernel(int n, const int32_t* 
 
 // Cluster-tiled SpMM (bk_spmm_tiled_d): the rows are regrouped into tiles of
 // T graph-local rows (host-side BFS clustering, host/matrix.cpp), so most
-// nonzeros of a tile's rows point at rows of the same tile.  A CTA copies the
-// tile's own X rows into shared memory once (cp.async, double-buffered: the
-// next tile's copy overlaps this tile's products) and reads in-tile nonzeros
-// from there; only the rest are gathered from L2/HBM.  Config 2's 7-point
-// stencil: ~5 L2 row-gathers per row with the plain kernel (L1 hit 26 %),
-// ~1 + the boundary fraction here.  Per row the arithmetic and its order are
-// the plain kernel's (nonzeros in their original order), so Y is bit-identical.
+// nonzeros of a tile's rows point at rows of the same tile (7-point stencil,
+// T = 64: ~4^3 blobs, ~3/4 of the nonzeros).  A CTA stages, with cp.async, the
+// tile's own X rows AND its index slice (row pointers, original row ids,
+// (code, val) of every nonzero) in shared memory; the products then read all
+// indices and the in-tile X rows on chip and gather only the rest from L2/HBM
+// — one round trip per row (its out-of-tile gathers issued together) instead
+// of three dependent ones (row pointer -> (col, val) -> gathers).  Single
+// buffer, several CTAs per SM: one CTA's staging overlaps the others' products.
+// Per row the arithmetic and its order are the plain kernel's (nonzeros in
+// their original order), so Y is bit-identical.
 template <int VPL>
-__global__ void __launch_bounds__(256) spmm_d_tile_kernel(int n, int T, int ntiles, const int32_t* __restrict__ rp2,
+__global__ void __launch_bounds__(256) spmm_d_tile_kernel(int n, int T, int ntiles, int nzmax,
+                                                           const int32_t* __restrict__ rp2,
                                                            const int32_t* __restrict__ code,
                                                            const double* __restrict__ val,
                                                            const int32_t* __restrict__ rowid,
                                                            const double* __restrict__ x, int ldx, int k, int kp,
                                                            bool v16, double* __restrict__ y, int ldy) {
-    extern __shared__ __align__(16) double win[];  // 2 x T x kp
+    extern __shared__ __align__(16) double win[];  // T x kp X rows | nzmax vals | nzmax codes, T+1 rp, T ids
+    double* sval = win + static_cast<size_t>(T) * kp;
+    int* scode = reinterpret_cast<int*>(sval + nzmax);
+    int* srp = scode + nzmax;
+    int* sid = srp + T + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    auto stage = [&](int t, int b) {
-        double* w = win + static_cast<size_t>(b) * T * kp;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int r0 = t * T, nr = min(T, n - r0);
-        if (v16) {
-            const int cpr = kp >> 1;
-            for (int e = tid; e < nr * cpr; e += blockDim.x) {
-                const int sl = e / cpr, c2 = (e - sl * cpr) << 1;
-                const int row = __ldg(rowid + r0 + sl);
-                cp_async16(w + sl * kp + c2, x + static_cast<size_t>(row) * ldx + c2, true);
-            }
-        } else {
-            for (int e = tid; e < nr * k; e += blockDim.x) {
-                const int sl = e / k, c = e - sl * k;
-                const int row = __ldg(rowid + r0 + sl);
-                cp_async8(w + sl * kp + c, x + static_cast<size_t>(row) * ldx + c, true);
+        const int p0 = __ldg(rp2 + r0), p1 = __ldg(rp2 + r0 + nr);
+        // index slice
+        for (int i = tid; i <= nr; i += blockDim.x) cp_async4(srp + i, rp2 + r0 + i);
+        for (int i = tid; i < nr; i += blockDim.x) cp_async4(sid + i, rowid + r0 + i);
+        for (int q = tid; q < p1 - p0; q += blockDim.x) {
+            cp_async4(scode + q, code + p0 + q);
+            cp_async8(sval + q, val + p0 + q, true);
+        }
+        // the tile's X rows: threads split by row, so each loads its row id once
+        const int tpr = max(1, static_cast<int>(blockDim.x) / T);  // threads per row
+        for (int sl = tid / tpr; sl < nr; sl += blockDim.x / tpr) {
+            const int row = __ldg(rowid + r0 + sl);
+            const double* src = x + static_cast<size_t>(row) * ldx;
+            double* dst = win + sl * kp;
+            if (v16) {
+                for (int c2 = (tid % tpr) * 2; c2 < kp; c2 += 2 * tpr) cp_async16(dst + c2, src + c2, true);
+            } else {
+                for (int c = tid % tpr; c < k; c += tpr) cp_async8(dst + c, src + c, true);
             }
         }
         cp_async_commit();
-    };
-    int t = blockIdx.x, b = 0;
-    if (t < ntiles) stage(t, 0);
-    for (; t < ntiles; t += gridDim.x, b ^= 1) {
-        const int tn = t + gridDim.x;
-        if (tn < ntiles) stage(tn, b ^ 1);
-        else cp_async_commit();
-        cp_async_wait<1>();
+        cp_async_wait<0>();
         __syncthreads();
-        const double* w = win + static_cast<size_t>(b) * T * kp;
-        const int r0 = t * T, nr = min(T, n - r0);
         for (int sl = warp; sl < nr; sl += nw) {
-            const int i = r0 + sl;
-            const int orow = __ldg(rowid + i);
-            const int s = __ldg(rp2 + i), e = __ldg(rp2 + i + 1);
+            const int s = srp[sl] - p0, e = srp[sl + 1] - p0;
             double acc[VPL];
 #pragma unroll
             for (int u = 0; u < VPL; ++u) acc[u] = 0.0;
-            for (int pb = s; pb < e; pb += 32) {
-                const int p = pb + lane;
-                int my_c = 0;
-                double my_v = 0.0;
-                if (p < e) {
-                    my_c = __ldg(code + p);
-                    my_v = __ldg(val + p);
-                }
-                const int cnt = min(32, e - pb);
-                constexpr int G = 4;
-                for (int q0 = 0; q0 < cnt; q0 += G) {
-                    double xv[G][VPL], vv[G];
+            constexpr int G = 4;
+            for (int q0 = s; q0 < e; q0 += G) {
+                double xv[G][VPL], vv[G];
 #pragma unroll
-                    for (int q = 0; q < G; ++q) {
-                        const bool live = q0 + q < cnt;
-                        const int c = __shfl_sync(0xffffffffu, my_c, live ? q0 + q : q0);
-                        vv[q] = __shfl_sync(0xffffffffu, my_v, live ? q0 + q : q0);
-                        if (c < 0) {  // in-tile row: shared memory
-                            const double* xr = w + (-c - 1) * kp + lane;
+                for (int q = 0; q < G; ++q) {
+                    const bool live = q0 + q < e;
+                    const int c = live ? scode[q0 + q] : -1;
+                    vv[q] = live ? sval[q0 + q] : 0.0;
+                    if (c < 0) {  // in-tile row (or padding): shared memory
+                        const double* xr = win + (live ? -c - 1 : 0) * kp + lane;
 #pragma unroll
-                            for (int u = 0; u < VPL; ++u) xv[q][u] = live && lane + 32 * u < k ? xr[32 * u] : 0.0;
-                        } else {
-                            const double* xr = x + static_cast<size_t>(c) * ldx + lane;
+                        for (int u = 0; u < VPL; ++u) xv[q][u] = live && lane + 32 * u < k ? xr[32 * u] : 0.0;
+                    } else {
+                        const double* xr = x + static_cast<size_t>(c) * ldx + lane;
 #pragma unroll
-                            for (int u = 0; u < VPL; ++u)
-                                xv[q][u] = live && lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
-                        }
+                        for (int u = 0; u < VPL; ++u) xv[q][u] = lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
                     }
-#pragma unroll
-                    for (int q = 0; q < G; ++q)
-                        if (q0 + q < cnt)
-#pragma unroll
-                            for (int u = 0; u < VPL; ++u) acc[u] = fma(vv[q], xv[q][u], acc[u]);
                 }
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    if (q0 + q < e)
+#pragma unroll
+                        for (int u = 0; u < VPL; ++u) acc[u] = fma(vv[q], xv[q][u], acc[u]);
             }
-            double* yr = y + static_cast<size_t>(orow) * ldy + lane;
+            double* yr = y + static_cast<size_t>(sid[sl]) * ldy + lane;
 #pragma unroll
             for (int u = 0; u < VPL; ++u)
                 if (lane + 32 * u < k) yr[32 * u] = acc[u];
         }
-        __syncthreads();  // buffer b is restaged two tiles on
+        __syncthreads();  // the buffer is restaged for the next tile
     }
-    cp_async_wait<0>();
 }
 
 // tile rows per CTA step and resident CTAs per SM for spmm_d_kernel
@@ -434,11 +424,11 @@ extern "C" int bk_spmm_z(int n, const int32_t* rp, const int32_t* ci, const doub
     BK_LAUNCHED();
 }
 
-extern "C" int bk_spmm_tiled_d(int n, int tile, const int32_t* rp2, const int32_t* code, const double* val2,
-                               const int32_t* rowid, const double* x, int ldx, int k, double* y, int ldy,
-                               void* stream) {
+extern "C" int bk_spmm_tiled_d(int n, int tile, int nzmax, const int32_t* rp2, const int32_t* code,
+                               const double* val2, const int32_t* rowid, const double* x, int ldx, int k, double* y,
+                               int ldy, void* stream) {
     if (n <= 0 || k <= 0) return 0;
-    if (tile <= 0 || tile > 256) return static_cast<int>(cudaErrorInvalidValue);
+    if (tile <= 0 || tile > 256 || nzmax < 0) return static_cast<int>(cudaErrorInvalidValue);
     const cudaStream_t s = as_stream(stream);
     // widths beyond 96 run as column chunks of <= 96 (the tile copy holds one chunk)
     for (int c0 = 0; c0 < k; c0 += 96) {
@@ -449,33 +439,26 @@ extern "C" int bk_spmm_tiled_d(int n, int tile, const int32_t* rp2, const int32_
         // 16-byte copies take an even width; the extra column is inside the row (ld even > k)
         const int kp = v16 ? (kc + 1) / 2 * 2 : kc;
         if (v16 && kp > ldx - c0) return static_cast<int>(cudaErrorInvalidValue);
-        const size_t smem = 2 * sizeof(double) * static_cast<size_t>(tile) * kp;
+        const size_t smem = sizeof(double) * (static_cast<size_t>(tile) * kp + nzmax) +
+                            sizeof(int) * (static_cast<size_t>(nzmax) + 2 * tile + 1);
+        if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidValue);
         const int ntiles = ceil_div(n, tile);
         static const int cps = [] {  // BK_SPMM_TILED_CPS: CTAs per SM (tuning runs)
             const char* e = getenv("BK_SPMM_TILED_CPS");
-            return e ? max(1, atoi(e)) : 1;
+            return e ? max(1, atoi(e)) : 4;
         }();
         const int grid = max(1, min(ntiles, kSMs * cps));
-        if (kc <= 32) {
-            static const cudaError_t a = cudaFuncSetAttribute(spmm_d_tile_kernel<1>,
-                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            BK_RET(a);
-            spmm_d_tile_kernel<1><<<grid, 256, smem, s>>>(n, tile, ntiles, rp2, code, val2, rowid, xc, ldx, kc, kp,
-                                                          v16, yc, ldy);
-        } else if (kc <= 64) {
-            static const cudaError_t a = cudaFuncSetAttribute(spmm_d_tile_kernel<2>,
-                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            BK_RET(a);
-            spmm_d_tile_kernel<2><<<grid, 256, smem, s>>>(n, tile, ntiles, rp2, code, val2, rowid, xc, ldx, kc, kp,
-                                                          v16, yc, ldy);
-        } else {
-            static const cudaError_t a = cudaFuncSetAttribute(spmm_d_tile_kernel<3>,
-                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            BK_RET(a);
-            spmm_d_tile_kernel<3><<<grid, 256, smem, s>>>(n, tile, ntiles, rp2, code, val2, rowid, xc, ldx, kc, kp,
-                                                          v16, yc, ldy);
-        }
-        BK_RET(cudaGetLastError());
+        auto launch = [&](auto kern) -> cudaError_t {
+            const cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem));
+            if (a != cudaSuccess) return a;
+            kern<<<grid, 256, smem, s>>>(n, tile, ntiles, nzmax, rp2, code, val2, rowid, xc, ldx, kc, kp, v16, yc,
+                                         ldy);
+            return cudaGetLastError();
+        };
+        if (kc <= 32) BK_RET(launch(spmm_d_tile_kernel<1>));
+        else if (kc <= 64) BK_RET(launch(spmm_d_tile_kernel<2>));
+        else BK_RET(launch(spmm_d_tile_kernel<3>));
     }
     return 0;
 }

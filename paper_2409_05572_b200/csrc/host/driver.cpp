@@ -287,8 +287,8 @@ private:
         if (k <= 0) return;
         auto t = prof_begin();
         if (cw_ == 1 && csr_->tile > 0)
-            BKC(bk_spmm_tiled_d(n_, csr_->tile, csr_->rp2.as<int32_t>(), csr_->code.as<int32_t>(), csr_->val2.d(),
-                                csr_->rowid.as<int32_t>(), x.p, x.ld, k, y.p, y.ld, st()));
+            BKC(bk_spmm_tiled_d(n_, csr_->tile, csr_->tile_nzmax, csr_->rp2.as<int32_t>(), csr_->code.as<int32_t>(),
+                                csr_->val2.d(), csr_->rowid.as<int32_t>(), x.p, x.ld, k, y.p, y.ld, st()));
         else if (cw_ == 1)
             BKC(bk_spmm_d(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
                           y.ld, st()));

@@ -116,7 +116,7 @@ struct DeviceCsr {
     bool negated = false;
     // cluster-tiled copy for bk_spmm_tiled_d (tile == 0: not built, the graph has
     // too little locality); see cluster_rows() in host/matrix.cpp
-    int tile = 0;
+    int tile = 0, tile_nzmax = 0;
     double in_tile_frac = 0.0;
     DevMem rp2, code, val2, rowid;
 };

@@ -387,9 +387,9 @@ const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
         cuda_check(cudaMemcpy(e->val.as<void>(), fval.data(), sizeof(double) * fval.size(), cudaMemcpyHostToDevice), "upload");
     }
     // cluster-tiled copy (real matrices; BLOCKEIG_SPMM_TILE = rows per tile).  Off by
-    // default: measured 3x slower than the plain K1 on config 2 (one 143 KB CTA per
-    // SM holds 8 warps, too few to cover the remaining gathers and the per-row
-    // index loads; the plain kernel keeps 32 warps per SM in flight)
+    // default: at parity with the plain K1 on config 2 (BFS tiles of 64 rows keep
+    // 64 % of the stencil's nonzeros in-tile), and it adds the clustering to a
+    // fresh handle's first solve
     static const int tile = [] {
         const char* v = std::getenv("BLOCKEIG_SPMM_TILE");
         return v ? std::max(0, std::min(256, std::atoi(v))) : 0;
@@ -412,7 +412,11 @@ const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
                 }
                 rp2[i + 1] = static_cast<int32_t>(q);
             }
+            int nzmax = 0;
+            for (int i = 0; i < n_; i += tile)
+                nzmax = std::max(nzmax, rp2[std::min(n_, i + tile)] - rp2[i]);
             e->tile = tile;
+            e->tile_nzmax = nzmax;
             e->in_tile_frac = frac;
             e->rp2.alloc(sizeof(int32_t) * rp2.size());
             e->code.alloc(sizeof(int32_t) * code.size());

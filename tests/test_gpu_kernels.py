@@ -112,14 +112,15 @@ def test_spmm_tiled_bit_identical(bk, k, perm):
     y1 = torch.zeros_like(x)
     y2 = torch.zeros_like(x)
     f = bk
-    f.bk_spmm_tiled_d.argtypes = [C.c_int, C.c_int] + [_D] * 5 + [C.c_int, C.c_int, _D, C.c_int, _D]
+    f.bk_spmm_tiled_d.argtypes = [C.c_int, C.c_int, C.c_int] + [_D] * 5 + [C.c_int, C.c_int, _D, C.c_int, _D]
+    nzmax = max(rp2[min(n, i + tile)] - rp2[i] for i in range(0, n, tile))
     t_rp, t_c, t_v = dev(frp), dev(fcol), dev(fval)
     assert f.bk_spmm_d(n, ptr(t_rp), ptr(t_c), ptr(t_v), ptr(x), ld, k, ptr(y1), ld, stream()) == 0
     r2 = dev(np.array(rp2, dtype=np.int32))
     c2 = dev(np.array(code, dtype=np.int32))
     v2 = dev(np.array(val2))
     oid = dev(order)
-    assert f.bk_spmm_tiled_d(n, tile, ptr(r2), ptr(c2), ptr(v2), ptr(oid), ptr(x), ld, k, ptr(y2), ld,
+    assert f.bk_spmm_tiled_d(n, tile, nzmax, ptr(r2), ptr(c2), ptr(v2), ptr(oid), ptr(x), ld, k, ptr(y2), ld,
                              stream()) == 0
     torch.cuda.synchronize()
     assert torch.equal(y1[:, :k], y2[:, :k])
