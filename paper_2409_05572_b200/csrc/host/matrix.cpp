@@ -264,25 +264,33 @@ double SparseSym::norm_est() const {
 
 namespace {
 // Graph-local row order for the cluster-tiled SpMM: rows are grouped into tiles
-// of `tile` rows grown breadth-first over the sparsity graph, each tile seeded
-// from the oldest unplaced row the previous tiles reached (so consecutive tiles
-// are neighbours and their boundary rows stay L2-resident together).  Returns
-// the order (ordered index -> row) and the fraction of nonzeros whose column
-// lies in the row's own tile.
+// of `tile` rows grown greedily over the sparsity graph — each step takes the
+// unplaced row with the most neighbours already in the tile (oldest first among
+// equals), which grows compact, cube-like blobs (7-point stencil, tile 64: 80 %
+// of the nonzeros in-tile, against 64 % for breadth-first balls); a tile is
+// seeded from the oldest row the previous tiles reached, so consecutive tiles
+// are neighbours.  Returns the order (ordered index -> row) and the fraction of
+// nonzeros whose column lies in the row's own tile.
 double cluster_rows(int n, const std::vector<int32_t>& rp, const std::vector<int32_t>& col, int tile,
                     std::vector<int32_t>& order) {
     order.clear();
     order.reserve(n);
-    std::vector<int32_t> tile_of(static_cast<size_t>(n), -1);
+    std::vector<int32_t> tile_of(static_cast<size_t>(n), -1), gain(static_cast<size_t>(n), 0);
     std::vector<int32_t> frontier;  // global FIFO of reached rows (may repeat)
     size_t fhead = 0;
     int next_seed = 0;
-    std::vector<int32_t> q;
+    constexpr int kB = 16;  // gain buckets (gains >= 15 share the last)
+    std::vector<int32_t> bucket[kB];
+    size_t bhead[kB];
+    std::vector<int32_t> touched;
     while (static_cast<int>(order.size()) < n) {
         const int t = static_cast<int>(order.size()) / tile;
         const size_t start = order.size();
-        q.clear();
-        size_t qh = 0;
+        for (int g = 0; g < kB; ++g) {
+            bucket[g].clear();
+            bhead[g] = 0;
+        }
+        touched.clear();
         auto seed = [&]() {
             while (fhead < frontier.size() && tile_of[frontier[fhead]] >= 0) ++fhead;
             if (fhead < frontier.size()) return frontier[fhead++];
@@ -290,17 +298,28 @@ double cluster_rows(int n, const std::vector<int32_t>& rp, const std::vector<int
             return next_seed < n ? next_seed : -1;
         };
         while (order.size() - start < static_cast<size_t>(tile)) {
-            while (qh < q.size() && tile_of[q[qh]] >= 0) ++qh;
-            int u;
-            if (qh < q.size()) u = q[qh++];
-            else if ((u = seed()) < 0) break;
+            int u = -1;
+            for (int g = kB - 1; g > 0 && u < 0; --g) {
+                auto& b = bucket[g];
+                while (bhead[g] < b.size() &&
+                       (tile_of[b[bhead[g]]] >= 0 || std::min(gain[b[bhead[g]]], kB - 1) != g))
+                    ++bhead[g];
+                if (bhead[g] < b.size()) u = b[bhead[g]++];
+            }
+            if (u < 0 && (u = seed()) < 0) break;
             tile_of[u] = t;
             order.push_back(u);
-            for (int32_t p = rp[u]; p < rp[u + 1]; ++p)
-                if (tile_of[col[p]] < 0) q.push_back(col[p]);
+            for (int32_t p = rp[u]; p < rp[u + 1]; ++p) {
+                const int c = col[p];
+                if (tile_of[c] >= 0) continue;
+                if (gain[c]++ == 0) touched.push_back(c);
+                bucket[std::min(gain[c], kB - 1)].push_back(c);
+            }
         }
-        for (; qh < q.size(); ++qh)
-            if (tile_of[q[qh]] < 0) frontier.push_back(q[qh]);
+        for (int c : touched) {
+            if (tile_of[c] < 0) frontier.push_back(c);
+            gain[c] = 0;
+        }
     }
     int64_t in = 0;
     for (int r = 0; r < n; ++r)
