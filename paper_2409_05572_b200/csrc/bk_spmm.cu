@@ -334,6 +334,99 @@ __global__ void __launch_bounds__(256) spmm_d_tile_kernel(int n, int T, int ntil
     }
 }
 
+// Half-warp form of the tiled kernel (16-byte X rows): two rows per warp, each
+// half-warp lane holding 2 columns per 16-byte load, so a nonzero costs half the
+// load / shared-memory instructions per row (the one-row-per-warp form is
+// issue-bound once the gathers stay on chip).
+template <int V2>
+__global__ void __launch_bounds__(256) spmm_d_tile2_kernel(int n, int T, int ntiles, int nzmax,
+                                                            const int32_t* __restrict__ rp2,
+                                                            const int32_t* __restrict__ code,
+                                                            const double* __restrict__ val,
+                                                            const int32_t* __restrict__ rowid,
+                                                            const double* __restrict__ x, int ldx, int k, int kp,
+                                                            double* __restrict__ y, int ldy) {
+    extern __shared__ __align__(16) double win[];  // T x kp X rows | nzmax vals | nzmax codes, T+1 rp, T ids
+    double* sval = win + static_cast<size_t>(T) * kp;
+    int* scode = reinterpret_cast<int*>(sval + nzmax);
+    int* srp = scode + nzmax;
+    int* sid = srp + T + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int hl = lane & 15, half = lane >> 4;
+    const int k2 = (k + 1) >> 1, kp2 = kp >> 1, ldx2 = ldx >> 1, ldy2 = ldy >> 1;
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+    const double2* w2 = reinterpret_cast<const double2*>(win);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int r0 = t * T, nr = min(T, n - r0);
+        const int p0 = __ldg(rp2 + r0), p1 = __ldg(rp2 + r0 + nr);
+        for (int i = tid; i <= nr; i += blockDim.x) cp_async4(srp + i, rp2 + r0 + i);
+        for (int i = tid; i < nr; i += blockDim.x) cp_async4(sid + i, rowid + r0 + i);
+        for (int q = tid; q < p1 - p0; q += blockDim.x) {
+            cp_async4(scode + q, code + p0 + q);
+            cp_async8(sval + q, val + p0 + q, true);
+        }
+        const int tpr = max(1, static_cast<int>(blockDim.x) / T);
+        for (int sl = tid / tpr; sl < nr; sl += blockDim.x / tpr) {
+            const int row = __ldg(rowid + r0 + sl);
+            const double* src = x + static_cast<size_t>(row) * ldx;
+            double* dst = win + sl * kp;
+            for (int c2 = (tid % tpr) * 2; c2 < kp; c2 += 2 * tpr) cp_async16(dst + c2, src + c2, true);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        for (int sb = 2 * warp; sb < nr; sb += 2 * nw) {
+            const int sl = sb + half;
+            const bool rowok = sl < nr;
+            const int s = rowok ? srp[sl] - p0 : 0, e = rowok ? srp[sl + 1] - p0 : 0;
+            double2 acc[V2];
+#pragma unroll
+            for (int u = 0; u < V2; ++u) acc[u] = make_double2(0.0, 0.0);
+            constexpr int G = 4;
+            for (int q0 = s; q0 < e; q0 += G) {
+                double2 xv[G][V2];
+                double vv[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const bool live = q0 + q < e;
+                    const int c = live ? scode[q0 + q] : -1;
+                    vv[q] = live ? sval[q0 + q] : 0.0;
+                    if (c < 0) {
+                        const double2* xr = w2 + (live ? -c - 1 : 0) * kp2 + hl;
+#pragma unroll
+                        for (int u = 0; u < V2; ++u)
+                            xv[q][u] = live && hl + 16 * u < k2 ? xr[16 * u] : make_double2(0.0, 0.0);
+                    } else {
+                        const double2* xr = x2 + static_cast<size_t>(c) * ldx2 + hl;
+#pragma unroll
+                        for (int u = 0; u < V2; ++u)
+                            xv[q][u] = hl + 16 * u < k2 ? __ldg(xr + 16 * u) : make_double2(0.0, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    if (q0 + q < e)
+#pragma unroll
+                        for (int u = 0; u < V2; ++u) {
+                            acc[u].x = fma(vv[q], xv[q][u].x, acc[u].x);
+                            acc[u].y = fma(vv[q], xv[q][u].y, acc[u].y);
+                        }
+            }
+            if (rowok) {
+                double* yr = y + static_cast<size_t>(sid[sl]) * ldy;
+#pragma unroll
+                for (int u = 0; u < V2; ++u) {
+                    const int c = 2 * (hl + 16 * u);
+                    if (c + 1 < k) reinterpret_cast<double2*>(yr)[hl + 16 * u] = acc[u];
+                    else if (c < k) yr[c] = acc[u].x;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    (void)ldy2;
+}
+
 // tile rows per CTA step and resident CTAs per SM for spmm_d_kernel
 // (BK_SPMM_TILE / BK_SPMM_CPS override, for tuning runs only)
 struct SpmmShape {
@@ -456,7 +549,22 @@ extern "C" int bk_spmm_tiled_d(int n, int tile, int nzmax, const int32_t* rp2, c
                                          ldy);
             return cudaGetLastError();
         };
-        if (kc <= 32) BK_RET(launch(spmm_d_tile_kernel<1>));
+        // half-warp rows with 16-byte accesses when X and Y rows allow them
+        static const bool one_row = getenv("BK_SPMM_TILED_1ROW") != nullptr;  // tuning runs
+        const bool y16 = (ldy % 2 == 0) && (reinterpret_cast<uintptr_t>(yc) % 16 == 0);
+        if (v16 && y16 && !one_row) {
+            auto launch2 = [&](auto kern) -> cudaError_t {
+                const cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           static_cast<int>(smem));
+                if (a != cudaSuccess) return a;
+                kern<<<grid, 256, smem, s>>>(n, tile, ntiles, nzmax, rp2, code, val2, rowid, xc, ldx, kc, kp, yc,
+                                             ldy);
+                return cudaGetLastError();
+            };
+            if (kc <= 32) BK_RET(launch2(spmm_d_tile2_kernel<1>));
+            else if (kc <= 64) BK_RET(launch2(spmm_d_tile2_kernel<2>));
+            else BK_RET(launch2(spmm_d_tile2_kernel<3>));
+        } else if (kc <= 32) BK_RET(launch(spmm_d_tile_kernel<1>));
         else if (kc <= 64) BK_RET(launch(spmm_d_tile_kernel<2>));
         else BK_RET(launch(spmm_d_tile_kernel<3>));
     }
