@@ -53,6 +53,34 @@ __device__ __forceinline__ void load_rows(double* dst, int pitch, const double* 
 }
 
 // ------------------------------------------------------------------ Gram
+// Diagonal tiles of the symmetric Gram with 72 x 72 tiles of 3 warps: only the
+// 45 upper 8 x 8 fragments of the 81 are computed, dealt 15 per warp by row
+// fragments {0,5,7} {1,3,8} {2,4,6} (9+4+2, 8+6+1, 7+5+3); the warp role is a
+// template parameter so every skip is decided at compile time.
+template <int W>
+struct TriRows {
+    static constexpr int r0 = W == 0 ? 0 : (W == 1 ? 1 : 2);
+    static constexpr int r1 = W == 0 ? 5 : (W == 1 ? 3 : 4);
+    static constexpr int r2 = W == 0 ? 7 : (W == 1 ? 8 : 6);
+    static constexpr int lo = r0;  // smallest row fragment: no column below it is needed
+    __host__ __device__ static constexpr int row(int mi) { return mi == 0 ? r0 : (mi == 1 ? r1 : r2); }
+};
+
+template <int W, int PX, int PY, int FN>
+__device__ __forceinline__ void tri_k4(double (&acc)[3][FN][2], const double* xd, const double* yd, int k4, int t,
+                                       int g) {
+    double af[3], bf[FN];
+#pragma unroll
+    for (int mi = 0; mi < 3; ++mi) af[mi] = xd[(k4 + t) * PX + TriRows<W>::row(mi) * 8 + g];
+#pragma unroll
+    for (int ni = TriRows<W>::lo; ni < FN; ++ni) bf[ni] = yd[(k4 + t) * PY + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 3; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < FN; ++ni)
+            if (ni >= TriRows<W>::row(mi)) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+}
+
 template <int TM, int TN, int TK, int WM, int WN, int STAGES, bool V16, bool SYM = false>
 __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double* __restrict__ x, int ldx, int a,
                                                              const double* __restrict__ y, int ldy, int b,
@@ -86,6 +114,8 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
     // X^T X on a diagonal tile of the symmetric Gram (CholQR's W^T W): the Y
     // tile is the X tile — staged once, read through both fragment paths
     const bool same = SYM && ti == tj && x == y && ldx == ldy;
+    constexpr bool TRI = SYM && TM == 72 && TN == 72 && WM == 3 && WN == 1;
+    const bool diag = SYM && ti == tj;
 
     double acc[FM][FN][2];
 #pragma unroll
@@ -112,6 +142,17 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
         cp_async_commit();
         const double* xd = xs + (kt % STAGES) * TK * PX;
         const double* yd = same ? xd : ys + (kt % STAGES) * TK * PY;
+        if constexpr (TRI) {
+            if (diag) {
+#pragma unroll
+                for (int k4 = 0; k4 < TK; k4 += 4) {
+                    if (warp == 0) tri_k4<0, PX, PY, FN>(acc, xd, yd, k4, t, g);
+                    else if (warp == 1) tri_k4<1, PX, PY, FN>(acc, xd, yd, k4, t, g);
+                    else tri_k4<2, PX, PY, FN>(acc, xd, yd, k4, t, g);
+                }
+                continue;
+            }
+        }
 #pragma unroll
         for (int k4 = 0; k4 < TK; k4 += 4) {
             double af[FM], bf[FN];
@@ -128,6 +169,29 @@ __global__ void __launch_bounds__(WM * WN * 32) gram_kernel(int n, const double*
     cp_async_wait<0>();
 
     double* o = out + static_cast<size_t>(split) * a * ldo;
+    if constexpr (TRI) {
+        if (diag) {  // computed upper fragments, each also written at its mirror position
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi) {
+                const int rf = warp == 0 ? TriRows<0>::row(mi) : (warp == 1 ? TriRows<1>::row(mi) : TriRows<2>::row(mi));
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) {
+                    if (ni < rf) continue;
+                    const int i = i0 + rf * 8 + g;
+                    const int j = j0 + ni * 8 + 2 * t;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int jj = j + h;
+                        if (i < a && jj < b) {
+                            o[static_cast<size_t>(i) * ldo + jj] = acc[mi][ni][h];
+                            if (ni > rf) o[static_cast<size_t>(jj) * ldo + i] = acc[mi][ni][h];
+                        }
+                    }
+                }
+            }
+            return;
+        }
+    }
 #pragma unroll
     for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
