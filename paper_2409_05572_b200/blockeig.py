@@ -342,10 +342,11 @@ class Result:
     @property
     def vectors(self) -> np.ndarray:
         n, k = self.rows, self.nev
-        out = np.zeros(n * k * 2)
+        out = np.empty(n * k)  # every entry is written by the copy-out
         got = self.L.lib.beig_result_vectors(self.h, _dptr(out), n * k)
         if got == n * k:
-            return out[: n * k].reshape((n, k), order="F")
+            return out.reshape((n, k), order="F")
+        out = np.empty(n * k * 2)
         got = self.L.lib.beig_result_vectors_z(self.h, _dptr(out), 2 * n * k)
         if got != 2 * n * k:
             raise BlockeigError(ERR_INTERNAL, "vector copy-out failed")
