@@ -236,7 +236,7 @@ def config4(side=96, x0=True):
     n = side ** 3
     rp2, c2, v2 = squared(n, rp, c, v)
     return Workload(f"cfg4_anderson_{side}_lobpcg", n, rp2, c2, v2, "lobpcg",
-                    dict(n_ev=128, n_ex=160, tol=1e-7, max_iters=20000), "fix", {},
+                    dict(n_ev=128, n_ex=160, tol=1e-7, max_iters=40000), "fix", {},
                     x0_columns(n, 160, 3, "normal") if x0 else None)
 
 
