@@ -384,23 +384,36 @@ const SparseSym::FullCsr& SparseSym::full_csr() const {
     frp = cnt;
     fcol.assign(static_cast<size_t>(nnz), 0);
     fval.assign(static_cast<size_t>(nnz) * per, 0.0);
-    std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
-    // rows in order: upper-part entries (c > r) come from later rows' lower
-    // entries, so fill by scanning rows and appending both mirror images;
-    // columns end up sorted because both scans are in increasing order.
-    std::vector<std::vector<std::pair<int, int64_t>>> upper(static_cast<size_t>(n_));
+    // rows in order: a row's lower entries, then its upper entries (c > r), which
+    // are later rows' lower entries — gathered by a counting-sort transpose
+    // (scanning rows in increasing order keeps each row's upper part sorted)
+    std::vector<int64_t> uptr(static_cast<size_t>(n_) + 1, 0);
     for (int r = 0; r < n_; ++r)
         for (int64_t p = rp_[r]; p < rp_[r + 1]; ++p)
-            if (col_[p] != r) upper[col_[p]].push_back({r, p});
+            if (col_[p] != r) uptr[col_[p] + 1]++;
+    for (int r = 0; r < n_; ++r) uptr[r + 1] += uptr[r];
+    std::vector<int64_t> usrc(static_cast<size_t>(uptr[n_]));  // source entry p of each upper entry
+    std::vector<int32_t> urow(static_cast<size_t>(uptr[n_]));
+    {
+        std::vector<int64_t> fill(uptr.begin(), uptr.end() - 1);
+        for (int r = 0; r < n_; ++r)
+            for (int64_t p = rp_[r]; p < rp_[r + 1]; ++p)
+                if (col_[p] != r) {
+                    const int64_t q = fill[col_[p]]++;
+                    usrc[q] = p;
+                    urow[q] = r;
+                }
+    }
     for (int r = 0; r < n_; ++r) {
-        int32_t q = pos[r];
+        int32_t q = cnt[r];
         for (int64_t p = rp_[r]; p < rp_[r + 1]; ++p) {
             fcol[q] = col_[p];
             for (int t = 0; t < per; ++t) fval[static_cast<size_t>(q) * per + t] = sgn * val_[p * per + t];
             ++q;
         }
-        for (const auto& [c, p] : upper[r]) {  // entry (r, c) = conj(A(c, r)), c > r
-            fcol[q] = c;
+        for (int64_t u = uptr[r]; u < uptr[r + 1]; ++u) {  // entry (r, c) = conj(A(c, r)), c > r
+            const int64_t p = usrc[u];
+            fcol[q] = urow[u];
             fval[static_cast<size_t>(q) * per] = sgn * val_[p * per];
             if (complex_) fval[static_cast<size_t>(q) * per + 1] = -sgn * val_[p * per + 1];
             ++q;
