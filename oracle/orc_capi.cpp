@@ -185,6 +185,8 @@ void beig_solve_ext_default(beig_solve_ext* ext) {
     ext->which = BEIG_WHICH_SMALLEST;
     ext->device = 0;
     ext->profile = 0;
+    ext->x0_on_device = 0;
+    ext->vectors_device = nullptr;
 }
 
 int beig_solve_ex(beig_result** out, const beig_matrix* a, int solver, const beig_solver_config* cfg,
@@ -203,6 +205,8 @@ int beig_solve_ex(beig_result** out, const beig_matrix* a, int solver, const bei
         return invalid("beig_solve_ex: unknown operator mode");
     if (ext && (ext->which < BEIG_WHICH_SMALLEST || ext->which > BEIG_WHICH_LARGEST))
         return invalid("beig_solve_ex: unknown target");
+    if (ext && (ext->x0_on_device || ext->vectors_device))
+        return invalid("beig_solve_ex: device-resident blocks need the GPU build");
     return guarded([&] {
         const auto t0 = std::chrono::steady_clock::now();
         orc::SolverCfg sc;
@@ -440,6 +444,11 @@ BEIG_API int orc_project_orthonormalize(const double* w, int n, int a_cols, cons
     });
 }
 
+BEIG_API int beig_harness_project_orthonormalize(const double* w, int n, int a_cols, const double* q, int m,
+                                                 double drop, double* out, int* kept) {
+    return orc_project_orthonormalize(w, n, a_cols, q, m, drop, out, kept);
+}
+
 BEIG_API int orc_sym_eig(const double* h, int d, double* values, double* vectors) {
     return guarded([&] {
         auto e = orc::sym_eig_small(colmajor(h, d, d));
@@ -464,6 +473,11 @@ BEIG_API int orc_hl_trick(const double* s, int n, int d, const double* z, int n_
         std::memcpy(p_out, xp.second.a.data(), xp.second.a.size() * sizeof(double));
         *p_cols = xp.second.c;
     });
+}
+
+BEIG_API int beig_harness_hl_trick(const double* s, int n, int d, const double* z, int n_now, int lock,
+                                   double* x_out, double* p_out, int* p_cols) {
+    return orc_hl_trick(s, n, d, z, n_now, lock, x_out, p_out, p_cols);
 }
 
 // one RR step: values (d), vectors (n x d), coeffs (d x d)

@@ -77,16 +77,51 @@ std::vector<T> spmv(const Sparse<T>& a, const T* x) {
     return y;
 }
 
-// kernel.cpp:28-33 — one column at a time (parallel over columns: each column
-// is the serial SpMV, so the result is independent of the thread count)
+// kernel.cpp:28-33 — one column at a time.  Columns are independent, so the
+// loop over columns is split into groups of up to 8 that share one sweep over
+// the matrix; within a column every operation happens in the serial SpMV's
+// order (spmv above), so the result is bit-identical to column-by-column and
+// independent of the thread count.
+template <class T, int G>
+static void spmv_group(const Sparse<T>& a, const Mat<T>& x, Mat<T>& y, int j0) {
+    const T* xc[G];
+    T* yc[G];
+    for (int g = 0; g < G; ++g) {
+        xc[g] = x.col(j0 + g);
+        yc[g] = y.col(j0 + g);
+    }
+    for (int r = 0; r < a.n; ++r) {
+        T acc[G], xr[G];
+        for (int g = 0; g < G; ++g) {
+            acc[g] = T(0);
+            xr[g] = xc[g][r];
+        }
+        for (int64_t p = a.rp[r]; p < a.rp[r + 1]; ++p) {
+            const int c = a.col[p];
+            const T v = a.val[p];
+            const T vc = conj_(v);
+            for (int g = 0; g < G; ++g) acc[g] += v * xc[g][c];
+            if (c != r)
+                for (int g = 0; g < G; ++g) yc[g][c] += vc * xr[g];
+        }
+        for (int g = 0; g < G; ++g) yc[g][r] += acc[g];
+    }
+}
+
 template <class T>
 Mat<T> spmv_block(const Sparse<T>& a, const Mat<T>& x) {
     if (x.r != a.n) throw std::invalid_argument("spmv_block: dimension mismatch");
     Mat<T> y(x.r, x.c);
-#pragma omp parallel for schedule(static) if (par_ok(double(a.nnz_lower()) * x.c))
-    for (int j = 0; j < x.c; ++j) {
-        std::vector<T> yj = spmv(a, x.col(j));
-        std::copy(yj.begin(), yj.end(), y.col(j));
+    constexpr int G = 8;
+    const int groups = (x.c + G - 1) / G;
+#pragma omp parallel for schedule(dynamic) if (par_ok(double(a.nnz_lower()) * x.c))
+    for (int gi = 0; gi < groups; ++gi) {
+        const int j0 = gi * G;
+        if (j0 + G <= x.c) {
+            spmv_group<T, G>(a, x, y, j0);
+        } else {
+            for (int j = j0; j < x.c; ++j) spmv_group<T, 1>(a, x, y, j);
+        }
     }
     return y;
 }
@@ -107,15 +142,61 @@ static inline T dotc(int n, const T* a, const T* b) {
     return s;
 }
 
-// C = A^H B; each entry is one ascending-k dot product
+// s[ii][jj] += conj(a_ii[k]) b_jj[k] for k in [k0, k1), ascending: BI x BJ
+// independent dot products carried in registers through one sweep
+template <class T, int BI, int BJ>
+static inline void dot_tile(int k0, int k1, const T* const* a, const T* const* b, T (&s)[BI][BJ]) {
+    for (int k = k0; k < k1; ++k) {
+        T av[BI], bv[BJ];
+        for (int i = 0; i < BI; ++i) av[i] = conj_(a[i][k]);
+        for (int j = 0; j < BJ; ++j) bv[j] = b[j][k];
+        for (int i = 0; i < BI; ++i)
+            for (int j = 0; j < BJ; ++j) s[i][j] += av[i] * bv[j];
+    }
+}
+
+// C = A^H B; each entry is one ascending-k dot product.  Blocked for the cache
+// (row chunks of kKc: partial sums are stored in C between chunks, an exact
+// round trip) and for registers (4 x 2 entries per sweep): every entry still
+// accumulates its terms one at a time in ascending k — bit-identical to dotc.
 template <class T>
 Mat<T> gemm_hn(const Mat<T>& a, const Mat<T>& b) {
     if (a.r != b.r) throw std::invalid_argument("gemm_hn: dimension mismatch");
     Mat<T> c(a.c, b.c);
     const int n = a.r;
-#pragma omp parallel for schedule(static) collapse(2) if (par_ok(double(n) * a.c * b.c))
-    for (int j = 0; j < b.c; ++j)
-        for (int i = 0; i < a.c; ++i) c(i, j) = dotc(n, a.col(i), b.col(j));
+    constexpr int BI = 4, BJ = (sizeof(T) == 8 ? 4 : 2), kKc = 256;
+    const int ni = (a.c + BI - 1) / BI, nj = (b.c + BJ - 1) / BJ;
+    const bool par = par_ok(double(n) * a.c * b.c);
+#pragma omp parallel if (par)
+    for (int k0 = 0; k0 < n; k0 += kKc) {
+        const int k1 = std::min(n, k0 + kKc);
+#pragma omp for schedule(static) collapse(2)
+        for (int jb = 0; jb < nj; ++jb)
+            for (int ib = 0; ib < ni; ++ib) {
+                const int i0 = ib * BI, j0 = jb * BJ;
+                if (i0 + BI <= a.c && j0 + BJ <= b.c) {
+                    const T* ap[BI];
+                    const T* bp[BJ];
+                    T s[BI][BJ];
+                    for (int i = 0; i < BI; ++i) ap[i] = a.col(i0 + i);
+                    for (int j = 0; j < BJ; ++j) bp[j] = b.col(j0 + j);
+                    for (int i = 0; i < BI; ++i)
+                        for (int j = 0; j < BJ; ++j) s[i][j] = c(i0 + i, j0 + j);
+                    dot_tile<T, BI, BJ>(k0, k1, ap, bp, s);
+                    for (int i = 0; i < BI; ++i)
+                        for (int j = 0; j < BJ; ++j) c(i0 + i, j0 + j) = s[i][j];
+                } else {
+                    for (int j = j0; j < std::min(b.c, j0 + BJ); ++j)
+                        for (int i = i0; i < std::min(a.c, i0 + BI); ++i) {
+                            const T* ap[1] = {a.col(i)};
+                            const T* bp[1] = {b.col(j)};
+                            T s[1][1] = {{c(i, j)}};
+                            dot_tile<T, 1, 1>(k0, k1, ap, bp, s);
+                            c(i, j) = s[0][0];
+                        }
+                }
+            }
+    }
     return c;
 }
 
@@ -143,17 +224,46 @@ Mat<T> gemm_nn(const Mat<T>& a, const Mat<T>& b) {
 }
 
 // v -= Q (Q^H v) over the first m columns of q (Eigen: temp = Q*(Q^T v); v -= temp)
+// coef[l] is one ascending-i dot product (8 of them per sweep); temp[i] sums
+// over l ascending, formed for a chunk of rows at a time with l outermost
+// (each temp[i] still adds its terms in ascending l) — bit-identical to the
+// row-at-a-time form, with unit-stride streams through Q.
 template <class T>
 static void project_out(int n, const T* q, int m, T* v) {
     if (m == 0) return;
     std::vector<T> coef(static_cast<size_t>(m));
+    constexpr int BL = 8;
+    const int nb = (m + BL - 1) / BL;
+    const T* vp[1] = {v};
+#pragma omp parallel for schedule(dynamic) if (par_ok(double(n) * m))
+    for (int lb = 0; lb < nb; ++lb) {
+        const int l0 = lb * BL;
+        if (l0 + BL <= m) {
+            const T* qp[BL];
+            T s[BL][1];
+            for (int i = 0; i < BL; ++i) {
+                qp[i] = q + static_cast<size_t>(l0 + i) * n;
+                s[i][0] = T(0);
+            }
+            dot_tile<T, BL, 1>(0, n, qp, vp, s);
+            for (int i = 0; i < BL; ++i) coef[l0 + i] = s[i][0];
+        } else {
+            for (int l = l0; l < m; ++l) coef[l] = dotc(n, q + static_cast<size_t>(l) * n, v);
+        }
+    }
+    constexpr int kChunk = 512;
+    const int nchunks = (n + kChunk - 1) / kChunk;
 #pragma omp parallel for schedule(static) if (par_ok(double(n) * m))
-    for (int l = 0; l < m; ++l) coef[l] = dotc(n, q + static_cast<size_t>(l) * n, v);
-#pragma omp parallel for schedule(static) if (par_ok(double(n) * m))
-    for (int i = 0; i < n; ++i) {
-        T t = T(0);
-        for (int l = 0; l < m; ++l) t += q[static_cast<size_t>(l) * n + i] * coef[l];
-        v[i] -= t;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int i0 = ch * kChunk, i1 = std::min(n, i0 + kChunk);
+        T t[kChunk];
+        for (int i = 0; i < i1 - i0; ++i) t[i] = T(0);
+        for (int l = 0; l < m; ++l) {
+            const T* ql = q + static_cast<size_t>(l) * n + i0;
+            const T cl = coef[l];
+            for (int i = 0; i < i1 - i0; ++i) t[i] += ql[i] * cl;
+        }
+        for (int i = i0; i < i1; ++i) v[i] -= t[i - i0];
     }
 }
 

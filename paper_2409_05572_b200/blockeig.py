@@ -45,7 +45,8 @@ class StrategyConfig(C.Structure):
 
 class SolveExt(C.Structure):
     _fields_ = [("op_mode", C.c_int), ("op_shift", C.c_double), ("which", C.c_int),
-                ("device", C.c_int), ("profile", C.c_int)]
+                ("device", C.c_int), ("profile", C.c_int), ("x0_on_device", C.c_int),
+                ("vectors_device", C.c_void_p)]
 
 
 class IterRecord(C.Structure):
@@ -134,11 +135,16 @@ SYMBOLS = {
     "beig_result_kernel_stats": (C.c_int, [_P, C.c_int, C.POINTER(KernelStat)]),
     "beig_result_diagnostics": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "beig_release_device_cache": (None, []),
+    "beig_harness_project_orthonormalize": (C.c_int, [_DP, C.c_int, C.c_int, _DP, C.c_int, C.c_double, _DP,
+                                                      C.POINTER(C.c_int)]),
+    "beig_harness_hl_trick": (C.c_int, [_DP, C.c_int, C.c_int, _DP, C.c_int, C.c_int, _DP, _DP,
+                                        C.POINTER(C.c_int)]),
 }
 REFERENCE_SYMBOLS = [s for s in SYMBOLS if s not in (
     "beig_matrix_from_csr", "beig_zmatrix_from_csr", "beig_matrix_is_complex",
     "beig_solve_ext_default", "beig_solve_ex", "beig_result_vectors_z", "beig_result_seconds",
-    "beig_result_kernel_stats", "beig_result_diagnostics", "beig_release_device_cache")]
+    "beig_result_kernel_stats", "beig_result_diagnostics", "beig_release_device_cache",
+    "beig_harness_project_orthonormalize", "beig_harness_hl_trick")]
 
 
 class BlockeigError(RuntimeError):
@@ -197,6 +203,28 @@ class Library:
             setattr(e, k, v)
         return e
 
+    # -- test harness (beig_harness_*)
+    def project_orthonormalize(self, w: np.ndarray, q: np.ndarray | None = None, drop: float = 1e-8):
+        w = np.asfortranarray(w, dtype=np.float64)
+        n, a = w.shape
+        q = np.zeros((n, 0)) if q is None else np.asfortranarray(q, dtype=np.float64)
+        out = np.zeros((n, max(a, 1)), order="F")
+        kept = C.c_int()
+        self.check(self.lib.beig_harness_project_orthonormalize(_dptr(w), n, a, _dptr(q) if q.size else None,
+                                                                q.shape[1], drop, _dptr(out), C.byref(kept)))
+        return out[:, :kept.value].copy(), kept.value
+
+    def hl_trick(self, s: np.ndarray, z: np.ndarray, n_now: int, lock: int = 0):
+        s = np.asfortranarray(s, dtype=np.float64)
+        z = np.asfortranarray(z, dtype=np.float64)
+        n, d = s.shape
+        x = np.zeros((n, n_now), order="F")
+        p = np.zeros((n, n_now), order="F")
+        pc = C.c_int()
+        self.check(self.lib.beig_harness_hl_trick(_dptr(s), n, d, _dptr(z), n_now, lock, _dptr(x), _dptr(p),
+                                                  C.byref(pc)))
+        return x, p[:, :pc.value].copy()
+
     # -- matrices
     def gen(self, spec: str) -> "Matrix":
         h = C.c_void_p()
@@ -227,12 +255,19 @@ class Library:
     # -- solving
     def solve(self, a: "Matrix", solver="lobpcg", cfg: SolverConfig | None = None,
               strategy: StrategyConfig | None = None, x0: np.ndarray | None = None,
-              ext: SolveExt | None = None, **cfg_kw) -> "Result":
+              ext: SolveExt | None = None, x0_device: tuple[int, int] | None = None,
+              **cfg_kw) -> "Result":
+        """x0_device = (device pointer, columns): a device-resident column-major
+        block (ext.x0_on_device); ext.vectors_device keeps the result on the device."""
         solver = SOLVERS[solver] if isinstance(solver, str) else solver
         cfg = cfg if cfg is not None else self.solver_config(**cfg_kw)
         strategy = strategy if strategy is not None else self.strategy_config()
         h = C.c_void_p()
-        if x0 is None:
+        if x0_device is not None:
+            if ext is None or not ext.x0_on_device:
+                raise ValueError("x0_device needs ext.x0_on_device = 1")
+            xp, cols = C.cast(C.c_void_p(int(x0_device[0])), _DP), int(x0_device[1])
+        elif x0 is None:
             xp, cols, keep = None, 0, None
         else:
             if np.iscomplexobj(x0):

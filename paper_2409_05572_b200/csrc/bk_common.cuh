@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/bk_kernels.h"
 
 #define BK_RET(expr)                                  \
@@ -13,6 +15,28 @@
     } while (0)
 
 #define BK_LAUNCHED() return static_cast<int>(cudaGetLastError())
+
+namespace bk {
+constexpr int kMaxDevices = 64;
+// Function attributes (dynamic shared memory, cluster size) and occupancy
+// queries are per device: evaluate once per (call site, current device), so a
+// host thread that moves between GPUs configures each of them.
+struct OncePerDevice {
+    std::once_flag flag[kMaxDevices];
+    cudaError_t err[kMaxDevices] = {};
+    template <class F>
+    cudaError_t operator()(F&& f) {
+        int dev = 0;
+        const cudaError_t g = cudaGetDevice(&dev);
+        if (g != cudaSuccess) return g;
+        if (dev < 0 || dev >= kMaxDevices) return f();
+        std::call_once(flag[dev], [&] { err[dev] = f(); });
+        return err[dev];
+    }
+};
+}  // namespace bk
+#define BK_ONCE_PER_DEVICE(expr) \
+    ([&]() -> cudaError_t { static ::bk::OncePerDevice _once; return _once([&]() -> cudaError_t { return (expr); }); }())
 
 namespace bk {
 

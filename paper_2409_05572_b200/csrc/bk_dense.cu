@@ -390,8 +390,8 @@ int gram_launch_v(int n, const double* x, int ldx, int a, const double* y, int l
     constexpr size_t smem = sizeof(double) * ST * TK * ((TM + 4) + (TN + 4));
     auto k16 = gram_kernel<TM, TN, TK, WM, WN, ST, true, SYM>;
     auto k8 = gram_kernel<TM, TN, TK, WM, WN, ST, false, SYM>;
-    static const cudaError_t a1 = prep(k16, smem);
-    static const cudaError_t a2 = prep(k8, smem);
+    const cudaError_t a1 = BK_ONCE_PER_DEVICE(prep(k16, smem));
+    const cudaError_t a2 = BK_ONCE_PER_DEVICE(prep(k8, smem));
     BK_RET(a1);
     BK_RET(a2);
     const int nt = ceil_div(a, TM);
@@ -722,9 +722,9 @@ int gemm_launch_v(int n, const double* x, int ldx, int d, const double* c, int l
     auto k16 = gemm_kernel<TM, TN, TK, WM, WN, ST, true, false>;
     auto k16c = gemm_kernel<TM, TN, TK, WM, WN, ST, true, true>;
     auto k8 = gemm_kernel<TM, TN, TK, WM, WN, ST, false, false>;
-    static const cudaError_t a1 = prep(k16, smem);
-    static const cudaError_t a2 = prep(k8, smem);
-    static const cudaError_t a3 = prep(k16c, smem);
+    const cudaError_t a1 = BK_ONCE_PER_DEVICE(prep(k16, smem));
+    const cudaError_t a2 = BK_ONCE_PER_DEVICE(prep(k8, smem));
+    const cudaError_t a3 = BK_ONCE_PER_DEVICE(prep(k16c, smem));
     BK_RET(a1);
     BK_RET(a2);
     BK_RET(a3);

@@ -335,9 +335,9 @@ int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop
     }
     auto s = static_cast<double*>(work);  // a x a (used when a > kCholSmemMaxA)
     if (a > 4096) return static_cast<int>(cudaErrorInvalidValue);
-    static const cudaError_t attr = cudaFuncSetAttribute(
+    const cudaError_t attr = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(
         chol_drop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        static_cast<int>((kCholSmemMaxA * kCholSmemMaxA + 4 * kCholSmemMaxA) * sizeof(double)));
+        static_cast<int>((kCholSmemMaxA * kCholSmemMaxA + 4 * kCholSmemMaxA) * sizeof(double))));
     BK_RET(attr);
     const size_t small = (3 * static_cast<size_t>(a) + (a + 1) / 2) * sizeof(double);
     const size_t smem = small + (a <= kCholSmemMaxA ? static_cast<size_t>(a) * a * sizeof(double) : 0);
@@ -383,9 +383,9 @@ extern "C" int bk_syev_jacobi_d(int d, double* h, int ldh, double* values, doubl
     double* v = hg + static_cast<size_t>(d) * d;
     const int use_smem = d <= kJacobiSmemMaxD ? 1 : 0;
     const size_t smem = use_smem ? static_cast<size_t>(d) * d * sizeof(double) : 0;
-    static const cudaError_t attr = cudaFuncSetAttribute(
+    const cudaError_t attr = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(
         jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        static_cast<int>(kJacobiSmemMaxD * kJacobiSmemMaxD * sizeof(double)));
+        static_cast<int>(kJacobiSmemMaxD * kJacobiSmemMaxD * sizeof(double))));
     BK_RET(attr);
     jacobi_kernel<<<1, kJacobiThreads, smem, s>>>(d, h, ldh, hg, v, values, z, ldz, info, use_smem);
     BK_LAUNCHED();

@@ -1493,8 +1493,8 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
     group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
     {
         const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 2 * (5 * static_cast<size_t>(d) + (d + 7) / 8));
-        static const cudaError_t ai = cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           static_cast<int>(sizeof(double) * 14 * kSyevMaxD));
+        const cudaError_t ai = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           static_cast<int>(sizeof(double) * 14 * kSyevMaxD)));
         BK_RET(ai);
         invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u);
     }
@@ -1509,8 +1509,8 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
         int smax = n_need < 160 ? n_need : 160;
         while (smax > 0 && static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8 > 28800) --smax;
         const size_t gsm = sizeof(double) * (static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8);
-        static const cudaError_t ag = cudaFuncSetAttribute(group_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           226 * 1024);
+        const cudaError_t ag = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(group_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           226 * 1024));
         BK_RET(ag);
         group_chol_kernel<<<n_need, 1024, gsm, s>>>(n_need, w.gram, w.gstart, w.ngroups, w.m, w.scratch,
                                                     w.ginfo, smax);
@@ -1542,14 +1542,16 @@ int coop_tridiag(int d, const double* h, int ldh, SyevWs& w, cudaStream_t s) {
     sym_copy_kernel<E><<<max(1, min(ceil_div(d * d, 256), 8 * kSMs)), 256, 0, s>>>(
         d, reinterpret_cast<const E*>(h), ldh, reinterpret_cast<E*>(w.za));
     const size_t smem = 3 * static_cast<size_t>(d) * sizeof(E);
-    static const cudaError_t attr = prep_smem(tridiag_coop_kernel<E>, 3 * sizeof(E) * kSyevMaxD);
+    const cudaError_t attr = BK_ONCE_PER_DEVICE(prep_smem(tridiag_coop_kernel<E>, 3 * sizeof(E) * kSyevMaxD));
     BK_RET(attr);
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        BK_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop_kernel<E>, kCoopThreads,
-                                                              3 * sizeof(E) * kSyevMaxD));
-        if (per_sm < 1) return static_cast<int>(cudaErrorLaunchOutOfResources);
-    }
+    static int per_sm_dev[kMaxDevices];  // occupancy is per device
+    int dev = 0;
+    BK_RET(cudaGetDevice(&dev));
+    dev = dev < kMaxDevices ? dev : 0;
+    BK_RET(BK_ONCE_PER_DEVICE(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm_dev[dev], tridiag_coop_kernel<E>, kCoopThreads, 3 * sizeof(E) * kSyevMaxD)));
+    const int per_sm = per_sm_dev[dev];
+    if (per_sm < 1) return static_cast<int>(cudaErrorLaunchOutOfResources);
     int grid = max(1, min(ceil_div(d, kCoopThreads / 32), kSMs));
     grid = min(grid, per_sm * kSMs);
     int dd = d;
@@ -1596,9 +1598,9 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     void* gram_work = static_cast<char*>(work) + total - ((bk_gram_work_bytes(d, d, d) + 255) & ~size_t(255));
     const int mm = d < kTriSmemMaxM + 1 ? d : kTriSmemMaxM + 1;
     const size_t smem = sizeof(double) * (4 * static_cast<size_t>(d) + static_cast<size_t>(mm) * mm);
-    static const cudaError_t attr = cudaFuncSetAttribute(
+    const cudaError_t attr = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(
         tridiag_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        static_cast<int>(sizeof(double) * (4 * kSyevMaxD + (kTriSmemMaxM + 1) * (kTriSmemMaxM + 1))));
+        static_cast<int>(sizeof(double) * (4 * kSyevMaxD + (kTriSmemMaxM + 1) * (kTriSmemMaxM + 1)))));
     BK_RET(attr);
     if (d > kSyevMaxD) return static_cast<int>(cudaErrorInvalidValue);
     if (d == 1) {
@@ -1615,9 +1617,9 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     static const bool force_coop = getenv("BK_SYEV_COOP") != nullptr;  // tuning runs only
     static const bool no_packed = getenv("BK_TRI_NO_PACKED") != nullptr;  // tuning runs only
     if (d <= kPackedUseMaxD && !force_coop && !no_packed) {
-        static const cudaError_t ap = cudaFuncSetAttribute(tridiag_packed_kernel,
+        const cudaError_t ap = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(tridiag_packed_kernel,
                                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                            static_cast<int>(packed_smem_bytes(kPackedMaxD)));
+                                                            static_cast<int>(packed_smem_bytes(kPackedMaxD))));
         BK_RET(ap);
         tridiag_packed_kernel<<<1, kPkThreads, packed_smem_bytes(d), s>>>(d, h, ldh, w.vref, w.tau, w.dg, w.off);
         BK_RET(cudaGetLastError());
@@ -1640,9 +1642,9 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
                             : (tthreads == 256   ? tridiag_cluster1_kernel<256>
                                : tthreads == 128 ? tridiag_cluster1_kernel<128>
                                                  : tridiag_cluster1_kernel<kClThreads>);
-        static const cudaError_t a1 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                            200 * 1024 + 8192);
-        static const cudaError_t a2 = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        const cudaError_t a1 = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            200 * 1024 + 8192));
+        const cudaError_t a2 = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         BK_RET(a1);
         BK_RET(a2);
         cudaLaunchConfig_t cfg = {};
@@ -1682,10 +1684,10 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     } else {
         const size_t bs = sizeof(double) * 8 * static_cast<size_t>(d);
         const int blocks = ceil_div(n_need, 8);
-        static const cudaError_t ab4 = prep_smem(backtr_reg_kernel<4>, sizeof(double) * 8 * kSyevMaxD);
-        static const cudaError_t ab8 = prep_smem(backtr_reg_kernel<8>, sizeof(double) * 8 * kSyevMaxD);
-        static const cudaError_t ab12 = prep_smem(backtr_reg_kernel<12>, sizeof(double) * 8 * kSyevMaxD);
-        static const cudaError_t ab16 = prep_smem(backtr_reg_kernel<16>, sizeof(double) * 8 * kSyevMaxD);
+        const cudaError_t ab4 = BK_ONCE_PER_DEVICE(prep_smem(backtr_reg_kernel<4>, sizeof(double) * 8 * kSyevMaxD));
+        const cudaError_t ab8 = BK_ONCE_PER_DEVICE(prep_smem(backtr_reg_kernel<8>, sizeof(double) * 8 * kSyevMaxD));
+        const cudaError_t ab12 = BK_ONCE_PER_DEVICE(prep_smem(backtr_reg_kernel<12>, sizeof(double) * 8 * kSyevMaxD));
+        const cudaError_t ab16 = BK_ONCE_PER_DEVICE(prep_smem(backtr_reg_kernel<16>, sizeof(double) * 8 * kSyevMaxD));
         BK_RET(ab4);
         BK_RET(ab8);
         BK_RET(ab12);

@@ -16,10 +16,6 @@ struct beig_matrix {
     b2::SparseSym m;
 };
 
-namespace {
-thread_local std::string g_aux_err;
-}
-
 // beig_last_error lives in capi.cpp; errors from here are reported through
 // the same thread-local slot by a small shim exported there.
 extern "C" void bk_internal_set_error(const char* msg);

@@ -30,6 +30,7 @@ namespace b2 {
 namespace {
 
 constexpr double kDropTol = 1e-8;  // kDropTolDefault, proj/src/kernel.hpp:17
+constexpr int kMaxRitzDim = 1200;  // K5 (bk_syev_d / _z) limit, kSyevMaxD in bk_syev.cu
 
 int round8(int x) { return (x + 7) & ~7; }
 
@@ -100,10 +101,18 @@ struct Stagnation {
 };
 
 class Engine {
+    // first member: the device is current before any member that creates
+    // device objects (the event pool) is initialised
+    int cfg_dev_;
+    static int set_device(int dev) {
+        BKC(cudaSetDevice(dev));
+        return dev;
+    }
+
 public:
     Engine(const SparseSym& a, const SolverConfig& cfg, SolverKind kind)
-        : a_(a), cfg_(cfg), kind_(kind), n_(a.rows()), cw_(a.is_complex() ? 2 : 1), rng_(cfg.seed) {
-        BKC(cudaSetDevice(cfg.device));
+        : cfg_dev_(set_device(cfg.device)), a_(a), cfg_(cfg), kind_(kind), n_(a.rows()), cw_(a.is_complex() ? 2 : 1),
+          rng_(cfg.seed) {
         csr_ = &a.device_csr(cfg.device, cfg.largest);
         BKC(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
         const int n_ex = cfg.n_ex, n_es = cfg.n_es;
@@ -178,6 +187,27 @@ public:
     SolveOutput run(const double* x0, int x0_cols);
     void set_strategy(const StrategyConfig& s) { strategy_ = s; }
 
+    // ---- test harness (bk_harness_*): one K4 or HL-trick call through the
+    // solvers' own code, on host column-major blocks
+    int harness_proj_ortho(const double* w, int a, const double* q, int m, double* out) {
+        upload_colmajor(w, a, T1());
+        if (m > 0) upload_colmajor(q, m, S(0));
+        const int kept = proj_ortho(n_, T1(), a, S(0), m, S(0).at(m));
+        download_colmajor(S(0).at(m), kept, out);
+        return kept;
+    }
+    int harness_hl(const double* s, int d, const double* z, int n_now, int lock, double* x, double* p) {
+        upload_colmajor(s, d, S(0));
+        const size_t zb = static_cast<size_t>(d) * d * sizeof(double);
+        DevMem zcm(zb);
+        BKC(cudaMemcpyAsync(zcm.d(), z, zb, cudaMemcpyHostToDevice, stream_));
+        BKC(bk_cm_to_rm_d(d, d, zcm.d(), d, Z_.d(), ldH_, st()));
+        const int pk = hl_lift(S(0), d, n_now, lock, S(1), -1);
+        download_colmajor(S(1), n_now, x);
+        download_colmajor(S(1).at(n_now), pk, p);
+        return pk;
+    }
+
 private:
     StrategyConfig strategy_;
     // ---------------------------------------------------------------- primitives
@@ -224,11 +254,15 @@ private:
     };
     // timing events are pooled per host thread across solves (a config-2 solve
     // records ~30k of them)
-    static std::vector<cudaEvent_t>& event_pool() {
-        static thread_local auto* v = new std::vector<cudaEvent_t>;
-        return *v;
+    // (per host thread AND device: an event belongs to the device it was created on)
+    static constexpr int kMaxDev = 64;
+    static std::vector<cudaEvent_t>& event_pool(int dev) {
+        static thread_local std::vector<cudaEvent_t>* v[kMaxDev] = {};
+        auto& p = v[dev % kMaxDev];
+        if (!p) p = new std::vector<cudaEvent_t>;
+        return *p;
     }
-    std::vector<cudaEvent_t>& ev_pool_ = event_pool();
+    std::vector<cudaEvent_t>& ev_pool_ = event_pool(cfg_dev_);
     std::vector<Pending> pending_;
     KernelStat kstats_[K_CLASSES];
     cudaEvent_t take_event() {
@@ -408,9 +442,12 @@ private:
         std::memcpy(dst, src, std::min(bytes, part));
         for (auto& x : th) x.join();
     }
-    static PinnedChunks& chunks() {
-        static thread_local PinnedChunks* c = new PinnedChunks;
-        return *c;
+    // per host thread and device (the chunk events belong to one device)
+    PinnedChunks& chunks() {
+        static thread_local PinnedChunks* c[kMaxDev] = {};
+        auto& p = c[cfg_.device % kMaxDev];
+        if (!p) p = new PinnedChunks;
+        return *p;
     }
     template <class Fill>
     void chunked_h2d(double* dst, size_t count, Fill fill) {
@@ -456,6 +493,15 @@ private:
         if (cw_ == 1) BKC(bk_cm_to_rm_d(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
         else BKC(bk_cm_to_rm_z(n_, cols, stage_.d(), n_, dst.p, dst.ld, st()));
         sync();  // the host buffer may be released by the caller
+    }
+
+    void download_colmajor(Blk src, int cols, double* h) {
+        if (cols <= 0) return;
+        const size_t count = static_cast<size_t>(n_) * cols;
+        DevMem cm(count * sizeof(double));
+        BKC(bk_rm_to_cm_d(n_, cols, src.p, src.ld, cm.d(), n_, st()));
+        BKC(cudaMemcpyAsync(h, cm.d(), count * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        sync();
     }
 
     // K4: project w (rows x a, clobbered) against q (rows x m), orthonormalise
@@ -624,7 +670,7 @@ private:
                 prof_end(tg, K_GRAM, 16.0 * n_ * 2 * d, 4.0 * n_ * d * (d + 1.0));
             }
         }
-        if (d > 1200) throw std::runtime_error("Rayleigh-Ritz dimension exceeds the device eigensolver limit (1200)");
+        if (d > kMaxRitzDim) throw std::runtime_error("Rayleigh-Ritz dimension exceeds the device eigensolver limit");
         int* info = INFO_.as<int>() + 8;
         auto ts = prof_begin();
         if (cw_ == 1)
@@ -645,6 +691,23 @@ private:
     // out[:, 0:k] = s[:, 0:d] Z[:, 0:k]
     void lift(Blk s, int d, const double* z, int ldz, int k, Blk out) {
         gemm(n_, s.p, s.ld, d, z, ldz, k, 1.0, 0.0, out.p, out.ld);
+    }
+    // HL trick (solvers.cpp:187-196, meter :382) in coefficient space:
+    // ZC = [Z(:, :n_now) | orth(Zp)], Zp = Z(:, lock:n_now) with rows < n_now
+    // zeroed (a d-row K4 call), then one fused lift out = [X, P] = S ZC.
+    // Returns |P|.  slot >= 0: speculative K4 (see proj_ortho).
+    int hl_lift(Blk s, int ds, int n_now, int lock, Blk out, int slot) {
+        const Blk zc = B(ZC_.d(), ldH_), cz = B(CZ_.d(), ldH_), z = B(Z_.d(), ldH_);
+        const int ahl = n_now - lock;
+        copy(ds, z, n_now, zc);
+        copy(ds, z.at(lock), ahl, cz);
+        zero_rows(cz, ahl, 0, n_now);
+        mark(0);
+        const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now), slot);
+        mark(4);
+        meter_.w.ortho_flops += static_cast<int64_t>(ds) * (n_now - lock) * (2 * n_now + (n_now - lock));
+        lift(s, ds, zc.p, zc.ld, n_now + pk, out);
+        return pk;
     }
 
     struct Rep {
@@ -737,11 +800,15 @@ private:
         out_.status = status;
         out_.values.resize(n_ev);
         BKC(cudaMemcpyAsync(out_.values.data(), VALS_.d(), n_ev * sizeof(double), cudaMemcpyDeviceToHost, stream_));
-        if (cw_ == 1) BKC(bk_rm_to_cm_d(n_, n_ev, v.p, v.ld, PT_.d(), n_, st()));
-        else BKC(bk_rm_to_cm_z(n_, n_ev, v.p, v.ld, PT_.d(), n_, st()));
+        // beig_solve_ext.vectors_device: the vectors stay on the device
+        double* cm = cfg_.vectors_device ? cfg_.vectors_device : PT_.d();
+        if (cw_ == 1) BKC(bk_rm_to_cm_d(n_, n_ev, v.p, v.ld, cm, n_, st()));
+        else BKC(bk_rm_to_cm_z(n_, n_ev, v.p, v.ld, cm, n_, st()));
         out_.complex_vectors = cw_ == 2;
-        out_.vectors.resize(static_cast<size_t>(n_) * n_ev * cw_);
-        chunked_d2h(out_.vectors.data(), PT_.d(), out_.vectors.size());
+        if (!cfg_.vectors_device) {
+            out_.vectors.resize(static_cast<size_t>(n_) * n_ev * cw_);
+            chunked_d2h(out_.vectors.data(), PT_.d(), out_.vectors.size());
+        }
         sync();
         if (cfg_.largest)
             for (auto& x : out_.values) x = -x;
@@ -859,7 +926,14 @@ int Engine::initial_block(const double* x0, int x0_cols, Blk dst) {
     const int n_ex = cfg_.n_ex;
     if (x0 != nullptr) {
         if (x0_cols != n_ex) throw std::invalid_argument("initial block must be n x n_ex");
-        upload_colmajor(x0, n_ex, T1());
+        if (cfg_.x0_on_device) {
+            // device-resident x0 (beig_solve_ext.x0_on_device): transposed in place
+            // into the row-major block, no host staging
+            if (cw_ == 1) BKC(bk_cm_to_rm_d(n_, n_ex, x0, n_, T1().p, T1().ld, st()));
+            else BKC(bk_cm_to_rm_z(n_, n_ex, x0, n_, T1().p, T1().ld, st()));
+        } else {
+            upload_colmajor(x0, n_ex, T1());
+        }
     } else {
         random_block(n_ex, T1());
     }
@@ -1107,7 +1181,6 @@ void Engine::solve_lobpcg() {
     int n_now = n_ex, np = 0, prev_lock = 0;
     BlockSizer sizer(strategy_);
     const Blk xd = B(XD_.d(), ldT_);
-    const Blk zc = B(ZC_.d(), ldH_), cz = B(CZ_.d(), ldH_), z = B(Z_.d(), ldH_);
     static const bool spec_off = std::getenv("BLOCKEIG_NO_SPEC") != nullptr;
 
     // everything after the decision; false when the solve ended inside
@@ -1176,18 +1249,8 @@ void Engine::solve_lobpcg() {
         mark(0);
         rayleigh_ritz(s, ds, n_old, n_now);
         mark(3);
-        // HL trick (solvers.cpp:187-196) in coefficient space:
-        // ZC = [Z(:, :n_now) | orth(Zp)], Zp = Z(:, lock:n_now) with rows < n_now zeroed
-        const int ahl = n_now - lock;  // n_now is post-expansion here
-        copy(ds, z, n_now, zc);
-        copy(ds, z.at(lock), ahl, cz);
-        zero_rows(cz, ahl, 0, n_now);
-        mark(0);
-        const int pk = proj_ortho(ds, cz, ahl, zc, n_now, zc.at(n_now), spec ? 1 : -1);
-        mark(4);
-        meter_.w.ortho_flops += static_cast<int64_t>(ds) * (n_now - lock) * (2 * n_now + (n_now - lock));
-        // [X, P] = S ZC
-        lift(s, ds, zc.p, zc.ld, n_now + pk, S(1 - cur_));
+        // HL trick (solvers.cpp:187-196): [X, P] = S [Z1, orth(Zp)] (n_now is post-expansion here)
+        const int pk = hl_lift(s, ds, n_now, lock, S(1 - cur_), spec ? 1 : -1);
         mark(5);
         cur_ ^= 1;
         np = pk;
@@ -1422,7 +1485,58 @@ SolverConfig resolve_config(SolverConfig cfg, SolverKind kind, const StrategyCon
     if (cfg.op_shifted && kind != SolverKind::si)
         throw std::invalid_argument("the shifted operator mode applies to the SI solver only");
     validate_strategy(s);
+    // extension check (no reference counterpart: Eigen has no size limit): the
+    // Rayleigh-Ritz dimension is at most n_ex (SI, TraceMIN), 2 n_ex (SD) or
+    // 3 n_ex (LOBPCG, expansion iterations included), capped by n; the device
+    // eigensolver K5 handles d <= kMaxRitzDim, so larger problems are refused
+    // here, before any device work, instead of failing mid-solve
+    {
+        const int64_t f = kind == SolverKind::lobpcg ? 3 : kind == SolverKind::sd ? 2 : 1;
+        const int64_t dmax = std::min<int64_t>(n, f * cfg.n_ex);
+        if (dmax > kMaxRitzDim)
+            throw std::invalid_argument("Rayleigh-Ritz dimension " + std::to_string(dmax) +
+                                        " exceeds the device eigensolver limit " + std::to_string(kMaxRitzDim) +
+                                        " (LOBPCG: 3 n_ex, SD: 2 n_ex, SI/TraceMIN: n_ex)");
+    }
     return cfg;
+}
+
+// Harness engines: identity matrix of order n (only the block machinery is
+// used), widths sized for the call.
+namespace {
+SparseSym harness_identity(int n) {
+    std::vector<int64_t> rp(static_cast<size_t>(n) + 1);
+    std::vector<int> col(n);
+    for (int i = 0; i <= n; ++i) rp[i] = i;
+    for (int i = 0; i < n; ++i) col[i] = i;
+    return SparseSym(n, std::move(rp), std::move(col), std::vector<double>(n, 1.0));
+}
+SolverConfig harness_cfg(int width, int device) {
+    SolverConfig c;
+    c.n_ev = 1;
+    c.n_ex = std::max(width, 2);
+    c.n_es = c.n_ex - 1;
+    c.device = device;
+    return c;
+}
+}  // namespace
+
+int harness_project_orthonormalize(const double* w, int n, int a, const double* q, int m, double* out, int device) {
+    if (n < 1 || a < 0 || m < 0 || a + m > n) throw std::invalid_argument("harness: bad block sizes");
+    const SparseSym id = harness_identity(n);
+    Engine e(id, harness_cfg(std::max(a, m), device), SolverKind::lobpcg);
+    return e.harness_proj_ortho(w, a, q, m, out);
+}
+
+int harness_hl_trick(const double* s, int n, int d, const double* z, int n_now, int lock, double* x, double* p,
+                     int device) {
+    // reference hl_trick argument checks (solvers.cpp:187-190)
+    if (n_now < 1 || n_now > d) throw std::invalid_argument("hl_trick: bad n_now");
+    lock = std::clamp(lock, 0, n_now);
+    if (d > n) throw std::invalid_argument("harness: d exceeds n");
+    const SparseSym id = harness_identity(n);
+    Engine e(id, harness_cfg(d, device), SolverKind::lobpcg);
+    return e.harness_hl(s, d, z, n_now, lock, x, p);
 }
 
 SolveOutput solve(SolverKind kind, const SparseSym& a, const SolverConfig& cfg_in, const StrategyConfig& s,

@@ -220,6 +220,8 @@ struct SolverConfig {
     bool largest = false;
     int device = 0;
     bool profile = false;
+    bool x0_on_device = false;        // x0 is a device pointer (column-major)
+    double* vectors_device = nullptr;  // result vectors stay on the device (column-major)
 };
 
 enum KernelClass { K_SPMM = 0, K_GRAM, K_GEMM, K_SYEV, K_CHOL, K_RESID, K_OTHER, K_CLASSES };
@@ -261,5 +263,10 @@ struct SolveOutput {
 SolverConfig resolve_config(SolverConfig cfg, SolverKind kind, const StrategyConfig& s, int n);
 SolveOutput solve(SolverKind kind, const SparseSym& a, const SolverConfig& cfg,
                   const StrategyConfig& s, const double* x0_colmajor, int x0_cols);
+
+// test harness (beig_harness_*): one K4 / HL-trick call through the solver code
+int harness_project_orthonormalize(const double* w, int n, int a, const double* q, int m, double* out, int device);
+int harness_hl_trick(const double* s, int n, int d, const double* z, int n_now, int lock, double* x, double* p,
+                     int device);
 
 }  // namespace b2

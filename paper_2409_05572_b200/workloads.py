@@ -260,3 +260,27 @@ def lap3d_eigs(m, k):
     a = 2 - 2 * np.cos(np.arange(1, m + 1) * np.pi / (m + 1))
     s = (a[:, None, None] + a[None, :, None] + a[None, None, :]).ravel()
     return np.sort(s)[:k]
+
+
+def magnetic_eigs(side=1024, phi=1.0 / 64, k=256):
+    """Closed form for config 5 (SURVEY.md §8c plan item 3, Harper-chain
+    reduction).  The y-link phase depends on x only, so a Fourier transform along
+    the periodic y direction (momentum q = 2 pi m / side) splits H into `side`
+    periodic chains along x with H_q = 4 - (hops to x +- 1) - 2 cos(q + 2 pi phi x).
+    Shifting x by one maps q to q + 2 pi phi, i.e. m to m + phi*side, so chains
+    whose m differ by a multiple of phi*side are unitarily equivalent: phi*side
+    distinct chains are diagonalised, each spectrum counted side/(phi*side) times.
+    Checked against a dense eigensolve at side 64 (tests/test_workloads_cpu.py)."""
+    step = round(phi * side)  # m -> m + step under x -> x + 1
+    if step < 1 or abs(phi * side - step) > 1e-12 or side % step:
+        step = side  # no equivalence to use: every chain
+    mult = side // step
+    x = np.arange(side)
+    vals = []
+    for m in range(step):
+        q = 2 * np.pi * m / side
+        h = np.diag(4.0 - 2.0 * np.cos(q + 2 * np.pi * phi * x))
+        h[x, (x + 1) % side] -= 1.0
+        h[(x + 1) % side, x] -= 1.0
+        vals.append(np.repeat(np.linalg.eigvalsh(h)[:k], mult))
+    return np.sort(np.concatenate(vals))[:k]

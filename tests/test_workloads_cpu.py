@@ -83,3 +83,16 @@ def test_config5_hermitian_and_band():
     assert np.ptp(e[:64]) < 1e-3 and e[64] - e[63] > 0.1
     w = W.config5(x0=False)
     assert (w.n, w.nnz_full) == (1048576, 5242880)
+
+
+def test_magnetic_closed_form_matches_dense():
+    """Config 5's Harper-chain closed form (the bench's accuracy check) against a
+    dense eigensolve of the same generator at side 64."""
+    side = 64
+    rp, c, v = W.magnetic(side)
+    a = W.full_from_lower(side * side, rp, c, v).toarray()
+    exact = np.linalg.eigvalsh(a)[:40]
+    np.testing.assert_allclose(W.magnetic_eigs(side, 1 / 64, 40), exact, rtol=0, atol=1e-12)
+    # full size: the lowest Landau band (SURVEY B4) is 0.0969748 wide to ~1e-14
+    full = W.magnetic_eigs(1024, 1 / 64, 256)
+    assert abs(full[0] - 0.0969747894970) < 1e-12 and full[-1] - full[0] < 1e-13
