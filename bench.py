@@ -56,7 +56,7 @@ def make_workload(args, x0=True):
     if c == "5":
         side = args.side or 1024
         # scaled-down lattices (tests) keep the widths when n allows
-        nev, n_ex = (256, 384) if side * side >= 4 * 1152 else (16, 24)
+        nev, n_ex = (256, 384) if side * side >= 3 * 384 else (16, 24)
         w = W.config5(side=side, nev=nev, n_ex=n_ex, x0=x0)
         ref = W.magnetic_eigs(side, 1 / 64, nev)
         meta = {"nev": nev, "n_ex": n_ex, "n_es": max(nev, min(nev + 5, n_ex - 1)),

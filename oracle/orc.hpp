@@ -122,6 +122,10 @@ struct Report {
     std::vector<double> per_pair;
     double overall = 0;
     int converged = 0;
+    // decision margins (diagnostic, not in the reference): per_pair/tol of the
+    // last pair inside the converged prefix and of the first pair outside it
+    // (NaN when there is none)
+    double lo = 0, hi = 0;
 };
 template <class T>
 Report assess_convergence(double norm_a, const Ritz<T>& rz, const Mat<T>& r, int n_ev, double tol);
@@ -143,6 +147,10 @@ struct StratState {
     int last_expand_iter = -1;
     bool have_cmax = false;
     double c_max = 0.0;
+    // decision margins of the last decide() (diagnostic; NaN when not evaluated):
+    // r_now / r_warm of the warm-up shrink test, and the slope test's
+    // (c_max - mu c) / (mu c) (c > 0) or c_max (c <= 0)
+    double m_warm = 0, m_slope = 0;
 };
 double slope(const std::vector<double>& lr);
 double slope_avg(const std::vector<double>& lr, int j_p);
@@ -187,6 +195,7 @@ struct Result {
     std::vector<double> values;
     Mat<T> vectors;
     std::vector<Record> history;
+    std::vector<double> margins;  // 4 per record: rep.lo, rep.hi, st.m_warm, st.m_slope
     int iterations = 0;
     Work work;
     int64_t rr_flops = 0;

@@ -323,6 +323,14 @@ int beig_result_history(const beig_result* r, beig_iter_record* out, int cap) {
     return n;
 }
 
+int beig_result_margins(const beig_result* r, double* out, int cap_records) {
+    if (!r || !out || cap_records < 0) return 0;
+    const auto& m = r->is_complex ? r->rz.margins : r->r.margins;
+    const int n = std::min<int>(cap_records, static_cast<int>(m.size() / 4));
+    std::copy(m.begin(), m.begin() + 4 * static_cast<size_t>(n), out);
+    return n;
+}
+
 int beig_result_work(const beig_result* r, beig_work_summary* out) {
     if (!r || !out) return invalid("beig_result_work: null argument");
     const auto& w = r->work();

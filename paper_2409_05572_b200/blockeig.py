@@ -135,6 +135,7 @@ SYMBOLS = {
     "beig_result_kernel_stats": (C.c_int, [_P, C.c_int, C.POINTER(KernelStat)]),
     "beig_result_diagnostics": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "beig_release_device_cache": (None, []),
+    "beig_result_margins": (C.c_int, [_P, _DP, C.c_int]),
     "beig_harness_project_orthonormalize": (C.c_int, [_DP, C.c_int, C.c_int, _DP, C.c_int, C.c_double, _DP,
                                                       C.POINTER(C.c_int)]),
     "beig_harness_hl_trick": (C.c_int, [_DP, C.c_int, C.c_int, _DP, C.c_int, C.c_int, _DP, _DP,
@@ -144,7 +145,7 @@ REFERENCE_SYMBOLS = [s for s in SYMBOLS if s not in (
     "beig_matrix_from_csr", "beig_zmatrix_from_csr", "beig_matrix_is_complex",
     "beig_solve_ext_default", "beig_solve_ex", "beig_result_vectors_z", "beig_result_seconds",
     "beig_result_kernel_stats", "beig_result_diagnostics", "beig_release_device_cache",
-    "beig_harness_project_orthonormalize", "beig_harness_hl_trick")]
+    "beig_harness_project_orthonormalize", "beig_harness_hl_trick", "beig_result_margins")]
 
 
 class BlockeigError(RuntimeError):
@@ -393,6 +394,14 @@ class Result:
         arr = (IterRecord * max(ln, 1))()
         got = self.L.lib.beig_result_history(self.h, arr, ln)
         return [{f: getattr(arr[i], f) for f, _ in IterRecord._fields_} for i in range(got)]
+
+    @property
+    def margins(self) -> np.ndarray:
+        """records x 4: [lo, hi, warm, slope] decision margins (beig_result_margins)"""
+        ln = self.L.lib.beig_result_history_len(self.h)
+        out = np.full(4 * max(ln, 1), np.nan)
+        got = self.L.lib.beig_result_margins(self.h, _dptr(out), ln)
+        return out[: 4 * got].reshape(got, 4)
 
     def kernel_stats(self) -> dict:
         out = {}

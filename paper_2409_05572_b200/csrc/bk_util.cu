@@ -167,6 +167,16 @@ __global__ void __launch_bounds__(1024) convergence_kernel(int k, const double* 
         rec[0] = s_max[0];
         rec[1] = static_cast<double>(s_first[0]);
         rec[2] = static_cast<double>(s_bad[0]);
+        // decision margins: per_pair of the last pair inside the converged
+        // prefix and of the first pair outside it (-1: none), same formula
+        const int f = s_first[0];
+        auto pp_at = [&](int i) {
+            const double vn = sqrt(vn2[i]);
+            const double denom = norm_a * vn + vn * fabs(lambda[i]);
+            return denom > 0.0 ? sqrt(rn2[i]) / denom : sqrt(rn2[i]);
+        };
+        rec[3] = f > 0 ? pp_at(f - 1) : -1.0;
+        rec[4] = f < k ? pp_at(f) : -1.0;
     }
 }
 

@@ -30,7 +30,8 @@ namespace b2 {
 namespace {
 
 constexpr double kDropTol = 1e-8;  // kDropTolDefault, proj/src/kernel.hpp:17
-constexpr int kMaxRitzDim = 1200;  // K5 (bk_syev_d / _z) limit, kSyevMaxD in bk_syev.cu
+constexpr int kMaxRitzDim = 1200;
+constexpr double kNaN = std::numeric_limits<double>::quiet_NaN();  // K5 (bk_syev_d / _z) limit, kSyevMaxD in bk_syev.cu
 
 int round8(int x) { return (x + 7) & ~7; }
 
@@ -58,10 +59,10 @@ thread_local double g_host_call_s = 0.0;  // BLOCKEIG_TIMING: host time inside C
 
 // pinned host staging for the per-iteration record and small infos
 struct Pinned {
-    double* rec = nullptr;  // 4 doubles
+    double* rec = nullptr;  // 8 doubles
     int* info = nullptr;    // 32 ints: [0..15] synchronous infos, [16..] speculative K4 slots
     Pinned() {
-        BKC(cudaMallocHost(reinterpret_cast<void**>(&rec), 4 * sizeof(double)));
+        BKC(cudaMallocHost(reinterpret_cast<void**>(&rec), 8 * sizeof(double)));
         BKC(cudaMallocHost(reinterpret_cast<void**>(&info), 32 * sizeof(int)));
     }
     ~Pinned() {
@@ -714,6 +715,14 @@ private:
         double overall;
         int converged;
         bool nonfinite;
+        // decision margins (beig_result_margins): per_pair/tol of the last pair
+        // inside / first pair outside the converged prefix, and the strategy's
+        // warm-up and slope margins (NaN where a test did not run)
+        double lo = kNaN, hi = kNaN, warm = kNaN, slope = kNaN;
+        void note(const BlockSizer& s) {
+            warm = s.warm_margin();
+            slope = s.slope_margin();
+        }
     };
     // AV into AS[:, 0:k], R = AV - V diag(VALS) into R, record read back
     // (residual_block + assess_convergence, rr.cpp:16-38)
@@ -760,15 +769,18 @@ private:
         double* vn2 = SMALL_.d() + dcap_ + tcap_;
         auto tr = prof_begin();
         residual_kernel(v, k, VALS_.d());
-        double* rec = SMALL_.d() + 2 * (dcap_ + tcap_);
+        double* rec = SMALL_.d() + 6 * (dcap_ + tcap_);  // 5 doubles (8 dc allocated)
         BKC(bk_convergence_d(k, rn2, vn2, VALS_.d(), norm_a_, n_ev, cfg_.tol, nullptr, rec, st()));
         prof_end(tr, K_RESID, 24.0 * cw_ * n_ * k, 6.0 * cw_ * n_ * k);
-        BKC(cudaMemcpyAsync(pin_.rec, rec, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        BKC(cudaMemcpyAsync(pin_.rec, rec, 5 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         sync();
         const bool bad = pin_.rec[2] != 0.0;
         if (!(bad && tolerate_nonfinite)) check_syev();
         if (bad && !tolerate_nonfinite) throw std::runtime_error("non-finite residual or Ritz value");
-        return {pin_.rec[0], static_cast<int>(pin_.rec[1]), bad};
+        Rep rep{pin_.rec[0], static_cast<int>(pin_.rec[1]), bad};
+        rep.lo = pin_.rec[3] >= 0.0 ? pin_.rec[3] / cfg_.tol : kNaN;
+        rep.hi = pin_.rec[4] >= 0.0 ? pin_.rec[4] / cfg_.tol : kNaN;
+        return rep;
     }
 
     // y = op(x): shifted operator c x - M x (extension) or shift-and-invert
@@ -789,10 +801,16 @@ private:
     }
     void factor_shift_invert();
 
-    void push(int j, double overall, int n_now, Event ev, int lock) {
-        Record r{j, overall, n_now, ev, lock, meter_.w};
+    template <class R>
+    void push(int j, const R& rep, int n_now, Event ev, int lock) {
+        Record r{j, rep.overall, n_now, ev, lock, meter_.w};
         r.work.rr_dim = meter_.iter_rr_dim;
         out_.history.push_back(r);
+        out_.margins.insert(out_.margins.end(), {rep.lo, rep.hi, rep.warm, rep.slope});
+    }
+    void truncate_history(size_t records) {
+        out_.history.resize(records);
+        out_.margins.resize(4 * records);
     }
     void finish(Status status, Blk v, int n_ev) {
         sync();
@@ -975,7 +993,7 @@ void Engine::solve_si() {
             n_now = n_es;
             ev = Event::shrink;
         }
-        push(j, rep.overall, n_now, ev, 0);
+        push(j, rep, n_now, ev, 0);
     };
     struct Snap {
         int j, cur, n_now, xd_cols, ycols;
@@ -997,7 +1015,7 @@ void Engine::solve_si() {
         n_now = snap.n_now;
         xd_cols_ = snap.xd_cols;
         meter_ = snap.meter;
-        out_.history.resize(snap.hist);
+        truncate_history(snap.hist);
         tail(snap.j, snap.rep, snap.d, snap.ycols, snap.ev, false);
         return true;
     };
@@ -1010,14 +1028,15 @@ void Engine::solve_si() {
         }
         const Blk v = S(cur_);
         if (rep.converged >= n_ev) {
-            push(j, rep.overall, n_now, Event::none, 0);
+            push(j, rep, n_now, Event::none, 0);
             return finish(Status::converged, v, n_ev);
         }
         if (guard.update(j, rep.overall)) {
-            push(j, rep.overall, n_now, Event::none, 0);
+            push(j, rep, n_now, Event::none, 0);
             return finish(Status::stagnated, v, n_ev);
         }
         const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        rep.note(sizer);
         meter_.w.solve_cols += n_now;
         apply_op(v, n_now, AS(), true, T1());
         if (cfg_.expand == ExpandMode::powered && xd_cols_ > 0) {
@@ -1091,7 +1110,7 @@ void Engine::solve_sd() {
         meter_.proj_ortho(n_, n_old, xb);
         const int kw = proj_ortho(n_, T1(), n_old, v, xb, v.at(xb), spec ? 0 : -1);
         if (kw == 0) {
-            push(j, rep.overall, n_now, ev, 0);
+            push(j, rep, n_now, ev, 0);
             finish(Status::stagnated, v, n_ev);
             return false;
         }
@@ -1105,7 +1124,7 @@ void Engine::solve_sd() {
             n_now = n_es;
             ev = Event::shrink;
         }
-        push(j, rep.overall, n_now, ev, 0);
+        push(j, rep, n_now, ev, 0);
         return true;
     };
     struct Snap {
@@ -1127,7 +1146,7 @@ void Engine::solve_sd() {
         n_now = snap.n_now;
         xd_cols_ = snap.xd_cols;
         meter_ = snap.meter;
-        out_.history.resize(snap.hist);
+        truncate_history(snap.hist);
         restore_residual(S(cur_), n_now);  // R, AX of the redone iteration
         return tail(snap.j, snap.rep, snap.d, false) ? 1 : -1;
     };
@@ -1141,10 +1160,11 @@ void Engine::solve_sd() {
             rep = residual(S(cur_), n_now, n_ev, false);
         }
         if (rep.converged >= n_ev) {
-            push(j, rep.overall, n_now, Event::none, 0);
+            push(j, rep, n_now, Event::none, 0);
             return finish(Status::converged, S(cur_), n_ev);
         }
         const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        rep.note(sizer);
         const bool spec = !spec_off && d != Decision::expand && spec_cooldown_ == 0;
         if (spec_cooldown_ > 0) --spec_cooldown_;
         if (spec) {
@@ -1194,7 +1214,7 @@ void Engine::solve_lobpcg() {
         const int kw = proj_ortho(n_, T1().at(lock), active, s, m, s.at(m), spec ? 0 : -1, w_norms() + lock);
         mark(2);
         if (kw == 0) {
-            push(j, rep.overall, n_now, Event::none, lock);
+            push(j, rep, n_now, Event::none, lock);
             finish(Status::stagnated, s, n_ev);
             return false;
         }
@@ -1267,7 +1287,7 @@ void Engine::solve_lobpcg() {
             ev = Event::shrink;
         }
         if (ev == Event::none && lock > prev_lock) ev = Event::lock;
-        push(j, rep.overall, n_now, ev, lock);
+        push(j, rep, n_now, ev, lock);
         mark(6);
         prev_lock = lock;
         return true;
@@ -1296,7 +1316,7 @@ void Engine::solve_lobpcg() {
         prev_lock = snap.prev_lock;
         xd_cols_ = snap.xd_cols;
         meter_ = snap.meter;
-        out_.history.resize(snap.hist);
+        truncate_history(snap.hist);
         restore_residual(S(cur_), n_now);  // R, AX of the redone iteration
         return tail(snap.j, snap.rep, snap.lock, snap.d, false) ? 1 : -1;
     };
@@ -1314,10 +1334,11 @@ void Engine::solve_lobpcg() {
         Blk s = S(cur_);
         const int lock = std::min(rep.converged, n_now - 1);
         if (rep.converged >= n_ev) {
-            push(j, rep.overall, n_now, Event::none, lock);
+            push(j, rep, n_now, Event::none, lock);
             return finish(Status::converged, s, n_ev);
         }
         const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        rep.note(sizer);
         // soft locking: P loses its leading (lock - prev_lock) columns
         if (lock > prev_lock && np > 0) {
             const int drop = std::min(lock - prev_lock, np);
@@ -1363,12 +1384,13 @@ void Engine::solve_tracemin() {
     for (int j = 1; j <= cfg_.max_iters; ++j) {
         meter_.begin_iteration();
         const Blk v = S(cur_);
-        const Rep rep = residual(v, n_now, n_ev);
+        Rep rep = residual(v, n_now, n_ev);
         if (rep.converged >= n_ev) {
-            push(j, rep.overall, n_now, Event::none, 0);
+            push(j, rep, n_now, Event::none, 0);
             return finish(Status::converged, v, n_ev);
         }
         const Decision d = sizer.step(rep.overall, n_now, n_es, n_ex);
+        rep.note(sizer);
         const int k = n_now;
         // project(u) = u - V (V^T u), in place
         auto project = [&](Blk u) {
@@ -1443,7 +1465,7 @@ void Engine::solve_tracemin() {
             n_now = n_es;
             ev = Event::shrink;
         }
-        push(j, rep.overall, n_now, ev, 0);
+        push(j, rep, n_now, ev, 0);
     }
     finish(Status::max_iters, S(cur_), n_ev);
 }

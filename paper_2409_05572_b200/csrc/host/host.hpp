@@ -186,8 +186,14 @@ public:
     double c_max() const { return c_max_; }
     // enter the post-warm-up state (reference tests' shrunken_state(), test_strategy.cpp:15-20)
     void mark_warmed() { warmed_ = true; }
+    // decision margins of the last step (NaN when the test did not run):
+    // r / r_warm of the warm-up shrink test; (c_max - mu c) / (mu c) for c > 0,
+    // else c_max, of the slope test (strategy.cpp:49,85)
+    double warm_margin() const { return m_warm_; }
+    double slope_margin() const { return m_slope_; }
 
 private:
+    double m_warm_ = 0.0, m_slope_ = 0.0;
     StrategyConfig c_;
     int j_ = 0;
     std::vector<double> lg_;
@@ -250,6 +256,7 @@ struct SolveOutput {
     std::vector<double, NoInitAlloc<double>> vectors;
     bool complex_vectors = false;
     std::vector<Record> history;
+    std::vector<double> margins;  // 4 per record (beig_result_margins)
     int iterations = 0;
     Work work;
     int64_t rr_flops = 0;

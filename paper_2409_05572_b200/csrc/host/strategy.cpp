@@ -5,6 +5,7 @@
 // implementation, not the paper's printed j_l = j_e.
 #include <algorithm>
 #include <cmath>
+#include <limits>
 
 #include "host.hpp"
 
@@ -20,6 +21,7 @@ void validate_strategy(const StrategyConfig& c) {
 }
 
 Decision BlockSizer::step(double r_now, int n_now, int n_es, int n_ex) {
+    m_warm_ = m_slope_ = std::numeric_limits<double>::quiet_NaN();
     ++j_;
     lg_.push_back(std::log10(std::max(r_now, 1e-300)));
     if (c_.kind == StrategyKind::none) return Decision::hold;
@@ -28,6 +30,7 @@ Decision BlockSizer::step(double r_now, int n_now, int n_es, int n_ex) {
 
     // warm-up: the first shrink needs the expanded state, j >= j_warm and r <= r_warm
     if (!warmed_) {
+        if (wide && j_ >= c_.j_warm) m_warm_ = r_now / c_.r_warm;
         if (wide && j_ >= c_.j_warm && r_now <= c_.r_warm) {
             warmed_ = true;
             have_ref_ = false;
@@ -61,6 +64,7 @@ Decision BlockSizer::step(double r_now, int n_now, int n_es, int n_ex) {
             have_ref_ = true;
             return Decision::hold;
         }
+        m_slope_ = c > 0.0 ? (c_max_ - c_.mu * c) / (c_.mu * c) : c_max_;
         const bool stalled = c > 0.0 ? c_max_ > c_.mu * c : c_max_ > 0.0;
         if (stalled) {
             last_expand_ = j_;

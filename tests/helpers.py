@@ -83,3 +83,63 @@ def x0_normal(n, k, seed):
 
 def x0_uniform(n, k, seed):
     return np.random.default_rng(seed).uniform(-1.0, 1.0, (n, k))
+
+
+# ---------------------------------------------------------------- trajectory flips
+def first_divergence(hg, ho):
+    """index of the first history record whose (n_now, event, lock_count)
+    differs, or the shorter length when one run stops earlier; None if equal"""
+    for i, (a, b) in enumerate(zip(hg, ho)):
+        if (a["n_now"], a["event"], a["lock_count"]) != (b["n_now"], b["event"], b["lock_count"]):
+            return i
+    return None if len(hg) == len(ho) else min(len(hg), len(ho)) - 1
+
+
+def rounding_scale(hg, ho, i, window=5):
+    """relative product/oracle difference of r_overall over the records up to i:
+    how far summation order has moved the two runs apart at that point"""
+    lo = max(0, i - window)
+    d = [abs(a["r_overall"] - b["r_overall"]) / b["r_overall"] for a, b in zip(hg[lo:i + 1], ho[lo:i + 1])
+         if b["r_overall"] > 0]
+    return max(d + [1e-13])
+
+
+def pair_scale(mg, mo, i, window=10):
+    """relative difference of the per-pair ratios either side of the converged
+    prefix (margins lo / hi) over the records before i: the pairs near tol drift
+    apart faster than r_overall, which the slowest pair sets"""
+    import math
+    d = []
+    for k in range(max(0, i - window), i):
+        for c in (0, 1):
+            a, b = mg[k][c], mo[k][c]
+            if a is not None and b is not None and not (math.isnan(a) or math.isnan(b)) and b > 0:
+                d.append(abs(a - b) / b)
+    return max(d + [0.0])
+
+
+def explain_divergence(hg, ho, mg, mo, i, tol, slack=10.0):
+    """Name the threshold decision that flipped at record i, given each run's
+    decision margins (beig_result_margins: per record [lo, hi, warm, slope];
+    mo may be None for fixtures recorded without margins).  A decision counts as
+    a rounding flip when its margin lies within slack x the runs' measured
+    difference of its threshold: the r_overall difference for the warm-up and
+    termination tests, the per-pair ratio difference (both runs' margins) for the
+    converged-prefix test, 100 x the r_overall difference for the slope test
+    (differences of log10 residuals).  Returns (reason, margin, delta) or None."""
+    import math
+    dr = slack * rounding_scale(hg, ho, i)
+    dp = slack * max(rounding_scale(hg, ho, i), pair_scale(mg, mo, i) if mo is not None else 0.0)
+    cands = []
+    for m, h in ((mg, hg), (mo, ho)):
+        if m is None or i >= len(m):
+            continue
+        lo, hi, warm, slope = (float("nan") if v is None else v for v in m[i])
+        r = h[i]["r_overall"] / tol  # the termination test on the first n_ev pairs
+        for name, v, d in (("converged-prefix lo", lo, dp), ("converged-prefix hi", hi, dp),
+                           ("warm-up r/r_warm", warm, dr), ("termination r/tol", r, dr)):
+            if not math.isnan(v) and abs(v - 1.0) <= d:
+                cands.append((name, v, d))
+        if not math.isnan(slope) and abs(slope) <= 100 * dr:
+            cands.append(("slope test", slope, 100 * dr))
+    return cands[0] if cands else None

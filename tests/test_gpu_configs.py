@@ -16,6 +16,7 @@ import numpy as np
 import pytest
 
 from paper_2409_05572_b200 import workloads as W
+from tests.helpers import explain_divergence, first_divergence
 
 pytestmark = pytest.mark.gpu
 
@@ -52,9 +53,10 @@ def trajectory_report(got, ref):
     return width, dlock
 
 
-def check_block(product, a, w, res, tol_mult=1.0):
+def check_block(product, a, w, res, tol_mult=1.0, north_star=False):
     """residual criterion of the reference (rr.cpp:29-33) on the returned pairs,
-    recomputed on the host in fp64, plus orthonormality"""
+    recomputed on the host in fp64, plus orthonormality; north_star: also the
+    stricter ||A v - lam v|| / ||A|| <= tol"""
     from scipy.sparse import csr_matrix  # noqa: F401 (scipy present in the image)
     full = W.full_from_lower(w.n, w.row_ptr, w.col, w.val)
     v, lam = res.vectors, np.asarray(res.values)
@@ -65,9 +67,28 @@ def check_block(product, a, w, res, tol_mult=1.0):
     vn = np.linalg.norm(v, axis=0)
     crit = rn / (na * vn + vn * np.abs(sgn * lam))
     assert crit.max() <= tol_mult * w.cfg["tol"], crit.max()
+    if north_star:
+        ns = rn / (na * vn)
+        assert ns.max() <= w.cfg["tol"], ns.max()
     g = v.conj().T @ v
     assert np.abs(g - np.eye(len(lam))).max() < 1e-10
     return crit
+
+
+def check_trajectory(res, ref, tol):
+    """identical (n_now, event, lock) trajectory, or a first split that a decision
+    margin within rounding of its threshold explains (tests/test_gpu_flips.py);
+    the iteration count may then move by the few iterations the last pairs take
+    to cross tol"""
+    hg, ho = res.history, ref["history"]
+    i = first_divergence(hg, ho)
+    if i is None:
+        assert res.iterations == ref["iterations"]
+        return None
+    why = explain_divergence(hg, ho, res.margins, ref.get("margins"), i, tol)
+    assert why is not None, (i, hg[i], ho[i], res.margins[i])
+    assert abs(res.iterations - ref["iterations"]) <= 3, (res.iterations, ref["iterations"], why)
+    return i, why
 
 
 def test_config1_matches_oracle_trajectory(product):
@@ -79,11 +100,7 @@ def test_config1_matches_oracle_trajectory(product):
     assert res.status == ref["status"] == 0
     np.testing.assert_allclose(res.values, ref["values"], rtol=1e-9)
     np.testing.assert_allclose(res.values, W.lap2d_eigs(100, 100, 20), rtol=1e-9)
-    flips, dlock = trajectory_report(res.history, ref["history"])
-    assert abs(res.iterations - ref["iterations"]) <= max(2, ref["iterations"] // 100), \
-        (res.iterations, ref["iterations"], flips[:5])
-    assert len(flips) <= 0.02 * ref["iterations"], flips[:10]
-    assert dlock <= 2
+    print("config 1 split:", check_trajectory(res, ref, w.cfg["tol"]))
     check_block(product, a, w, res)
 
 
@@ -99,48 +116,86 @@ def test_config2_matches_oracle_trajectory(product, strategy, n_ex):
     assert res.status == ref["status"] == 0
     np.testing.assert_allclose(res.values, ref["values"], rtol=1e-9)
     np.testing.assert_allclose(res.values, W.lap3d_eigs(64, 64), rtol=1e-9 if n_ex > 64 else 1e-8)
-    flips, dlock = trajectory_report(res.history, ref["history"])
-    # the last pairs cross tol with residual histories that differ at the 1e-4
-    # relative level late in the run (FP64 summation order in every contraction),
-    # so the final converged-prefix decisions land within a few iterations
-    # (observed 215-220 across kernel revisions vs the oracle's 219)
-    assert abs(res.iterations - ref["iterations"]) <= max(3, ref["iterations"] // 40), \
-        (res.iterations, ref["iterations"], flips[:5])
-    assert len(flips) <= 0.05 * ref["iterations"], flips[:10]
-    assert dlock <= 5, dlock
-    check_block(product, a, w, res)
+    print(f"config 2 {strategy}@{n_ex} split:", check_trajectory(res, ref, w.cfg["tol"]))
+    check_block(product, a, w, res, north_star=True)
 
 
-@pytest.mark.parametrize("name,make", [
-    ("cfg3_clustered_1000000_lobpcg_it3", lambda: W.config3("lobpcg")),
-    ("cfg3_clustered_1000000_si_it3", lambda: W.config3("si")),
-    ("cfg4_anderson_96_lobpcg_it3", lambda: W.config4()),
+@pytest.mark.parametrize("name,make,iters,rtol", [
+    ("cfg3_clustered_1000000_lobpcg_it3", lambda: W.config3("lobpcg"), 3, 1e-6),
+    ("cfg3_clustered_1000000_si_it3", lambda: W.config3("si"), 3, 1e-6),
+    ("cfg4_anderson_96_lobpcg_it3", lambda: W.config4(), 3, 1e-6),
+    # through the first shrink (iteration 33) and expansion (36) of the fix strategy
+    ("cfg3_clustered_1000000_lobpcg_it40", lambda: W.config3("lobpcg"), 40, 1e-5),
 ])
-def test_large_configs_prefix_match_oracle(product, name, make):
-    """configs 3/4: the oracle needs minutes per iteration at these sizes, so its
-    first 3 iterations are the fixture: same inputs (hashes), same trajectory,
-    same residual history and Ritz values to rounding"""
+def test_large_configs_prefix_match_oracle(product, name, make, iters, rtol):
+    """configs 3/4: the oracle needs minutes per iteration at these sizes, so a
+    prefix of its run is the fixture: same inputs (hashes), same trajectory (or a
+    split explained by a decision margin at rounding level), same residual
+    history and Ritz values to rounding"""
     ref = fixture(name)
     w = make()
     assert ref["matrix_sha256"] == W.sha256(w.row_ptr, w.col, w.val)
     assert ref["x0_sha256"] == W.sha256(w.x0)
-    _, res = run(product, w, max_iters=3)
+    _, res = run(product, w, max_iters=iters)
     assert res.status == ref["status"]
-    assert events(res.history) == events(ref["history"])
-    got_r = np.array([h["r_overall"] for h in res.history])
-    ref_r = np.array([h["r_overall"] for h in ref["history"]])
-    np.testing.assert_allclose(got_r, ref_r, rtol=1e-6)
-    np.testing.assert_allclose(res.values, ref["values"], rtol=1e-9)
+    i = first_divergence(res.history, ref["history"])
+    if i is not None:
+        why = explain_divergence(res.history, ref["history"], res.margins, ref.get("margins"), i, w.cfg["tol"])
+        assert why is not None, (i, res.history[i], ref["history"][i])
+    k = len(ref["history"]) if i is None else i
+    got_r = np.array([h["r_overall"] for h in res.history[:k]])
+    ref_r = np.array([h["r_overall"] for h in ref["history"][:k]])
+    np.testing.assert_allclose(got_r, ref_r, rtol=rtol)
+    if i is None:
+        np.testing.assert_allclose(res.values, ref["values"], rtol=1e-9)
+    if iters >= 40:  # the shrink/expand cycle happened in both runs
+        ev = [h["event"] for h in ref["history"]]
+        assert 1 in ev and 2 in ev
 
 
 def test_config5_band_and_residuals(product):
     """config 5's operator on a reduced lattice (side 256, same flux 1/64, so the
-    same lowest Landau band: degenerate to ~6e-14 at 0.0969748)
-    for test run time: every returned value must sit in the band.  The full
-    1024^2 / nev 256 run is measured by tools/run_config.py --config 5
-    (DESIGN.md, profiles/)."""
+    same lowest Landau band: degenerate to ~6e-14 at 0.0969748):
+    every returned value must sit in the band."""
     w = W.config5(side=256, nev=32, n_ex=48)
     a, res = run(product, w, max_iters=400)
     assert res.status == 0, res.status
-    np.testing.assert_allclose(res.values, 0.0969748, atol=2e-7)
-    check_block(product, a, w, res)
+    np.testing.assert_allclose(res.values, W.magnetic_eigs(256, 1 / 64, 32), rtol=1e-9)
+    check_block(product, a, w, res, north_star=True)
+
+
+def test_config5_full_size(product):
+    """BASELINE configs[4] at full size (n = 2^20, complex128, nev 256, width up to
+    384): converged, all 256 values within 1e-9 relative of the Harper-chain
+    closed form (workloads.magnetic_eigs), every returned pair below tol in the
+    reference criterion and in the north star's ||A v - lam v|| / ||A||, and the
+    returned block orthonormal."""
+    w = W.config5()
+    a, res = run(product, w)
+    assert res.status == 0, res.status
+    exact = W.magnetic_eigs(1024, 1 / 64, 256)
+    np.testing.assert_allclose(res.values, exact, rtol=1e-9)
+    check_block(product, a, w, res, north_star=True)
+
+
+@pytest.mark.parametrize("solver", ["lobpcg"])
+def test_config3_full_size(product, solver):
+    """BASELINE configs[2] at full size (n = 10^6, the 100 largest eigenpairs):
+    converged; every returned pair passes the reference criterion recomputed on
+    the host; the north star's stricter ||A v - lam v|| / ||A|| (up to 2x
+    stricter here, |lam| ~ ||A||) is reported per pair and bounded by
+    2 tol.  (SI with the operator A at width 200 stagnates, as the reference's
+    StagnationGuard would: rate ~1 - 1.7e-5; its prefix is checked
+    against the oracle in test_large_configs_prefix_match_oracle.)"""
+    w = W.config3(solver)
+    a, res = run(product, w)
+    assert res.status == 0, (res.status, res.iterations)
+    crit = check_block(product, a, w, res)
+    full = W.full_from_lower(w.n, w.row_ptr, w.col, w.val)
+    v, lam = res.vectors, np.asarray(res.values)
+    ns = np.linalg.norm(full @ v - v * lam, axis=0) / (a.norm_est() * np.linalg.norm(v, axis=0))
+    print(f"config 3 {solver}: ref criterion max {crit.max():.3e}; north star max {ns.max():.3e}, "
+          f"{int((ns > w.cfg['tol']).sum())} of {len(ns)} pairs above tol")
+    assert ns.max() <= 2 * w.cfg["tol"]
+    # values descending (largest), distinct from the spectrum's next cluster
+    assert np.all(np.diff(lam) <= 0)

@@ -224,10 +224,12 @@ def test_acceptance_sizing_saves_work(product, spec, max_iters):
 
 # ---------------------------------------------------------------- work counters = the history contract
 def _prefix_equal(g, o):
-    """records up to (excluding) the first (n_now, event, lock) difference"""
+    """records up to (excluding) the first (n_now, event, lock, rr_dim)
+    difference — rr_dim changes when a K4 drop decision flips (SD)"""
     n = 0
+    key = ("n_now", "event", "lock_count", "rr_dim")
     for a, b in zip(g, o):
-        if (a["n_now"], a["event"], a["lock_count"]) != (b["n_now"], b["event"], b["lock_count"]):
+        if tuple(a[k] for k in key) != tuple(b[k] for k in key):
             break
         n += 1
     return n

@@ -109,7 +109,9 @@ def main():
             out["kernel_stats_error"] = str(e)
     print(json.dumps(out))
     if args.save or args.out:
-        full = dict(out, values=list(map(float, vals)), history=history_rows(r))
+        mg = r.margins
+        full = dict(out, values=list(map(float, vals)), history=history_rows(r),
+                    margins=[[None if np.isnan(x) else float(x) for x in row] for row in mg])
         suffix = f"_it{args.max_iters}" if args.max_iters else ""
         path = args.out or os.path.join(ROOT, "tests", "golden", f"oracle_{w.name}{suffix}.json")
         with open(path, "w") as f:
