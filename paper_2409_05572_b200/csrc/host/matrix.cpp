@@ -647,8 +647,12 @@ SparseSym parse_matrix_market_file(const std::string& path) {
         throw ParseError("only 'matrix coordinate' inputs are supported", no);
     field = lowered(field);
     sym = lowered(sym);
-    if (field != "real" && field != "integer") throw ParseError("unsupported field '" + field + "'", no);
-    if (sym != "symmetric" && sym != "general") throw ParseError("unsupported symmetry '" + sym + "'", no);
+    // extension: "complex hermitian" (lower triangle, real diagonal) and
+    // "complex general" (must be Hermitian) build a complex Hermitian matrix
+    const bool cplx = field == "complex";
+    if (field != "real" && field != "integer" && !cplx) throw ParseError("unsupported field '" + field + "'", no);
+    if (cplx ? (sym != "hermitian" && sym != "general") : (sym != "symmetric" && sym != "general"))
+        throw ParseError("unsupported symmetry '" + sym + "'", no);
     const bool general = sym == "general";
     if (!content_line(in, line, no)) throw ParseError("missing size line", no + 1);
     long rows = 0, cols = 0, nnz = 0;
@@ -661,7 +665,7 @@ SparseSym parse_matrix_market_file(const std::string& path) {
     if (rows != cols) throw ParseError("matrix is not square", no);
     if (rows < 0 || nnz < 0) throw ParseError("negative dimensions", no);
     struct Pair {
-        double lo = 0, up = 0;
+        double lo = 0, up = 0, lo_im = 0, up_im = 0;
         bool has_lo = false, has_up = false;
         long ln_lo = 0, ln_up = 0;
     };
@@ -674,14 +678,18 @@ SparseSym parse_matrix_market_file(const std::string& path) {
                              no + 1);
         std::istringstream ss(line);
         long i, j;
-        double v;
+        double v, vi = 0.0;
         std::string rest;
-        if (!(ss >> i >> j >> v)) throw ParseError("malformed entry (need 'i j value')", no);
+        if (!(ss >> i >> j >> v) || (cplx && !(ss >> vi)))
+            throw ParseError(cplx ? "malformed entry (need 'i j re im')" : "malformed entry (need 'i j value')", no);
         if (ss >> rest) throw ParseError("trailing tokens on entry line", no);
         if (i < 1 || i > rows || j < 1 || j > cols) throw ParseError("index out of range", no);
-        if (!std::isfinite(v)) throw ParseError("non-finite value", no);
+        if (!std::isfinite(v) || !std::isfinite(vi)) throw ParseError("non-finite value", no);
         const bool low = i >= j;
-        if (!general && !low) throw ParseError("symmetric input must store the lower triangle", no);
+        if (!general && !low)
+            throw ParseError(cplx ? "hermitian input must store the lower triangle"
+                                  : "symmetric input must store the lower triangle", no);
+        if (cplx && i == j && vi != 0.0) throw ParseError("hermitian diagonal must be real", no);
         const int64_t r = (low ? i : j) - 1, c = (low ? j : i) - 1;
         const int64_t key = r * rows + c;
         auto it = slots.find(key);
@@ -692,13 +700,41 @@ SparseSym parse_matrix_market_file(const std::string& path) {
         Pair& s = it->second;
         if (low) {
             if (s.has_lo) throw ParseError("duplicate entry", no);
-            s.lo = v, s.has_lo = true, s.ln_lo = no;
+            s.lo = v, s.lo_im = vi, s.has_lo = true, s.ln_lo = no;
         } else {
             if (s.has_up) throw ParseError("duplicate entry", no);
-            s.up = v, s.has_up = true, s.ln_up = no;
+            s.up = v, s.up_im = vi, s.has_up = true, s.ln_up = no;
         }
     }
     std::sort(order.begin(), order.end());
+    if (cplx) {  // Hermitian: the mirror of (r, c) holds conj(a_rc)
+        std::vector<int64_t> rp(static_cast<size_t>(rows) + 1, 0);
+        std::vector<int> col;
+        std::vector<double> val;
+        col.reserve(order.size());
+        val.reserve(2 * order.size());
+        for (int64_t key : order) {
+            const Pair& s = slots[key];
+            const int r = static_cast<int>(key / rows), c = static_cast<int>(key % rows);
+            if (r != c && general) {
+                const std::string where = "(" + std::to_string(r + 1) + "," + std::to_string(c + 1) + ")";
+                if (!s.has_lo || !s.has_up)
+                    throw ParseError("general input is not hermitian: entry " + where + " lacks its mirror",
+                                     s.has_lo ? s.ln_lo : s.ln_up);
+                const double scale = std::max({std::hypot(s.lo, s.lo_im), std::hypot(s.up, s.up_im), 1e-300});
+                if (std::hypot(s.lo - s.up, s.lo_im + s.up_im) > 1e-12 * scale)
+                    throw ParseError("general input is not hermitian: entry " + where + " mismatches its mirror",
+                                     s.ln_up);
+            }
+            if (r == c && general && s.lo_im != 0.0) throw ParseError("hermitian diagonal must be real", s.ln_lo);
+            rp[r + 1]++;
+            col.push_back(c);
+            val.push_back(s.lo);
+            val.push_back(s.lo_im);
+        }
+        for (long r = 0; r < rows; ++r) rp[r + 1] += rp[r];
+        return SparseSym(static_cast<int>(rows), std::move(rp), std::move(col), std::move(val), true);
+    }
     std::vector<Entry> es;
     es.reserve(order.size());
     for (int64_t key : order) {
@@ -719,15 +755,20 @@ SparseSym parse_matrix_market_file(const std::string& path) {
 }
 
 void write_matrix_market_file(const SparseSym& a, const std::string& path) {
-    if (a.is_complex()) throw std::invalid_argument("Matrix Market export: real matrices only");
     std::ofstream out(path);
     if (!out) throw IoError("cannot open '" + path + "' for writing");
-    out << "%%MatrixMarket matrix coordinate real symmetric\n";
+    const bool cplx = a.is_complex();  // extension: "complex hermitian", lower triangle
+    out << (cplx ? "%%MatrixMarket matrix coordinate complex hermitian\n"
+                 : "%%MatrixMarket matrix coordinate real symmetric\n");
     out << a.rows() << " " << a.rows() << " " << a.nnz_lower() << "\n";
-    char buf[80];
+    char buf[120];
     for (int r = 0; r < a.rows(); ++r)
         for (int64_t p = a.row_ptr()[r]; p < a.row_ptr()[r + 1]; ++p) {
-            std::snprintf(buf, sizeof buf, "%d %d %.17g\n", r + 1, a.col()[p] + 1, a.val()[p]);
+            if (cplx)
+                std::snprintf(buf, sizeof buf, "%d %d %.17g %.17g\n", r + 1, a.col()[p] + 1, a.val()[2 * p],
+                              a.val()[2 * p + 1]);
+            else
+                std::snprintf(buf, sizeof buf, "%d %d %.17g\n", r + 1, a.col()[p] + 1, a.val()[p]);
             out << buf;
         }
     if (!out.flush()) throw IoError("write failed for '" + path + "'");

@@ -86,6 +86,41 @@ def test_matrix_market_round_trip(prod, tmp_path):
     assert (b.rows, b.nnz_lower) == (a.rows, a.nnz_lower)
 
 
+def test_matrix_market_complex_hermitian(prod, tmp_path):
+    """extension of matio.cpp:89-214: 'complex hermitian' (lower triangle, real
+    diagonal) and 'complex general' (mirror must be the conjugate), with the
+    reference's strictness; export writes 'complex hermitian'"""
+    good = tmp_path / "h.mtx"
+    good.write_text("%%MatrixMarket matrix coordinate complex hermitian\n3 3 4\n"
+                    "1 1 2.0 0.0\n2 1 -1.0 0.5\n2 2 2.0 0.0\n3 3 4.0 0.0\n")
+    a = prod.read(good)
+    assert a.is_complex and (a.rows, a.nnz_lower) == (3, 4)
+    out = tmp_path / "h2.mtx"
+    a.write(out)
+    text = out.read_text().splitlines()
+    assert text[0] == "%%MatrixMarket matrix coordinate complex hermitian"
+    assert text[3].split() == ["2", "1", "-1", "0.5"]
+    b = prod.read(out)
+    assert b.is_complex and (b.rows, b.nnz_lower) == (3, 4)
+    gen = tmp_path / "g.mtx"
+    gen.write_text("%%MatrixMarket matrix coordinate complex general\n2 2 4\n"
+                   "1 1 1.0 0.0\n2 1 0.0 1.0\n1 2 0.0 -1.0\n2 2 1.0 0.0\n")
+    assert prod.read(gen).nnz_lower == 3
+    bad_cases = [
+        "%%MatrixMarket matrix coordinate complex general\n2 2 4\n1 1 1 0\n2 1 0 1\n1 2 0 1\n2 2 1 0\n",
+        "%%MatrixMarket matrix coordinate complex hermitian\n2 2 2\n1 1 1 0.5\n2 2 1 0\n",
+        "%%MatrixMarket matrix coordinate complex hermitian\n2 2 2\n1 2 1 0\n2 2 1 0\n",
+        "%%MatrixMarket matrix coordinate complex hermitian\n2 2 1\n2 1 1\n",
+        "%%MatrixMarket matrix coordinate complex symmetric\n2 2 1\n2 1 1 0\n",
+    ]
+    for i, text in enumerate(bad_cases):
+        f = tmp_path / f"bad{i}.mtx"
+        f.write_text(text)
+        with pytest.raises(B.BlockeigError) as e:
+            prod.read(f)
+        assert e.value.code == B.ERR_PARSE, (i, e.value)
+
+
 def test_solve_argument_validation_before_device(prod):
     a = prod.gen("diag:1,2,3,4")
     for kw in ({"n_ev": 0}, {"n_ev": 2, "tol": 0.0}):
