@@ -145,6 +145,18 @@ int small_grid(int64_t total) { return static_cast<int>(std::max<int64_t>(1, std
 
 using namespace bk;
 
+// long contractions (n > 512 rows) take the 3M DMMA kernels of bk_zdense.cu
+extern "C" int bk_z3m_enabled();
+extern "C" int bk_gram_z3m(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
+                           void* work, const int* run_if, void* stream);
+extern "C" int bk_gram_sym_z3m(int n, const double* x, int ldx, const double* y, int ldy, int d, double* c, int ldc,
+                               void* work, void* stream);
+extern "C" int bk_gemm_z3m(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                           double beta, double* y, int ldy, const int* run_if, void* stream);
+namespace {
+inline bool use3m(int n) { return n > 512 && bk_z3m_enabled(); }
+}  // namespace
+
 extern "C" size_t bk_gram_z_work_bytes(int n, int a, int b) {
     return align256(bk_gram_work_bytes(n, 2 * a, 2 * b)) + align256(4 * static_cast<size_t>(a) * b * sizeof(double));
 }
@@ -152,6 +164,7 @@ extern "C" size_t bk_gram_z_work_bytes(int n, int a, int b) {
 extern "C" int bk_gram_z(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c, int ldc,
                          void* work, void* stream) {
     if (a <= 0 || b <= 0) return 0;
+    if (use3m(n)) return bk_gram_z3m(n, x, ldx, a, y, ldy, b, c, ldc, work, nullptr, stream);
     const cudaStream_t s = as_stream(stream);
     double* gp = reinterpret_cast<double*>(static_cast<char*>(work) + align256(bk_gram_work_bytes(n, 2 * a, 2 * b)));
     int rc = bk_gram_d(n, x, 2 * ldx, 2 * a, y, 2 * ldy, 2 * b, gp, 2 * b, work, stream);
@@ -167,6 +180,7 @@ extern "C" int bk_gram_z(int n, const double* x, int ldx, int a, const double* y
 extern "C" int bk_gram_sym_z(int n, const double* x, int ldx, const double* y, int ldy, int d, double* c, int ldc,
                              void* work, void* stream) {
     if (d <= 0) return 0;
+    if (use3m(n)) return bk_gram_sym_z3m(n, x, ldx, y, ldy, d, c, ldc, work, stream);
     const cudaStream_t s = as_stream(stream);
     double* gp = reinterpret_cast<double*>(static_cast<char*>(work) + align256(bk_gram_work_bytes(n, 2 * d, 2 * d)));
     int rc = bk_gram_sym_d(n, x, 2 * ldx, y, 2 * ldy, 2 * d, gp, 2 * d, work, stream);
@@ -179,6 +193,7 @@ extern "C" int bk_gram_sym_z(int n, const double* x, int ldx, const double* y, i
 extern "C" int bk_gram_if_z(int n, const double* x, int ldx, int a, const double* y, int ldy, int b, double* c,
                             int ldc, void* work, const int* run_if, void* stream) {
     if (a <= 0 || b <= 0 || n <= 0) return 0;
+    if (use3m(n)) return bk_gram_z3m(n, x, ldx, a, y, ldy, b, c, ldc, work, run_if, stream);
     const cudaStream_t s = as_stream(stream);
     double* gp = reinterpret_cast<double*>(static_cast<char*>(work) + align256(bk_gram_work_bytes(n, 2 * a, 2 * b)));
     int rc = bk_gram_if_d(n, x, 2 * ldx, 2 * a, y, 2 * ldy, 2 * b, gp, 2 * b, work, run_if, stream);
@@ -190,6 +205,7 @@ extern "C" int bk_gram_if_z(int n, const double* x, int ldx, int a, const double
 extern "C" int bk_gemm_if_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
                             double beta, double* y, int ldy, void* work, const int* run_if, void* stream) {
     if (n <= 0 || k <= 0 || d <= 0) return 0;
+    if (use3m(n)) return bk_gemm_z3m(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if, stream);
     const cudaStream_t s = as_stream(stream);
     double* e = static_cast<double*>(work);
     expand_kernel<<<small_grid(static_cast<int64_t>(d) * k), 256, 0, s>>>(d, k, c, ldc, e);
@@ -203,6 +219,7 @@ extern "C" size_t bk_gemm_z_work_bytes(int d, int k) { return 4 * static_cast<si
 extern "C" int bk_gemm_z(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
                          double beta, double* y, int ldy, void* work, void* stream) {
     if (n <= 0 || k <= 0) return 0;
+    if (d > 0 && use3m(n)) return bk_gemm_z3m(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, nullptr, stream);
     const cudaStream_t s = as_stream(stream);
     double* e = static_cast<double*>(work);
     if (d > 0) expand_kernel<<<small_grid(static_cast<int64_t>(d) * k), 256, 0, s>>>(d, k, c, ldc, e);

@@ -118,7 +118,31 @@ def pair_scale(mg, mo, i, window=10):
     return max(d + [0.0])
 
 
-def explain_divergence(hg, ho, mg, mo, i, tol, slack=10.0):
+def degenerate_boundary(hg, ho, i, values, rel=1e-9):
+    """The converged-prefix test (rr.cpp:35-36) split inside a degenerate
+    eigenvalue cluster: the pairs converged in one run only (indices between
+    the two lock counts) each have a neighbour whose eigenvalue agrees to `rel`.
+    Within a degenerate eigenspace the individual Ritz vectors are fixed only up
+    to a rotation that rounding chooses, so their per-pair residuals — and which
+    of them passes tol first — are not determined by the problem (the 3D
+    Laplacian's triples and sextets, config 2)."""
+    if values is None or i >= min(len(hg), len(ho)):
+        return None
+    lg, lo = hg[i]["lock_count"], ho[i]["lock_count"]
+    if lg == lo:
+        return None
+    v = np.asarray(values, dtype=float)
+    pairs = range(min(lg, lo), max(lg, lo))
+    for p in pairs:
+        if p >= len(v):
+            return None
+        near = [q for q in (p - 1, p + 1) if 0 <= q < len(v) and abs(v[q] - v[p]) <= rel * abs(v[p])]
+        if not near:
+            return None
+    return ("degenerate converged-prefix boundary", (lg, lo), float(v[min(lg, lo)]))
+
+
+def explain_divergence(hg, ho, mg, mo, i, tol, slack=10.0, values=None):
     """Name the threshold decision that flipped at record i, given each run's
     decision margins (beig_result_margins: per record [lo, hi, warm, slope];
     mo may be None for fixtures recorded without margins).  A decision counts as
@@ -126,8 +150,13 @@ def explain_divergence(hg, ho, mg, mo, i, tol, slack=10.0):
     difference of its threshold: the r_overall difference for the warm-up and
     termination tests, the per-pair ratio difference (both runs' margins) for the
     converged-prefix test, 100 x the r_overall difference for the slope test
-    (differences of log10 residuals).  Returns (reason, margin, delta) or None."""
+    (differences of log10 residuals).  With `values` (the converged eigenvalues),
+    a lock-count split whose boundary pairs are degenerate is explained too
+    (degenerate_boundary).  Returns (reason, margin, delta) or None."""
     import math
+    deg = degenerate_boundary(hg, ho, i, values)
+    if deg is not None:
+        return deg
     dr = slack * rounding_scale(hg, ho, i)
     dp = slack * max(rounding_scale(hg, ho, i), pair_scale(mg, mo, i) if mo is not None else 0.0)
     cands = []

@@ -74,7 +74,7 @@ def work(nbytes):
     return torch.empty(nbytes // 8 + 1, dtype=torch.float64, device="cuda")
 
 
-@pytest.mark.parametrize("n,a,b", [(5000, 37, 53), (20000, 96, 96), (777, 1, 5)])
+@pytest.mark.parametrize("n,a,b", [(5000, 37, 53), (20000, 96, 96), (777, 1, 5), (70000, 384, 384), (40000, 768, 130)])
 def test_gram_z(bk, n, a, b):
     rng = np.random.default_rng(n + a)
     x, y = crandn(rng, n, a), crandn(rng, n, b)
@@ -87,7 +87,7 @@ def test_gram_z(bk, n, a, b):
     assert np.abs(host_c(c, (a, b)) - ref).max() < 1e-13 * n
 
 
-@pytest.mark.parametrize("n,d", [(6000, 130), (3000, 47)])
+@pytest.mark.parametrize("n,d", [(6000, 130), (3000, 47), (50000, 400)])
 def test_gram_sym_z(bk, n, d):
     # Rayleigh-Ritz form S^H (A S) with Hermitian A: upper tiles + Hermitian mirror
     rng = np.random.default_rng(d)
@@ -111,7 +111,7 @@ def test_gram_sym_z(bk, n, d):
                 assert h[p, q] == np.conj(h[q, p])
 
 
-@pytest.mark.parametrize("n,d,k", [(5000, 40, 24), (3000, 96, 160)])
+@pytest.mark.parametrize("n,d,k", [(5000, 40, 24), (3000, 96, 160), (60000, 1152, 200), (9000, 261, 384)])
 def test_gemm_z(bk, n, d, k):
     rng = np.random.default_rng(d * k)
     x, cm, y0 = crandn(rng, n, d), crandn(rng, d, k), crandn(rng, n, k)

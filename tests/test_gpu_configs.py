@@ -85,7 +85,7 @@ def check_trajectory(res, ref, tol):
     if i is None:
         assert res.iterations == ref["iterations"]
         return None
-    why = explain_divergence(hg, ho, res.margins, ref.get("margins"), i, tol)
+    why = explain_divergence(hg, ho, res.margins, ref.get("margins"), i, tol, values=ref["values"])
     assert why is not None, (i, hg[i], ho[i], res.margins[i])
     assert abs(res.iterations - ref["iterations"]) <= 3, (res.iterations, ref["iterations"], why)
     return i, why
