@@ -124,6 +124,12 @@ BK_API int bk_convergence_d(int k, const double* rn2, const double* vn2, const d
 BK_API size_t bk_chol_work_bytes(int a);
 BK_API int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref2, double drop,
                           double* m, int ldm, int* info, void* work, void* stream);
+/* the same, also writing cond[0] = 1 when some kept pivot kept less than 1e-3 of
+ * its projected norm squared (g_jj / p_j > 1e3: the fused CholQR + Newton-Schulz
+ * update would lose orthogonality, eps g_jj / p_j), cond[1] = 1 for a nonempty
+ * well-conditioned block — device predicates for the bk_*_if_* kernels */
+BK_API int bk_chol_drop_cond_d(int a, const double* g, int ldg, const double* ref2, double drop,
+                               double* m, int ldm, int* info, int* cond, void* work, void* stream);
 
 /* ---- K5 symmetric eigensolver (replaces sym_eig_small, proj/src/kernel.cpp:95-100) ----
  * Eigendecomposition of 0.5(H + H^T) (d x d row-major, ldh): values ascending
@@ -229,6 +235,8 @@ BK_API int bk_ns_coeff_z(int a, const double* g, int ldg, double* m, int ldm, vo
 BK_API size_t bk_chol_z_work_bytes(int a);
 BK_API int bk_chol_drop_z(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
                           int ldm, int* info, void* work, void* stream);
+BK_API int bk_chol_drop_cond_z(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
+                               int ldm, int* info, int* cond, void* work, void* stream);
 BK_API int bk_cm_to_rm_z(int n, int k, const double* cm, int ldcm, double* rm, int ldrm, void* stream);
 BK_API int bk_rm_to_cm_z(int n, int k, const double* rm, int ldrm, double* cm, int ldcm, void* stream);
 /* Hermitian projected eigenproblem: grid-cooperative Householder reduction to a
@@ -255,6 +263,25 @@ BK_API int bk_host_decide_sequence(int kind, int j_e, int j_s, double mu, int j_
                                    double r_warm, const double* r, int count, int n_es, int n_ex,
                                    int start_n_now, int start_shrunk, int apply_changes,
                                    int* decisions);
+
+/* ---- sparse shift-and-invert factor (reference SpdFactor sparse path,
+ * proj/src/kernel.cpp:110-134) ----
+ * The symbolic structure comes from the host analysis (host/spchol.cpp): L in
+ * CSC (colptr, rowind with the diagonal first, val), its row patterns (rptr, rk
+ * ascending, rpos = position of L(j, rk) in val), the etree level sets (order,
+ * lvlptr; lvlptr_host is the same array in host memory), C = P (sgn A - shift I)
+ * P^T's lower entries as (aidx = destination in val, aval).
+ * factor: fail = 1 when a pivot is not positive (not SPD).
+ * solve: y = P^T L^-T L^-1 P x for m right-hand sides (row-major, x != y), t a
+ * scratch n x ldt block, perm[new] = old. */
+BK_API int bk_spchol_factor_d(int n, int nlev, const int* lvlptr_host, const int* order, const int64_t* colptr,
+                              const int* rowind, double* val, int64_t nnz_l, const int64_t* rptr, const int* rk,
+                              const int64_t* rpos, int64_t nnz_c, const int64_t* aidx, const double* aval,
+                              int* fail, void* stream);
+BK_API int bk_spchol_solve_d(int n, int m, const double* x, int ldx, double* y, int ldy, double* t, int ldt,
+                             const int* perm, int nlev, const int* lvlptr, const int* order,
+                             const int64_t* colptr, const int* rowind, const double* val, const int64_t* rptr,
+                             const int* rk, const int64_t* rpos, void* stream);
 
 #ifdef __cplusplus
 }

@@ -208,11 +208,17 @@ Result<T> solve(Solver kind, const Sparse<T>& a, const SolverCfg& cfg, const Str
 template <class T>
 std::pair<Mat<T>, Mat<T>> hl_trick(const Mat<T>& s, const Mat<T>& z, int n_now, int lock);
 
-// dense Cholesky of (A - zeta I) for the reference's shift-and-invert SI (n <= 2000 path)
+// Cholesky of (A - zeta I) for the reference's shift-and-invert SI: dense for
+// n <= 2000 (kernel.cpp:103-108), and for n > 2000 the sparse path
+// (kernel.cpp:109-134, SimplicialLLT with AMD) restated as a band (envelope)
+// Cholesky in the natural order — the factor of the same matrix up to a
+// symmetric permutation, so solves agree to rounding
 template <class T>
 struct DenseLLT {
     int n = 0;
     Mat<T> l;
+    int bw = -1;          // band path: lower bandwidth
+    std::vector<T> band;  // L(i, j), i - bw <= j <= i, at band[i * (bw + 1) + j - i + bw]
     DenseLLT(const Sparse<T>& a, double zeta);
     Mat<T> solve(const Mat<T>& b) const;
 };

@@ -516,10 +516,33 @@ double estimate_norm2(const Sparse<T>& a) {
 // kernel.cpp:102-137, dense path only (n <= 2000); the sparse AMD path is
 // outside the oracle (SI on large n runs in operator mode).
 template <class T>
-DenseLLT<T>::DenseLLT(const Sparse<T>& a, double zeta) : n(a.n), l(a.n, a.n) {
-    if (n > 2000)
-        throw std::invalid_argument(
-            "shift-and-invert beyond the dense threshold (n > 2000) is not restated; use operator mode");
+DenseLLT<T>::DenseLLT(const Sparse<T>& a, double zeta) : n(a.n), l(a.n <= 2000 ? a.n : 0, a.n <= 2000 ? a.n : 0) {
+    if (n > 2000) {
+        // band Cholesky (kernel.cpp:109-134 restated; see orc.hpp)
+        bw = 0;
+        for (int r = 0; r < n; ++r)
+            for (int64_t p = a.rp[r]; p < a.rp[r + 1]; ++p) bw = std::max(bw, r - a.col[p]);
+        const int w = bw + 1;
+        if (static_cast<double>(n) * w > 4e8) throw std::invalid_argument("oracle band Cholesky: bandwidth too large");
+        band.assign(static_cast<size_t>(n) * w, T(0));
+        auto L = [&](int i, int j) -> T& { return band[static_cast<size_t>(i) * w + j - i + bw]; };
+        for (int r = 0; r < n; ++r)
+            for (int64_t p = a.rp[r]; p < a.rp[r + 1]; ++p) L(r, a.col[p]) = a.val[p];
+        for (int i = 0; i < n; ++i) L(i, i) -= zeta;
+        for (int j = 0; j < n; ++j) {
+            double djj = re_(L(j, j));
+            for (int k = std::max(0, j - bw); k < j; ++k) djj -= abs2_(L(j, k));
+            if (!(djj > 0.0)) throw std::runtime_error("SpdFactor: matrix is not positive definite");
+            const double ljj = std::sqrt(djj);
+            L(j, j) = ljj;
+            for (int i = j + 1; i <= std::min(n - 1, j + bw); ++i) {
+                T s = L(i, j);
+                for (int k = std::max(0, i - bw); k < j; ++k) s -= L(i, k) * conj_(L(j, k));
+                L(i, j) = s / ljj;
+            }
+        }
+        return;
+    }
     Mat<T> m(n, n);
     for (int r = 0; r < n; ++r)
         for (int64_t p = a.rp[r]; p < a.rp[r + 1]; ++p) {
@@ -545,6 +568,24 @@ template <class T>
 Mat<T> DenseLLT<T>::solve(const Mat<T>& b) const {
     if (b.r != n) throw std::invalid_argument("SpdFactor::solve: dimension mismatch");
     Mat<T> x = b;
+    if (bw >= 0) {
+        const int w = bw + 1;
+        auto L = [&](int i, int j) { return band[static_cast<size_t>(i) * w + j - i + bw]; };
+        for (int c = 0; c < b.c; ++c) {
+            T* y = x.col(c);
+            for (int i = 0; i < n; ++i) {
+                T s = y[i];
+                for (int k = std::max(0, i - bw); k < i; ++k) s -= L(i, k) * y[k];
+                y[i] = s / L(i, i);
+            }
+            for (int i = n - 1; i >= 0; --i) {
+                T s = y[i];
+                for (int k = i + 1; k <= std::min(n - 1, i + bw); ++k) s -= conj_(L(k, i)) * y[k];
+                y[i] = s / L(i, i);
+            }
+        }
+        return x;
+    }
     for (int c = 0; c < b.c; ++c) {
         T* y = x.col(c);
         for (int i = 0; i < n; ++i) {  // L y = b

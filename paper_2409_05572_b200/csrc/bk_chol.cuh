@@ -21,8 +21,13 @@ struct SmemRef {
 };
 
 // one-CTA launch of the routine below (bk_small.cu); pairs: see above
+// cond (optional, 2 ints): [0] = 1 when some kept pivot lost more than kCondFused
+// of its projected norm squared (g_jj / p_j > kCondFused: the block is
+// ill-conditioned, so the caller orthonormalises the tall product explicitly),
+// [1] = 1 when a nonempty block is well-conditioned; predicates of bk_*_if_*
 int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop, double* m, int ldm, int* info,
-                void* work, cudaStream_t st, bool pairs);
+                void* work, cudaStream_t st, bool pairs, int* cond = nullptr);
+constexpr double kCondFused = 1e3;
 
 // Shared-memory layout (dyn_s): gd[a] thr2[a] piv[a] slot[a] (ints) | S (a x a, a <= smem_max_a).
 // S holds the Schur complement in its upper triangle and, in its strict lower
@@ -36,7 +41,8 @@ template <class Ptr>
 __device__ __forceinline__ void chol_drop_core(int a, const double* __restrict__ g, int ldg,
                                                const double* __restrict__ ref2, double drop,
                                                double* __restrict__ m, int ldm, int* __restrict__ info, Ptr S,
-                                               double* gd, double* thr2, double* piv, int* slot, bool pairs) {
+                                               double* gd, double* thr2, double* piv, int* slot, bool pairs,
+                                               int* __restrict__ cond = nullptr) {
     __shared__ int s_keep[2];
     __shared__ double s_invp[2];
     __shared__ int s_kept, s_flags;
@@ -62,6 +68,7 @@ __device__ __forceinline__ void chol_drop_core(int a, const double* __restrict__
     constexpr double kLo2 = (1.0 - 1e-4) * (1.0 - 1e-4), kHi2 = (1.0 + 1e-4) * (1.0 + 1e-4);
     // thread 0's running state: decisions, flags, kept count
     int kept = 0, flags = 0;  // flags: 1 unsure, 2 bad
+    double worst = 0.0;       // max g_jj / p_j over kept pivots (cond)
     auto decide = [&](int j, double p) {
         const double gjj = gd[j], t2 = thr2[j];
         int keep;
@@ -87,6 +94,7 @@ __device__ __forceinline__ void chol_drop_core(int a, const double* __restrict__
         slot[j] = keep ? kept : -1;
         piv[j] = p;
         kept += keep;
+        if (keep) worst = fmax(worst, gjj / p);
         s_keep[j & 1] = keep;
         s_invp[j & 1] = keep ? __drcp_rn(p) : 0.0;  // reciprocal without the division routine
     };
@@ -142,6 +150,11 @@ __device__ __forceinline__ void chol_drop_core(int a, const double* __restrict__
         info[0] = nk;
         info[1] = s_flags & 1;
         info[2] = (s_flags >> 1) & 1;
+        if (cond) {
+            const int ill = nk > 0 && !(worst <= kCondFused);
+            cond[0] = ill;
+            cond[1] = nk > 0 && !ill;
+        }
     }
 }
 
@@ -149,7 +162,7 @@ __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__
                                                const double* __restrict__ ref2, double drop,
                                                double* __restrict__ m, int ldm, int* __restrict__ info,
                                                double* __restrict__ s, int smem_max_a, double* dyn_s,
-                                               bool pairs = false) {
+                                               bool pairs = false, int* __restrict__ cond = nullptr) {
     double* gd = dyn_s;
     double* thr2 = dyn_s + a;
     double* piv = dyn_s + 2 * a;
@@ -159,9 +172,9 @@ __device__ __forceinline__ void chol_drop_body(int a, const double* __restrict__
         // keeps every access an LDS/STS (a generic pointer compiles to LD/ST)
         extern __shared__ double chol_smem[];
         SmemRef S{chol_smem + 3 * a + (a + 1) / 2};
-        chol_drop_core(a, g, ldg, ref2, drop, m, ldm, info, S, gd, thr2, piv, slot, pairs);
+        chol_drop_core(a, g, ldg, ref2, drop, m, ldm, info, S, gd, thr2, piv, slot, pairs, cond);
     } else {
-        chol_drop_core(a, g, ldg, ref2, drop, m, ldm, info, s, gd, thr2, piv, slot, pairs);
+        chol_drop_core(a, g, ldg, ref2, drop, m, ldm, info, s, gd, thr2, piv, slot, pairs, cond);
     }
 }
 

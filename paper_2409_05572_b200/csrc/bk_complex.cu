@@ -295,11 +295,12 @@ extern "C" size_t bk_chol_z_work_bytes(int a) {
            align256(a2 * sizeof(double));
 }
 
-extern "C" int bk_chol_drop_z(int a, const double* g, int ldg, const double* ref2, double drop, double* m, int ldm,
-                              int* info, void* work, void* stream) {
+extern "C" int bk_chol_drop_cond_z(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
+                                   int ldm, int* info, int* cond, void* work, void* stream) {
     const cudaStream_t s = as_stream(stream);
     if (a <= 0) {
         BK_RET(cudaMemsetAsync(info, 0, 3 * sizeof(int), s));
+        if (cond) BK_RET(cudaMemsetAsync(cond, 0, 2 * sizeof(int), s));
         return 0;
     }
     const size_t a2 = 2 * static_cast<size_t>(a);
@@ -314,10 +315,15 @@ extern "C" int bk_chol_drop_z(int a, const double* g, int ldg, const double* ref
     emb_kernel<<<small_grid(static_cast<int64_t>(a) * a), 256, 0, s>>>(a, g, ldg, e);
     if (ref2) dup_kernel<<<ceil_div(a, 256), 256, 0, s>>>(a, ref2, r2);
     int rc = chol_launch(static_cast<int>(a2), e, static_cast<int>(a2), ref2 ? r2 : nullptr, drop, mr,
-                         static_cast<int>(a2), info, cw, s, true);
+                         static_cast<int>(a2), info, cw, s, true, cond);
     if (rc) return rc;
     chol_extract_kernel<<<small_grid(static_cast<int64_t>(a) * a), 256, 0, s>>>(a, mr, m, ldm, info);
     BK_LAUNCHED();
+}
+
+extern "C" int bk_chol_drop_z(int a, const double* g, int ldg, const double* ref2, double drop, double* m, int ldm,
+                              int* info, void* work, void* stream) {
+    return bk_chol_drop_cond_z(a, g, ldg, ref2, drop, m, ldm, info, nullptr, work, stream);
 }
 
 extern "C" int bk_cm_to_rm_z(int n, int k, const double* cm, int ldcm, double* rm, int ldrm, void* stream) {

@@ -33,9 +33,9 @@ __global__ void __launch_bounds__(1024) chol_drop_kernel(int a, const double* __
                                                           const double* __restrict__ ref2, double drop,
                                                           double* __restrict__ m, int ldm,
                                                           int* __restrict__ info, double* __restrict__ s,
-                                                          int pairs) {
+                                                          int pairs, int* __restrict__ cond) {
     extern __shared__ double dyn_s[];
-    chol_drop_body(a, g, ldg, ref2, drop, m, ldm, info, s, kCholSmemMaxA, dyn_s, pairs != 0);
+    chol_drop_body(a, g, ldg, ref2, drop, m, ldm, info, s, kCholSmemMaxA, dyn_s, pairs != 0, cond);
 }
 
 // Grid-cooperative variant for blocks beyond shared memory (a > kCholSmemMaxA:
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(1024) chol_drop_kernel(int a, const double* __
 __global__ void __launch_bounds__(1024) chol_coop_kernel(int a, const double* __restrict__ g, int ldg,
                                                           const double* __restrict__ ref2, double drop,
                                                           double* __restrict__ m, int ldm, int* __restrict__ info,
-                                                          double* __restrict__ s, int pairs) {
+                                                          double* __restrict__ s, int pairs, int* __restrict__ cond) {
     namespace cgr = cooperative_groups;
     cgr::grid_group grid = cgr::this_grid();
     double* gd = s + static_cast<size_t>(a) * a;
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(1024) chol_coop_kernel(int a, const double* __
     const double drop2 = drop * drop;
     constexpr double kLo2 = (1.0 - 1e-4) * (1.0 - 1e-4), kHi2 = (1.0 + 1e-4) * (1.0 + 1e-4);
     int kept = 0;
+    double worst = 0.0;  // max g_jj / p_j over kept pivots (cond)
     for (int j = 0; j < a; ++j) {
         const double p = s[static_cast<size_t>(j) * a + j];
         const double gjj = gd[j];
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(1024) chol_coop_kernel(int a, const double* __
         }
         if (keep) {
             ++kept;
+            worst = fmax(worst, gjj / p);
             const double invp = 1.0 / p;
             const double* rowj = s + static_cast<size_t>(j) * a;
             for (int k = j + 1 + gw; k < a; k += gwarps) {
@@ -153,6 +155,11 @@ __global__ void __launch_bounds__(1024) chol_coop_kernel(int a, const double* __
         info[0] = kept;
         info[1] = flags[0];
         info[2] = flags[1];
+        if (cond) {
+            const int ill = kept > 0 && !(worst <= kCondFused);
+            cond[0] = ill;
+            cond[1] = kept > 0 && !ill;
+        }
     }
 }
 
@@ -328,9 +335,10 @@ extern "C" size_t bk_chol_work_bytes(int a) {
 
 namespace bk {
 int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop, double* m, int ldm, int* info,
-                void* work, cudaStream_t st, bool pairs) {
+                void* work, cudaStream_t st, bool pairs, int* cond) {
     if (a <= 0) {
         BK_RET(cudaMemsetAsync(info, 0, 3 * sizeof(int), st));
+        if (cond) BK_RET(cudaMemsetAsync(cond, 0, 2 * sizeof(int), st));
         return 0;
     }
     auto s = static_cast<double*>(work);  // a x a (used when a > kCholSmemMaxA)
@@ -348,7 +356,7 @@ int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop
         const int grid = max(1, min(min(ceil_div(a, 32), kSMs), max(per_sm, 1) * kSMs));
         int aa = a, l1 = ldg, l2 = ldm, pr = pairs ? 1 : 0;
         void* args[] = {&aa, const_cast<double**>(&g), &l1, const_cast<double**>(&ref2), &drop, &m, &l2, &info, &s,
-                        &pr};
+                        &pr, &cond};
         BK_RET(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(chol_coop_kernel), dim3(grid), dim3(1024),
                                            args, 0, st));
         return 0;
@@ -359,7 +367,7 @@ int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop
         const char* e = getenv("BK_CHOL_THREADS");
         return e ? max(32, min(1024, atoi(e) / 32 * 32)) : 1024;
     }();
-    chol_drop_kernel<<<1, threads, smem, st>>>(a, g, ldg, ref2, drop, m, ldm, info, s, pairs ? 1 : 0);
+    chol_drop_kernel<<<1, threads, smem, st>>>(a, g, ldg, ref2, drop, m, ldm, info, s, pairs ? 1 : 0, cond);
     BK_LAUNCHED();
 }
 }  // namespace bk
@@ -367,6 +375,11 @@ int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop
 extern "C" int bk_chol_drop_d(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
                               int ldm, int* info, void* work, void* stream) {
     return chol_launch(a, g, ldg, ref2, drop, m, ldm, info, work, as_stream(stream), false);
+}
+
+extern "C" int bk_chol_drop_cond_d(int a, const double* g, int ldg, const double* ref2, double drop, double* m,
+                                   int ldm, int* info, int* cond, void* work, void* stream) {
+    return chol_launch(a, g, ldg, ref2, drop, m, ldm, info, work, as_stream(stream), false, cond);
 }
 
 extern "C" size_t bk_syev_jacobi_work_bytes(int d) {

@@ -60,10 +60,11 @@ thread_local double g_host_call_s = 0.0;  // BLOCKEIG_TIMING: host time inside C
 // pinned host staging for the per-iteration record and small infos
 struct Pinned {
     double* rec = nullptr;  // 8 doubles
-    int* info = nullptr;    // 32 ints: [0..15] synchronous infos, [16..] speculative K4 slots
+    int* info = nullptr;    // 64 ints: [0..15] synchronous infos, [16..] speculative K4 slots,
+                            // [48..] K4 conditioning flags (2 per call slot)
     Pinned() {
         BKC(cudaMallocHost(reinterpret_cast<void**>(&rec), 8 * sizeof(double)));
-        BKC(cudaMallocHost(reinterpret_cast<void**>(&info), 32 * sizeof(int)));
+        BKC(cudaMallocHost(reinterpret_cast<void**>(&info), 64 * sizeof(int)));
     }
     ~Pinned() {
         cudaFreeHost(rec);
@@ -148,7 +149,7 @@ public:
         M1_.alloc(static_cast<size_t>(tcap_) * tcap_ * es);
         M2_.alloc(static_cast<size_t>(tcap_) * tcap_ * es);
         SMALL_.alloc(8 * dc * sizeof(double));
-        INFO_.alloc(64 * sizeof(int));
+        INFO_.alloc(96 * sizeof(int));
         const int idc = static_cast<int>(dc);
         size_t work;
         if (cw_ == 1) {
@@ -534,11 +535,16 @@ private:
             BKC(cudaMemsetAsync(info + 3, 0, sizeof(int), stream_));
         }
         gram(rows, w.p, w.ld, a, w.p, w.ld, a, GB_.d(), a);
+        // conditioning flags of this call: [0] ill (g_jj / p_j > 1e3 for a kept
+        // pivot), [1] well — predicates of the two second-pass forms below
+        int* cond = INFO_.as<int>() + 64 + 2 * (slot + 1);
+        int* cond_host = pin_.info + 48 + 2 * (slot + 1);
         auto tc = prof_begin();
-        if (cw_ == 1) BKC(bk_chol_drop_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
-        else BKC(bk_chol_drop_z(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, WORK_.p(), st()));
+        if (cw_ == 1) BKC(bk_chol_drop_cond_d(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, cond, WORK_.p(), st()));
+        else BKC(bk_chol_drop_cond_z(a, GB_.d(), a, ref2, kDropTol, M1_.d(), a, info, cond, WORK_.p(), st()));
         prof_end(tc, K_CHOL, 8.0 * cw_ * a * a, cw_ * cw_ * a * a * a / 3.0);
         BKC(cudaMemcpyAsync(info_host, info, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        BKC(cudaMemcpyAsync(cond_host, cond, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
         ++proj_calls_;
         int kept = a;
         if (slot >= 0) {
@@ -561,13 +567,26 @@ private:
         // and one n-row update fewer per orthonormalisation.  (The tall product's
         // own rounding, O(kappa eps) with kappa <= 1e4 after the pivot check, is
         // below what the Rayleigh-Ritz step resolves.)
+        // That fused form corrects only the Cholesky's own rounding: W1's true Gram
+        // differs from M1^T G M1 by M1^T dG M1 ~ eps g_jj / p_j, so when a kept
+        // pivot lost more than 1e-3 of its projected norm squared (device flag
+        // cond[0], from the Cholesky) the tall form below runs instead — W1 = W M1
+        // formed, its Gram taken, one Newton-Schulz step — restoring orthogonality
+        // to rounding (CholQR2 with the second factorisation replaced by the NS
+        // step).  Both forms are launched, each predicated on its flag: no host
+        // round trip.
         static const bool ns_tall = std::getenv("BLOCKEIG_NS_TALL") != nullptr;
         if (rows >= n_ && !ns_tall) {
             gemm(a, GB_.d(), a, a, M1_.d(), a, kept, 1.0, 0.0, COEF_.d(), kept);       // T = G M1
             gram(a, M1_.d(), a, kept, COEF_.d(), kept, kept, GB_.d(), kept);           // G1 = M1^T T
             ns_coeff(kept, GB_.d(), kept, M2_.d(), kept);                               // M2 = (3I - G1)/2
             gemm(a, M1_.d(), a, kept, M2_.d(), kept, kept, 1.0, 0.0, COEF_.d(), kept);  // M1 M2
-            gemm(rows, w.p, w.ld, a, COEF_.d(), kept, kept, 1.0, 0.0, out.p, out.ld);
+            gemm_if(rows, w.p, w.ld, a, COEF_.d(), kept, kept, 1.0, 0.0, out.p, out.ld, cond + 1, cond_host + 1);
+            Blk pt = B(PT_.d(), ldT_);
+            gemm_if(rows, w.p, w.ld, a, M1_.d(), a, kept, 1.0, 0.0, pt.p, pt.ld, cond, cond_host);
+            gram_if(rows, pt.p, pt.ld, kept, pt.p, pt.ld, kept, GB_.d(), kept, cond, cond_host);
+            ns_coeff(kept, GB_.d(), kept, M2_.d(), kept);  // (stale input when skipped: unused)
+            gemm_if(rows, pt.p, pt.ld, kept, M2_.d(), kept, kept, 1.0, 0.0, out.p, out.ld, cond, cond_host);
             return kept;
         }
         Blk pt = B(PT_.d(), ldT_);
@@ -795,6 +814,12 @@ private:
             lincomb(n_, k, cfg_.op_c, x, -1.0, ax_known, y);
             return;
         }
+        if (spchol_) {  // n > 2000: sparse factor, device triangular solves
+            auto t = prof_begin();
+            spchol_->solve(x.p, x.ld, k, y.p, y.ld, st());
+            prof_end(t, K_OTHER, 0.0, 0.0);
+            return;
+        }
         // (A - zeta I)^{-1} = M M^T with M = R^{-1} from the dense Cholesky
         gram(n_, INV_.d(), n_, n_, x.p, x.ld, k, PT_.d(), ldT_);
         gemm(n_, INV_.d(), n_, n_, PT_.d(), ldT_, k, 1.0, 0.0, y.p, y.ld);
@@ -873,6 +898,7 @@ private:
     int tcap_ = 0, dcap_ = 0, ldS_ = 0, ldT_ = 0, ldH_ = 0;
     DevMem S_[2], AS_, R_, XD_, T1_, T2_, PT_, VEC_, H_, Z_, ZC_, CZ_, VALS_, COEF_, GB_, M1_, M2_, SMALL_,
         INFO_, WORK_, TD_, INV_, stage_, CEXP_, VALS_BAK_;
+    std::unique_ptr<SpChol> spchol_;
     DevMem CG_[6];
     // pinned staging is per host thread and outlives the solve (cudaFreeHost
     // synchronises the device and costs ms per solve)
@@ -914,11 +940,12 @@ private:
 // SpdFactor dense path, kernel.cpp:102-137, n <= 2000): K4's Cholesky kernel
 // without dropping gives M = R^{-1}, so (A - zeta I)^{-1} = M M^T.
 void Engine::factor_shift_invert() {
-    if (n_ > 2000)
-        throw std::invalid_argument(
-            "shift-and-invert SI is limited to n <= 2000 on the device build; use the shifted operator mode");
     if (cw_ != 1)
         throw std::invalid_argument("shift-and-invert SI: complex matrices need the shifted operator mode");
+    if (n_ > 2000) {  // reference sparse path (SimplicialLLT, AMD): host symbolic, device numeric
+        spchol_ = std::make_unique<SpChol>(a_, cfg_.largest ? -1.0 : 1.0, cfg_.shift, stream_);
+        return;
+    }
     const size_t nn = static_cast<size_t>(n_) * n_;
     std::vector<double> dense(nn, 0.0);
     const double sgn = cfg_.largest ? -1.0 : 1.0;

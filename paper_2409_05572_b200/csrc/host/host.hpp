@@ -168,6 +168,26 @@ double spd_shift_value(double lambda1);
 SparseSym parse_matrix_market_file(const std::string& path);
 void write_matrix_market_file(const SparseSym& a, const std::string& path);
 
+// ---------------------------------------------------------------- sparse shift-and-invert
+// Factor of sgn A - shift I for shift-and-invert SI on n > 2000 (reference
+// SpdFactor sparse path, proj/src/kernel.cpp:110-134): symbolic analysis on the
+// host, numeric factorisation and solves on the device (host/spchol.cpp,
+// bk_spchol.cu).  Throws runtime_error when the matrix is not positive definite.
+class SpChol {
+public:
+    SpChol(const SparseSym& a, double sgn, double shift, void* stream);
+    // y = (sgn A - shift I)^{-1} x for m columns of row-major blocks (x != y)
+    void solve(const double* x, int ldx, int m, double* y, int ldy, void* stream);
+    int64_t nnz_l() const { return nnz_l_; }
+    int levels() const { return nlev_; }
+
+private:
+    int n_ = 0, nlev_ = 0;
+    int64_t nnz_l_ = 0;
+    std::vector<int> perm_h_, lvlptr_h_;
+    DevMem colptr_, rowind_, val_, rptr_, rk_, rpos_, order_, lvlptr_, perm_, fail_, t_;
+};
+
 // ---------------------------------------------------------------- strategy
 // proj/src/strategy.{hpp,cpp}: same knobs, same decisions.
 enum class StrategyKind { none = 0, fix = 1, slope = 2, slopek = 3 };

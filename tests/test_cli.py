@@ -112,17 +112,20 @@ def test_product_history_csv_matches_oracle(solver):
     o = cli(ORACLE_CLI, *args)
     assert g.returncode == o.returncode == 0, (g.stderr, o.stderr)
     hg, ho = rows(g.stdout), rows(o.stdout)
-    # SD keeps a residual column whose remaining norm sits at the 1e-8 drop
-    # threshold for hundreds of iterations: its basis, and so
-    # r_overall, carries rounding-level drift that grows along the run (2e-6
-    # relative by iteration 292 on the B200) without changing any decision
-    # (1e-4 relative by iteration 397, 1e-3 by 452); elsewhere 1e-6 relative plus an absolute
-    # floor of 1e-12 (the residual ratio is relative to ||A||: its rounding noise
-    # does not shrink with it, and a ratio near tol 1e-8 differs by ~4e-14)
-    rtol = 1e-2 if solver == "sd" else 1e-6
+    # r_overall: 1e-6 relative plus an absolute floor of 1e-12 (the residual ratio
+    # is relative to ||A||: its rounding noise does not shrink with it, and a ratio
+    # near tol 1e-8 differs by ~4e-14).  SD keeps a residual column whose remaining
+    # norm sits at the 1e-8 drop threshold for hundreds of iterations (DESIGN.md
+    # "Parity"): its drift grows ~10x per 50 iterations past ~300 (2e-6 at 292,
+    # 2e-2 at 465 on the B200) until a K4 drop decision flips (kept counts, hence
+    # spmv_cols, differ by ~iteration 565 with the same widths): SD's records are
+    # compared over the first 250 iterations
+    rtol = 1e-6
     for a, b in zip(hg, ho):
         if (a["n_now"], a["event"]) != (b["n_now"], b["event"]):
             break  # a rounding flip (tests/test_gpu_flips.py); the prefix is compared
+        if solver == "sd" and int(a["iteration"]) > 250:
+            break
         for c in HIST_COLS:
             if c == "r_overall":
                 assert abs(float(a[c]) - float(b[c])) <= rtol * float(b[c]) + 1e-12, (a, b)

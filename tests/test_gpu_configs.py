@@ -72,6 +72,11 @@ def check_block(product, a, w, res, tol_mult=1.0, north_star=False):
         assert ns.max() <= w.cfg["tol"], ns.max()
     g = v.conj().T @ v
     assert np.abs(g - np.eye(len(lam))).max() < 1e-10
+    if w.solver == "lobpcg" and res.history:
+        # the device's own convergence record (max over the n_ev pairs of the same
+        # criterion, computed by the residual kernel) agrees with the host
+        dev = res.history[-1]["r_overall"]
+        assert abs(crit.max() - dev) <= 1e-6 * dev + 1e-15, (crit.max(), dev, int(crit.argmax()))
     return crit
 
 

@@ -230,3 +230,22 @@ def test_random_block_reproducible(ok):
     a = ok.random_block(9, 3, 77)
     assert np.array_equal(a, ok.random_block(9, 3, 77))
     assert not np.array_equal(a, ok.random_block(9, 3, 78))
+
+
+def test_oracle_sparse_shift_invert_band_path(oracle):
+    """kernel.cpp:109-134 (n > 2000, SimplicialLLT) restated as a band Cholesky:
+    SI with shift-and-invert on a 2D Laplacian of n = 3600 reaches the closed
+    form, and an indefinite A - zeta I is refused like the reference"""
+    import numpy as np
+    from paper_2409_05572_b200 import workloads as W
+    from paper_2409_05572_b200.blockeig import BlockeigError
+    rp, c, v = W.grid_laplacian((60, 60))
+    r = oracle.solve(oracle.from_csr(3600, rp, c, v), "si", n_ev=8, tol=1e-10, max_iters=500, seed=5, shift=0.0,
+                     strategy=oracle.strategy_config("fix"))
+    assert r.status == 0
+    np.testing.assert_allclose(r.values, W.lap2d_eigs(60, 60, 8), rtol=1e-9)
+    try:
+        oracle.solve(oracle.from_csr(3600, rp, c, v), "si", n_ev=4, shift=0.5, max_iters=5)
+        raise AssertionError("indefinite factor accepted")
+    except BlockeigError as e:
+        assert e.code == 4 and "not positive definite" in e.msg
