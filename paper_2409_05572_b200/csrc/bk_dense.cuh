@@ -32,6 +32,24 @@ __device__ __forceinline__ void load_rows(double* dst, int pitch, const double* 
     }
 }
 
+// 16-byte cp.async tile copy with the shape fixed at compile time (ROWS rows of
+// CPR 16-byte chunks, NT threads): src[r0 + r][c0 + 2c'] -> dst[r * pitch + 2c'],
+// zero-filled outside rows < r_end, columns < c_end (c_end even: complex views)
+template <int ROWS, int CPR, int NT>
+__device__ __forceinline__ void load_tile16(double* dst, int pitch, const double* __restrict__ src, int ld, int r0,
+                                            int r_end, int c0, int c_end, int tid) {
+    constexpr int TOTAL = ROWS * CPR;
+#pragma unroll
+    for (int it = 0; it < (TOTAL + NT - 1) / NT; ++it) {
+        const int e = tid + it * NT;
+        if (TOTAL % NT != 0 && e >= TOTAL) break;
+        const int r = e / CPR, c = 2 * (e % CPR);
+        const int row = r0 + r, col = c0 + c;
+        const bool ok = row < r_end && col < c_end;
+        cp_async16(dst + r * pitch + c, ok ? src + static_cast<size_t>(row) * ld + col : src, ok);
+    }
+}
+
 struct GramPlan {
     int splits, rows_per_split;
 };

@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(WM * WN * 32) zgram3m_kernel(int n, const doub
     const int nk = ceil_div(max(r_end - r_begin, 0), TK);
     auto load_stage = [&](int kt, int st) {
         const int r0 = r_begin + kt * TK;
-        load_rows<true>(xs + st * TK * PX, PX, x, 2 * ldx, r0, r_end, 2 * i0, 2 * a, TK, 2 * TM, tid, NT);
-        if (!same) load_rows<true>(ys + st * TK * PY, PY, y, 2 * ldy, r0, r_end, 2 * j0, 2 * b, TK, 2 * TN, tid, NT);
+        load_tile16<TK, TM, NT>(xs + st * TK * PX, PX, x, 2 * ldx, r0, r_end, 2 * i0, 2 * a, tid);
+        if (!same) load_tile16<TK, TN, NT>(ys + st * TK * PY, PY, y, 2 * ldy, r0, r_end, 2 * j0, 2 * b, tid);
     };
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
@@ -106,19 +106,25 @@ __global__ void __launch_bounds__(WM * WN * 32) zgram3m_kernel(int n, const doub
 #pragma unroll
             for (int ni = 0; ni < FN; ++ni)
                 yf[ni] = *reinterpret_cast<const double2*>(yd + (k4 + t) * py + 2 * (wn + ni * 8 + g));
-            double ysum[FN];
+            // T1 and T2 products first, the operand sums of T3 meanwhile: the
+            // DADDs' latency is off the DMMA issue path
+            double ysum[FN], xdiff[FM];
 #pragma unroll
             for (int ni = 0; ni < FN; ++ni) ysum[ni] = yf[ni].x + yf[ni].y;
 #pragma unroll
-            for (int mi = 0; mi < FM; ++mi) {
-                const double xdiff = xf[mi].x - xf[mi].y;
+            for (int mi = 0; mi < FM; ++mi) xdiff[mi] = xf[mi].x - xf[mi].y;
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < FN; ++ni) {
                     dmma_8x8x4(acc[0][mi][ni][0], acc[0][mi][ni][1], xf[mi].x, yf[ni].x);
                     dmma_8x8x4(acc[1][mi][ni][0], acc[1][mi][ni][1], xf[mi].y, yf[ni].y);
-                    dmma_8x8x4(acc[2][mi][ni][0], acc[2][mi][ni][1], xdiff, ysum[ni]);
                 }
-            }
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni)
+                    dmma_8x8x4(acc[2][mi][ni][0], acc[2][mi][ni][1], xdiff[mi], ysum[ni]);
         }
     }
     cp_async_wait<0>();
@@ -268,8 +274,8 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) zgemm3m_kernel(int n, cons
     const int nk = ceil_div(d, TK);
     auto load_stage = [&](int kt, int st) {
         const int k0 = kt * TK;
-        load_rows<true>(xs + st * TM * PX, PX, x, 2 * ldx, r0, n, 2 * k0, 2 * d, TM, 2 * TK, tid, NT);
-        load_rows<true>(cs + st * TK * PC, PC, cm, 2 * ldc, k0, d, 2 * c0, 2 * k, TK, 2 * TN, tid, NT);
+        load_tile16<TM, TK, NT>(xs + st * TM * PX, PX, x, 2 * ldx, r0, n, 2 * k0, 2 * d, tid);
+        load_tile16<TK, TN, NT>(cs + st * TK * PC, PC, cm, 2 * ldc, k0, d, 2 * c0, 2 * k, tid);
     };
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
@@ -293,19 +299,23 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) zgemm3m_kernel(int n, cons
 #pragma unroll
             for (int ni = 0; ni < FN; ++ni)
                 cf[ni] = *reinterpret_cast<const double2*>(cd + (k4 + t) * PC + 2 * (wn + ni * 8 + g));
-            double csum[FN];
+            double csum[FN], xsum[FM];
 #pragma unroll
             for (int ni = 0; ni < FN; ++ni) csum[ni] = cf[ni].x + cf[ni].y;
 #pragma unroll
-            for (int mi = 0; mi < FM; ++mi) {
-                const double xsum = xf[mi].x + xf[mi].y;
+            for (int mi = 0; mi < FM; ++mi) xsum[mi] = xf[mi].x + xf[mi].y;
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < FN; ++ni) {
                     dmma_8x8x4(acc[0][mi][ni][0], acc[0][mi][ni][1], xf[mi].x, cf[ni].x);
                     dmma_8x8x4(acc[1][mi][ni][0], acc[1][mi][ni][1], xf[mi].y, cf[ni].y);
-                    dmma_8x8x4(acc[2][mi][ni][0], acc[2][mi][ni][1], xsum, csum[ni]);
                 }
-            }
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni)
+                    dmma_8x8x4(acc[2][mi][ni][0], acc[2][mi][ni][1], xsum[mi], csum[ni]);
         }
     }
     cp_async_wait<0>();

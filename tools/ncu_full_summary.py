@@ -12,8 +12,10 @@ import csv
 import json
 import sys
 
-MAIN = {"gram": "gram_kernel", "gemm": "gemm_kernel", "spmm": "spmm_d_kernel"}
-AUX = {"gram": ["gram_reduce"]}
+# main kernels of each class, real and complex (3M) forms
+MAIN = {"gram": ["gram_kernel", "zgram3m_kernel"], "gemm": ["gemm_kernel", "zgemm3m_kernel"],
+        "spmm": ["spmm_d_kernel", "spmm_d_half_kernel", "spmm_z_kernel"]}
+AUX = {"gram": ["gram_reduce", "zgram_reduce"]}
 
 
 def short(name):
@@ -70,7 +72,7 @@ def main():
         # < 4 MB and are excluded here too (their reduce launches follow them)
         mains, members = [], []
         for idx, x in enumerate(launches):
-            if x["kernel"] != main_k or x["dram_bytes"] < 4e6:
+            if x["kernel"] not in main_k or x["dram_bytes"] < 4e6:
                 continue
             mains.append(x)
             members.append(x)
