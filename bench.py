@@ -217,7 +217,10 @@ def ncu_traffic(kernel, workload):
                 d = json.load(f)
             k = d.get("classes", {}).get(kernel)
             if k and k.get("dram_bytes_per_launch"):
-                return k["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+                src = os.path.relpath(path, ROOT)
+                if k.get("launch"):  # a representative launch's capture, not the class average
+                    src += f" ({k['launch']}: {k.get('ratio', 'n/a')}x its algorithmic bytes)"
+                return k["dram_bytes_per_launch"], src
         except (OSError, ValueError):
             continue
     return None, None

@@ -1310,7 +1310,24 @@ __global__ void __launch_bounds__(kCoopThreads) tridiag_coop_kernel(int d, E* __
             E s = mk<E>(0.0, 0.0);
             E* row = a + static_cast<size_t>(r) * d;
             const E vr = hp ? vprev[r] : mk<E>(0.0, 0.0), wr = hp ? wprev[r] : mk<E>(0.0, 0.0);
-            for (int c = j + 1 + lane; c < d; c += 32) {
+            // 4 row elements per lane in flight: the pass is L2-latency bound
+            // (a step's trailing block is spread over every warp of the grid)
+            int c = j + 1 + lane;
+            for (; c + 96 < d; c += 128) {
+                E av[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) av[u] = row[c + 32 * u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cc = c + 32 * u;
+                    if (hp) {
+                        av[u] = av[u] - (mul(vr, cj(wprev[cc])) + mul(wr, cj(vprev[cc])));
+                        row[cc] = av[u];
+                    }
+                    s = s + mul(av[u], vcur[cc]);
+                }
+            }
+            for (; c < d; c += 32) {
                 E av = row[c];
                 if (hp) {
                     av = av - (mul(vr, cj(wprev[c])) + mul(wr, cj(vprev[c])));
@@ -1332,11 +1349,12 @@ __global__ void __launch_bounds__(kCoopThreads) tridiag_coop_kernel(int d, E* __
         }
         grid.sync();
         // ---- C: w_j = p_j - (tau_j / 2)(p_j^H v_j) v_j
-        if (tid == 0) {
+        if (wid == 0) {  // the grid's partials, lane-strided then a fixed shuffle tree
             E acc = mk<E>(0.0, 0.0);
-            for (int g = 0; g < static_cast<int>(gridDim.x); ++g)
+            for (int g = lane; g < static_cast<int>(gridDim.x); g += 32)
                 acc = acc + part[static_cast<size_t>(buf) * gridDim.x + g];
-            s_pv = acc;
+            acc = wsum(acc);
+            if (lane == 0) s_pv = acc;
         }
         __syncthreads();
         const E aw = scal(-0.5, mul(t, s_pv));
