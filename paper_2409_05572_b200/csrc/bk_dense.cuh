@@ -50,6 +50,38 @@ __device__ __forceinline__ void load_tile16(double* dst, int pitch, const double
     }
 }
 
+// The same with the real kernels' shapes: V16 copies 16-byte chunks (an odd
+// width's last chunk copies 8 bytes and zero-fills the rest), else 8-byte
+// elements; ROWS x COLS doubles, NT threads, all fixed at compile time
+template <bool V16, int ROWS, int COLS, int NT>
+__device__ __forceinline__ void load_tile(double* dst, int pitch, const double* __restrict__ src, int ld, int r0,
+                                          int r_end, int c0, int c_end, int tid) {
+    if constexpr (V16) {
+        constexpr int CPR = COLS / 2, TOTAL = ROWS * CPR;
+#pragma unroll
+        for (int it = 0; it < (TOTAL + NT - 1) / NT; ++it) {
+            const int e = tid + it * NT;
+            if (TOTAL % NT != 0 && e >= TOTAL) break;
+            const int r = e / CPR, c = 2 * (e % CPR);
+            const int row = r0 + r, col = c0 + c;
+            int bytes = 0;
+            if (row < r_end && col < c_end) bytes = col + 1 < c_end ? 16 : 8;
+            cp_async16(dst + r * pitch + c, bytes ? src + static_cast<size_t>(row) * ld + col : src, bytes);
+        }
+    } else {
+        constexpr int TOTAL = ROWS * COLS;
+#pragma unroll
+        for (int it = 0; it < (TOTAL + NT - 1) / NT; ++it) {
+            const int e = tid + it * NT;
+            if (TOTAL % NT != 0 && e >= TOTAL) break;
+            const int r = e / COLS, c = e % COLS;
+            const int row = r0 + r, col = c0 + c;
+            const bool ok = row < r_end && col < c_end;
+            cp_async8(dst + r * pitch + c, ok ? src + static_cast<size_t>(row) * ld + col : src, ok);
+        }
+    }
+}
+
 struct GramPlan {
     int splits, rows_per_split;
 };
