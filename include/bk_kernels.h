@@ -179,6 +179,8 @@ BK_API int bk_coldot_d(int n, const double* x, int ldx, const double* y, int ldy
  * bk_cg_step1: for active c: pap <= 0 deactivates, else alpha = rs/pap,
  *              x += alpha p, r -= alpha ap.
  * bk_cg_step2: for active c: beta = rs_new/rs, p = r + beta p, rs = rs_new. */
+/* CG start for the TraceMIN solves (kernel.cpp:143-145): bnorm = sqrt(rs), active = bnorm != 0 */
+BK_API int bk_cg_init_d(int k, const double* rs, double* bnorm, int* active, void* stream);
 BK_API int bk_cg_check_d(int k, const double* rs, const double* bnorm, int* active, int* count,
                          void* stream);
 BK_API int bk_cg_step1_d(int n, int k, const double* rs, const double* pap, int* active, double* x,

@@ -36,7 +36,10 @@ namespace {
 constexpr int kTriThreads = 1024;
 constexpr int kTriSmemMaxM = 150;  // trailing block m x m in shared memory when m <= 150
 constexpr int kSyevMaxD = 1200;  // 4d + 151^2 doubles of shared memory <= 227 KB
-constexpr int kSyevJacobiMaxD = 48;
+// the one-CTA Jacobi path is kept for BK_SYEV_JACOBI_MAX=<d> tuning runs: the
+// tridiagonal path measured faster at every d (tools/syev_probe.py, all pairs:
+// d = 16 173 -> 115 us, 40 568 -> 208 us; config 1 end to end 2.90 -> 2.37 s)
+constexpr int kSyevJacobiMaxD = 0;
 
 // ------------------------------------------------------------------ 1. tridiagonalisation
 // a: d x d working copy (row-major, lda = d), symmetric, both triangles kept.
@@ -1774,9 +1777,8 @@ extern "C" int bk_syev_z(int d, const double* h, int ldh, int n_need, double* va
     BK_LAUNCHED();
 }
 
-// Dispatch: the one-CTA cyclic Jacobi (bk_small.cu) for small projected
-// problems, where its d-1 rounds per sweep are cheap and it gives the most
-// accurate vectors; tridiagonalisation + bisection + inverse iteration above.
+// Dispatch: tridiagonalisation + bisection + inverse iteration; the one-CTA
+// cyclic Jacobi (bk_small.cu) only on request (BK_SYEV_JACOBI_MAX).
 extern "C" size_t bk_syev_work_bytes(int d) {
     const size_t a = bk_syev_jacobi_work_bytes(d), b = bk_syev_tri_work_bytes(d);
     return a > b ? a : b;

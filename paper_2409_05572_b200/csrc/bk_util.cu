@@ -300,6 +300,14 @@ __global__ void __launch_bounds__(256) coldot_partial(int n, const double* __res
     }
 }
 
+// bnorm = ||b|| per column, active = (bnorm != 0) (kernel.cpp:143-145)
+__global__ void cg_init_kernel(int k, const double* rs, double* bnorm, int* active) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+        bnorm[c] = sqrt(rs[c]);
+        active[c] = bnorm[c] != 0.0;
+    }
+}
+
 __global__ void cg_check_kernel(int k, const double* rs, const double* bnorm, int* active, int* count) {
     __shared__ int cnt;
     if (threadIdx.x == 0) cnt = 0;
@@ -321,7 +329,11 @@ __global__ void cg_step1_kernel(int n, int k, const double* rs, const double* pa
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(e / k), c = static_cast<int>(e % k), cs = c >> sh;
-        if (!active[cs] || !(pap[cs] > 0.0)) continue;
+        if (!active[cs]) continue;
+        if (!(pap[cs] > 0.0)) {  // kernel.cpp:153: this column's CG stops here
+            active[cs] = 0;
+            continue;
+        }
         const double alpha = rs[cs] / pap[cs];
         x[static_cast<size_t>(i) * ldx + c] += alpha * p[static_cast<size_t>(i) * ldp + c];
         r[static_cast<size_t>(i) * ldr + c] -= alpha * ap[static_cast<size_t>(i) * ldap + c];
@@ -480,6 +492,12 @@ extern "C" int bk_coldot_d(int n, const double* x, int ldx, const double* y, int
     auto partial = static_cast<double*>(work);
     coldot_partial<<<dim3(nb, ceil_div(k, 32)), dim3(32, 8), 0, s>>>(n, x, ldx, y, ldy, k, partial);
     sum_partials<<<ceil_div(k, 8), 256, 0, s>>>(nb, k, partial, out);
+    BK_LAUNCHED();
+}
+
+extern "C" int bk_cg_init_d(int k, const double* rs, double* bnorm, int* active, void* stream) {
+    if (k <= 0) return 0;
+    cg_init_kernel<<<ceil_div(k, 256), 256, 0, as_stream(stream)>>>(k, rs, bnorm, active);
     BK_LAUNCHED();
 }
 

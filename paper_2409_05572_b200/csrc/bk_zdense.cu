@@ -26,6 +26,9 @@
 // Split-K partial tiles of the Grams are reduced in a fixed order as in
 // bk_dense.cu (deterministic).  References: rr.cpp:11,13 (S^T AS, S Z),
 // kernel.cpp:76,79 (q^T v, q c), solvers.cpp:195 (hl_trick lifts).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "bk_dense.cuh"
@@ -358,6 +361,199 @@ int zgemm_launch_v(int n, const double* x, int ldx, int d, const double* c, int 
     BK_LAUNCHED();
 }
 
+
+// ------------------------------------------------------------------ update, TMA-fed
+// The same 3M update with the X operand (TM rows x 8 complex = 128-byte rows per
+// stage) moved by the Tensor Memory Accelerator: one cp.async.bulk.tensor box per
+// stage issued by one thread, completion on an mbarrier, 128-byte swizzle (16-byte
+// chunk c of row r lands at chunk c ^ (r & 7)).  The swizzle alone would leave the
+// fragment loads 2-way bank-conflicted (the two rows of a quarter-warp phase XOR
+// their chunks with 0 and 1), so fragment row g of the DMMA reads tile row
+// sigma(g) = 4 (g & 1) + g / 2: the rows of a phase then differ in bit 2 and their
+// chunks cover all 8 of a 128-byte line.  The output rows follow the same map.
+// C (8 k-rows x TN complex) stays on cp.async with its padded pitch.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int TM, int TN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM * WN * 32) zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap tmx, int n,
+                                                                   int d, const double* __restrict__ cm, int ldc,
+                                                                   int k, double alpha, double beta,
+                                                                   double* __restrict__ y, int ldy, int nct,
+                                                                   const int* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;
+    constexpr int TK = 8;                 // complex columns per stage: one 128-byte row
+    constexpr int NT = WM * WN * 32;
+    constexpr int PC = 2 * TN + 4;        // doubles
+    constexpr int XB = TM * 128;          // bytes of one X stage
+    constexpr int FM = TM / WM / 8, FN = TN / WN / 8;
+    static_assert(FM * WM * 8 == TM && FN * WN * 8 == TN, "warp tiling");
+    extern __shared__ __align__(1024) unsigned char zsm[];
+    unsigned char* xs = zsm;                                          // STAGES x XB (1024-aligned)
+    double* cs = reinterpret_cast<double*>(zsm + STAGES * XB);        // STAGES x TK x PC
+    uint64_t* bar = reinterpret_cast<uint64_t*>(cs + STAGES * TK * PC);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int sg = ((g & 1) << 2) | (g >> 1);  // fragment row g -> tile row
+    const int ct = blockIdx.x % nct, rt = blockIdx.x / nct;
+    const int r0 = rt * TM, c0 = ct * TN;
+    const int wm = (warp / WN) * (TM / WM), wn = (warp % WN) * (TN / WN);
+    if (tid == 0) {
+        for (int st = 0; st < STAGES; ++st) mbar_init(bar + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    double acc[3][FM][FN][2];
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) acc[p][mi][ni][0] = acc[p][mi][ni][1] = 0.0;
+
+    const int nk = ceil_div(d, TK);
+    auto load_stage = [&](int kt, int st) {
+        if (tid == 0) {
+            mbar_expect_tx(bar + st, XB);
+            tma_load_2d(xs + st * XB, &tmx, 2 * kt * TK, r0, bar + st);
+        }
+        load_tile16<TK, TN, NT>(cs + st * TK * PC, PC, cm, 2 * ldc, kt * TK, d, 2 * c0, 2 * k, tid);
+    };
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+        if (st < nk) load_stage(st, st);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();  // C stage kt visible; every warp is past stage kt - 1
+        const int nxt = kt + STAGES - 1;
+        if (nxt < nk) load_stage(nxt, nxt % STAGES);
+        cp_async_commit();
+        const int st = kt % STAGES;
+        mbar_wait(bar + st, (kt / STAGES) & 1);
+        const unsigned char* xd = xs + st * XB;
+        const double* cd = cs + st * TK * PC;
+#pragma unroll
+        for (int k4 = 0; k4 < TK; k4 += 4) {
+            double2 xf[FM], cf[FN];
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi) {
+                const int r = wm + mi * 8 + sg;
+                xf[mi] = *reinterpret_cast<const double2*>(xd + r * 128 + (((k4 + t) ^ (r & 7)) << 4));
+            }
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni)
+                cf[ni] = *reinterpret_cast<const double2*>(cd + (k4 + t) * PC + 2 * (wn + ni * 8 + g));
+            double csum[FN], xsum[FM];
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) csum[ni] = cf[ni].x + cf[ni].y;
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi) xsum[mi] = xf[mi].x + xf[mi].y;
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) {
+                    dmma_8x8x4(acc[0][mi][ni][0], acc[0][mi][ni][1], xf[mi].x, cf[ni].x);
+                    dmma_8x8x4(acc[1][mi][ni][0], acc[1][mi][ni][1], xf[mi].y, cf[ni].y);
+                }
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni)
+                    dmma_8x8x4(acc[2][mi][ni][0], acc[2][mi][ni][1], xsum[mi], csum[ni]);
+        }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < FN; ++ni) {
+            const int i = r0 + wm + mi * 8 + sg;
+            const int j = c0 + wn + ni * 8 + 2 * t;
+            if (i >= n) continue;
+            double2* yr = reinterpret_cast<double2*>(y + 2 * static_cast<size_t>(i) * ldy);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (j + h >= k) continue;
+                const double t1 = acc[0][mi][ni][h], t2 = acc[1][mi][ni][h], t3 = acc[2][mi][ni][h];
+                const double re = t1 - t2, im = (t3 - t1) - t2;
+                double2 v;
+                if (beta == 0.0) {
+                    v = make_double2(alpha * re, alpha * im);
+                } else {
+                    const double2 old = yr[j + h];
+                    v = make_double2(fma(alpha, re, beta * old.x), fma(alpha, im, beta * old.y));
+                }
+                yr[j + h] = v;
+            }
+        }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+template <int TM, int TN, int WM, int WN, int ST>
+int zgemm_tma_launch_v(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha,
+                       double beta, double* y, int ldy, cudaStream_t s, const int* run_if) {
+    auto enc = encode_fn();
+    if (!enc) return static_cast<int>(cudaErrorNotSupported);
+    // X as a 2-D tensor of doubles: 2d columns in use, n rows, row pitch 16 ldx bytes
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2) * d, static_cast<cuuint64_t>(n)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 16};
+    const cuuint32_t box[2] = {16, TM};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
+    constexpr size_t smem = ST * TM * 128 + sizeof(double) * ST * 8 * (2 * TN + 4) + ST * 8 + 1024;
+    auto kern = zgemm3m_tma_kernel<TM, TN, WM, WN, ST>;
+    BK_RET(BK_ONCE_PER_DEVICE(prep(kern, smem)));
+    const int nct = ceil_div(k, TN);
+    const int64_t blocks = static_cast<int64_t>(ceil_div(n, TM)) * nct;
+    kern<<<static_cast<unsigned>(blocks), WM * WN * 32, smem, s>>>(map, n, d, c, ldc, k, alpha, beta, y, ldy, nct,
+                                                                  run_if);
+    BK_LAUNCHED();
+}
+
 int zgemm_launch(int n, const double* x, int ldx, int d, const double* c, int ldc, int k, double alpha, double beta,
                  double* y, int ldy, cudaStream_t s, const int* run_if) {
     static const int v = env_int("BK_ZGEMM", 0);
@@ -372,6 +568,10 @@ int zgemm_launch(int n, const double* x, int ldx, int d, const double* c, int ld
             return zgemm_launch_v<64, 48, 8, 2, 2, 4, 3>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
         case 5:  // 32 x 48, 2 warps of 16 x 24... as 2 x 1 warps of 16 x 48
             return zgemm_launch_v<32, 48, 8, 2, 1, 4, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+        case 6:  // TMA-fed X (64 x 48, 4 warps of 32 x 24, 4 stages)
+            return zgemm_tma_launch_v<64, 48, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+        case 7:  // TMA-fed X, 6 stages
+            return zgemm_tma_launch_v<64, 48, 2, 2, 6>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
         default:  // 64 x 48, 4 warps of 32 x 24, 8-deep, 4 stages
             return zgemm_launch_v<64, 48, 8, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
     }

@@ -134,6 +134,7 @@ public:
     const std::vector<double>& val() const { return val_; }  // interleaved when complex
     double diagonal(int i) const;                             // real part; 0 when absent
     double norm_est() const;                                  // estimate_norm2, cached
+    bool norm_cached() const { return norm_cache_->load(std::memory_order_relaxed) >= 0.0; }
     // full (both triangles) CSR on `device`, optionally with negated values (M = -A)
     const DeviceCsr& device_csr(int device, bool negate) const;
     // full (both triangles) CSR: per row the lower entries then the mirrored
