@@ -72,47 +72,125 @@ __global__ void __launch_bounds__(1024) chol_coop_kernel(int a, const double* __
     constexpr double kLo2 = (1.0 - 1e-4) * (1.0 - 1e-4), kHi2 = (1.0 + 1e-4) * (1.0 + 1e-4);
     int kept = 0;
     double worst = 0.0;  // max g_jj / p_j over kept pivots (cond)
-    for (int j = 0; j < a; ++j) {
-        const double p = s[static_cast<size_t>(j) * a + j];
+    // keep decision of a non-odd-twin pivot (the reference's drop rule)
+    auto decide_even = [&](int j, double p, bool& unsure, bool& bad) -> int {
         const double gjj = gd[j];
-        int keep;
-        bool unsure = false, bad = false;
         if (!isfinite(p) || !isfinite(gjj)) {
             bad = true;
-            keep = 0;
-        } else if (pairs && (j & 1)) {
-            keep = slot[j - 1] >= 0 && p > 0.0;
-            unsure = (slot[j - 1] >= 0) != (p > 0.0);
-        } else if (ref2 == nullptr) {
-            keep = p > 0.0;
+            return 0;
+        }
+        if (ref2 == nullptr) {
             unsure = p <= 1e-8 * gjj;
-        } else {
-            const double thr2 = drop2 * r2[j];
-            if (r2[j] == 0.0 || gjj < thr2) {
-                keep = 0;
+            return p > 0.0;
+        }
+        const double thr2 = drop2 * r2[j];
+        if (r2[j] == 0.0 || gjj < thr2) return 0;
+        unsure = p < 1e-8 * gjj || (p > kLo2 * thr2 && p < kHi2 * thr2);
+        return p >= thr2;
+    };
+    if (pairs == 2 && (a & 1) == 0) {
+        // Real embedding of a complex Gram: pivots 2c and 2c + 1 in one grid step
+        // (half the grid barriers).  Bit-identical to the pivot-by-pivot loop
+        // below: every thread forms row 2c + 1's update by pivot 2c on the fly,
+        // f = s[2c][2c+1] / p0, s'[2c+1][l] = s[2c+1][l] - f s[2c][l], with the
+        // same expressions that loop evaluates, and each trailing row receives
+        // the two rank-1 updates in the same order; row 2c + 1 itself is written
+        // back in the next step (nobody reads it there).
+        for (int j = 0; j < a; j += 2) {
+            if (j >= 2 && slot[j - 2] >= 0) {  // deferred write-back of row j - 1
+                const double* rowe = s + static_cast<size_t>(j - 2) * a;
+                double* rowo = s + static_cast<size_t>(j - 1) * a;
+                const double fo = rowe[j - 1] * (1.0 / piv[j - 2]);
+                for (int l = j - 1 + gtid; l < a; l += gthreads) rowo[l] -= fo * rowe[l];
+            }
+            const double* row0 = s + static_cast<size_t>(j) * a;
+            const double* row1 = row0 + a;
+            const double p0 = row0[j];
+            bool unsure0 = false, bad0 = false, bad1 = false;
+            const int keep0 = decide_even(j, p0, unsure0, bad0);
+            const double invp0 = keep0 ? 1.0 / p0 : 0.0;
+            const double f01 = keep0 ? row0[j + 1] * invp0 : 0.0;
+            const double p1 = keep0 ? row1[j + 1] - f01 * row0[j + 1] : row1[j + 1];
+            int keep1;
+            bool unsure1 = false;
+            if (!isfinite(p1) || !isfinite(gd[j + 1])) {
+                bad1 = true;
+                keep1 = 0;
             } else {
-                keep = p >= thr2;
-                unsure = p < 1e-8 * gjj || (p > kLo2 * thr2 && p < kHi2 * thr2);
+                keep1 = keep0 && p1 > 0.0;
+                unsure1 = (keep0 != 0) != (p1 > 0.0);
             }
-        }
-        if (lead) {
-            if (unsure) flags[0] = 1;
-            if (bad) flags[1] = 1;
-            slot[j] = keep ? kept : -1;
-            piv[j] = p;
-        }
-        if (keep) {
-            ++kept;
-            worst = fmax(worst, gjj / p);
-            const double invp = 1.0 / p;
-            const double* rowj = s + static_cast<size_t>(j) * a;
-            for (int k = j + 1 + gw; k < a; k += gwarps) {
-                const double rk = rowj[k] * invp;
-                double* rowk = s + static_cast<size_t>(k) * a;
-                for (int l = k + lane; l < a; l += 32) rowk[l] -= rk * rowj[l];
+            if (lead) {
+                if (unsure0 || unsure1) flags[0] = 1;
+                if (bad0 || bad1) flags[1] = 1;
+                slot[j] = keep0 ? kept : -1;
+                slot[j + 1] = keep1 ? kept + keep0 : -1;
+                piv[j] = p0;
+                piv[j + 1] = p1;
             }
+            if (keep0) worst = fmax(worst, gd[j] / p0);
+            if (keep1) worst = fmax(worst, gd[j + 1] / p1);
+            kept += keep0 + keep1;
+            if (keep0) {
+                const double invp1 = keep1 ? 1.0 / p1 : 0.0;
+                for (int k = j + 2 + gw; k < a; k += gwarps) {
+                    const double rk0 = row0[k] * invp0;
+                    const double s1k = row1[k] - f01 * row0[k];
+                    const double rk1 = s1k * invp1;
+                    double* rowk = s + static_cast<size_t>(k) * a;
+                    for (int l = k + lane; l < a; l += 32) {
+                        double v = rowk[l];
+                        v -= rk0 * row0[l];
+                        if (keep1) v -= rk1 * (row1[l] - f01 * row0[l]);
+                        rowk[l] = v;
+                    }
+                }
+            }
+            grid.sync();
+        }
+        if (a >= 2 && slot[a - 2] >= 0) {  // the last odd row
+            const double* rowe = s + static_cast<size_t>(a - 2) * a;
+            double* rowo = s + static_cast<size_t>(a - 1) * a;
+            const double fo = rowe[a - 1] * (1.0 / piv[a - 2]);
+            for (int l = a - 1 + gtid; l < a; l += gthreads) rowo[l] -= fo * rowe[l];
         }
         grid.sync();
+    } else {
+        for (int j = 0; j < a; ++j) {
+            const double p = s[static_cast<size_t>(j) * a + j];
+            const double gjj = gd[j];
+            int keep;
+            bool unsure = false, bad = false;
+            if (pairs && (j & 1)) {
+                if (!isfinite(p) || !isfinite(gjj)) {
+                    bad = true;
+                    keep = 0;
+                } else {
+                    keep = slot[j - 1] >= 0 && p > 0.0;
+                    unsure = (slot[j - 1] >= 0) != (p > 0.0);
+                }
+            } else {
+                keep = decide_even(j, p, unsure, bad);
+            }
+            if (lead) {
+                if (unsure) flags[0] = 1;
+                if (bad) flags[1] = 1;
+                slot[j] = keep ? kept : -1;
+                piv[j] = p;
+            }
+            if (keep) {
+                ++kept;
+                worst = fmax(worst, gjj / p);
+                const double invp = 1.0 / p;
+                const double* rowj = s + static_cast<size_t>(j) * a;
+                for (int k = j + 1 + gw; k < a; k += gwarps) {
+                    const double rk = rowj[k] * invp;
+                    double* rowk = s + static_cast<size_t>(k) * a;
+                    for (int l = k + lane; l < a; l += 32) rowk[l] -= rk * rowj[l];
+                }
+            }
+            grid.sync();
+        }
     }
     for (size_t e = gtid; e < static_cast<size_t>(a) * a; e += gthreads) {
         const int j = static_cast<int>(e / a), l = static_cast<int>(e % a);
@@ -354,7 +432,10 @@ int chol_launch(int a, const double* g, int ldg, const double* ref2, double drop
         int per_sm = 0;
         BK_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, 1024, 0));
         const int grid = max(1, min(min(ceil_div(a, 32), kSMs), max(per_sm, 1) * kSMs));
-        int aa = a, l1 = ldg, l2 = ldm, pr = pairs ? 1 : 0;
+        // pairs: 2 = the paired-pivot grid step (default), 1 = pivot by pivot
+        // (BK_CHOL_PAIRSTEP=0, read per call: the bit-identity test)
+        const char* ps = getenv("BK_CHOL_PAIRSTEP");
+        int aa = a, l1 = ldg, l2 = ldm, pr = pairs ? ((ps && ps[0] == '0') ? 1 : 2) : 0;
         void* args[] = {&aa, const_cast<double**>(&g), &l1, const_cast<double**>(&ref2), &drop, &m, &l2, &info, &s,
                         &pr, &cond};
         BK_RET(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(chol_coop_kernel), dim3(grid), dim3(1024),

@@ -572,7 +572,13 @@ int zgemm_launch(int n, const double* x, int ldx, int d, const double* c, int ld
             return zgemm_tma_launch_v<64, 48, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
         case 7:  // TMA-fed X, 6 stages
             return zgemm_tma_launch_v<64, 48, 2, 2, 6>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
-        default:  // 64 x 48, 4 warps of 32 x 24, 8-deep, 4 stages
+        case 8:  // cp.async only
+            return zgemm_launch_v<64, 48, 8, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
+        default:  // 64 x 48, 4 warps of 32 x 24, 8-deep, 4 stages; X by TMA when beta = 0 (the lifts and
+                  // the CholQR update: 1152 -> 768 42.5 -> 42.6 TF/s), cp.async when the update also
+                  // reads Y (768 -> 384, beta = 1: 41.4 with cp.async against 40.6 with TMA)
+            if (beta == 0.0)
+                return zgemm_tma_launch_v<64, 48, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
             return zgemm_launch_v<64, 48, 8, 2, 2, 4>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, s, run_if);
     }
 }

@@ -193,6 +193,32 @@ def test_chol_drop_z(bk):
     assert info[1] == 1
 
 
+@pytest.mark.parametrize("a,dep", [(96, False), (384, True)])
+def test_chol_z_paired_step_bit_identical(bk, a, dep):
+    """complex blocks beyond shared memory (2a > 160 real) take the grid-
+    cooperative Cholesky; its default paired-pivot step (pivots 2c, 2c+1 of the
+    real embedding in one grid barrier) must reproduce the pivot-by-pivot loop
+    bit for bit, decisions and R^-1 alike, also with dropped columns"""
+    import os
+    rng = np.random.default_rng(a)
+    w = crandn(rng, 3000, a)
+    if dep:
+        w[:, 40] = 0.0
+        w[:, 77] = 1e-9 * w[:, 77] + (0.3 - 1j) * w[:, 12]
+    out = []
+    for flag in ("1", "0"):
+        os.environ["BK_CHOL_PAIRSTEP"] = flag
+        try:
+            out.append(_chol_z(bk, w))
+        finally:
+            os.environ.pop("BK_CHOL_PAIRSTEP", None)
+    (m2, i2), (m1, i1) = out
+    assert i1 == i2, (i1, i2)
+    assert np.array_equal(m1.view(np.float64), m2.view(np.float64))
+    if dep:
+        assert i1[0] < a
+
+
 def test_spmm_z_magnetic(bk, oracle):
     rp, col, val = W.magnetic(32, 1.0 / 16)
     n = 32 * 32
