@@ -182,6 +182,23 @@ def test_config5_band_and_residuals(product):
     check_block(product, a, w, res, north_star=True)
 
 
+def test_config5_reduced_matches_complex_oracle(product):
+    """config 5's operator at side 256 (nev 32, width 48) against the complex
+    instantiation of the oracle (the reference is real-only, so this pins the
+    complex path to the restated algorithm, not to the reference): same inputs,
+    values to 1e-9, the same (n_now, event, lock) trajectory or a named split
+    (every wanted value sits in the degenerate lowest Landau band, so lock
+    decisions between its pairs are rotation-dependent), iteration counts close"""
+    ref = fixture("cfg5_magnetic_256_nev32")
+    w = W.config5(side=256, nev=32, n_ex=48)
+    assert ref["matrix_sha256"] == W.sha256(w.row_ptr, w.col, w.val)
+    assert ref["x0_sha256"] == W.sha256(w.x0)
+    a, res = run(product, w, max_iters=400)
+    assert res.status == ref["status"] == 0
+    np.testing.assert_allclose(res.values, ref["values"], rtol=1e-9)
+    print("config 5 (side 256) split:", check_trajectory(res, ref, w.cfg["tol"]))
+
+
 def test_config5_full_size(product):
     """BASELINE configs[4] at full size (n = 2^20, complex128, nev 256, width up to
     384): converged, all 256 values within 1e-9 relative of the Harper-chain

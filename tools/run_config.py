@@ -34,7 +34,11 @@ def workload(args):
     elif c == "4":
         w = W.config4(side=args.side or 96)
     elif c == "5":
-        w = W.config5(side=args.side or 1024)
+        side = args.side or 1024
+        if args.nev:  # reduced lattice runs (tests): nev and n_ex given
+            w = W.config5(side=side, nev=args.nev, n_ex=args.n_ex or (3 * args.nev) // 2)
+        else:
+            w = W.config5(side=side)
     else:
         raise SystemExit(f"unknown config {c}")
     if args.strategy and c != "2":
@@ -66,6 +70,7 @@ def main():
     ap.add_argument("--strategy", default=None)
     ap.add_argument("--impl", default="product", choices=["product", "oracle"])
     ap.add_argument("--n_ex", type=int, default=0)
+    ap.add_argument("--nev", type=int, default=0)
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--side", type=int, default=0)
     ap.add_argument("--max_iters", type=int, default=0)
