@@ -366,15 +366,17 @@ inline size_t packed_smem_bytes(int d) {
     return sizeof(double) * (static_cast<size_t>(d) * (d + 1) / 2 + static_cast<size_t>(6 + kPkWarps) * d);
 }
 
-__global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, const double* __restrict__ h, int ldh,
+template <int NT_, int PM, int PR>
+__global__ void __launch_bounds__(NT_, 1) tridiag_packed_kernel(int d, const double* __restrict__ h, int ldh,
                                                                         double* __restrict__ vref,
                                                                         double* __restrict__ tau,
                                                                         double* __restrict__ diag,
                                                                         double* __restrict__ off) {
     extern __shared__ double sm[];
-    __shared__ double red[kPkWarps];
+    __shared__ double red[NT_ / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    constexpr int nt = kPkThreads, nw = kPkWarps;
+    constexpr int nt = NT_, nw = NT_ / 32;
+    static_assert(PR <= 16, "the row reduce-scatter serves 16 rows per warp");
     double* A = sm;  // row i of the lower triangle at A + i(i+1)/2
     double* v = A + static_cast<size_t>(d) * (d + 1) / 2;
     double* vp = v + d;
@@ -432,9 +434,9 @@ __global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, co
         __syncthreads();
         // (2) fused pass over the trailing lower triangle (rows, cols >= j0)
         const int j0 = k + 1;
-        double vj[kPkM], vpj[kPkM], wpj[kPkM], cacc[kPkM];
+        double vj[PM], vpj[PM], wpj[PM], cacc[PM];
 #pragma unroll
-        for (int m = 0; m < kPkM; ++m) {
+        for (int m = 0; m < PM; ++m) {
             const int j = j0 + lane + 32 * m;
             const bool ok = j < d;
             vj[m] = ok ? v[j] : 0.0;
@@ -444,18 +446,18 @@ __global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, co
         }
         // loops leave by warp-uniform breaks: the trailing triangle shrinks with k,
         // and guarded-but-unrolled bodies would be predicated, not skipped
-        double racc[kPkR];
+        double racc[PR];
 #pragma unroll
-        for (int r = 0; r < kPkR; ++r) racc[r] = 0.0;
+        for (int r = 0; r < PR; ++r) racc[r] = 0.0;
 #pragma unroll
-        for (int r = 0; r < kPkR; ++r) {
+        for (int r = 0; r < PR; ++r) {
             const int i = j0 + wid + nw * r;
             if (i >= d) break;
             double* row = rowp(i);
             const double vi = v[i], vpi = vp[i], wpi = wp[i];
             const int mhi = (i - j0) >> 5;  // last chunk holding a j <= i
 #pragma unroll
-            for (int m = 0; m < kPkM; ++m) {
+            for (int m = 0; m < PM; ++m) {
                 if (m > mhi) break;
                 const int j = j0 + lane + 32 * m;
                 if (j <= i) {
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, co
             const bool h1 = lane & 16, h2 = lane & 8, h3 = lane & 4, h4 = lane & 2;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const double lo8 = q < kPkR ? racc[q] : 0.0, hi8 = q + 8 < kPkR ? racc[q + 8] : 0.0;
+                const double lo8 = q < PR ? racc[q] : 0.0, hi8 = q + 8 < PR ? racc[q + 8] : 0.0;
                 v8[q] = (h1 ? hi8 : lo8) + __shfl_xor_sync(0xffffffffu, h1 ? lo8 : hi8, 16);
             }
 #pragma unroll
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(kPkThreads, 1) tridiag_packed_kernel(int d, co
             if (!(lane & 1) && i < d) rp[i] = v1;
         }
 #pragma unroll
-        for (int m = 0; m < kPkM; ++m) {
+        for (int m = 0; m < PM; ++m) {
             const int j = j0 + lane + 32 * m;
             if (j < d) cp[wid * d + j] = cacc[m];
         }
@@ -1637,12 +1639,25 @@ extern "C" int bk_syev_tri_d(int d, const double* h, int ldh, int n_need, double
     bool launched = false;
     static const bool force_coop = getenv("BK_SYEV_COOP") != nullptr;  // tuning runs only
     static const bool no_packed = getenv("BK_TRI_NO_PACKED") != nullptr;  // tuning runs only
-    if (d <= kPackedUseMaxD && !force_coop && !no_packed) {
-        const cudaError_t ap = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(tridiag_packed_kernel,
+    static const bool no_small_packed = getenv("BK_TRI_NO_SMALL_PACKED") != nullptr;  // A/B runs
+    if (d <= 65 && !force_coop && !no_packed && !no_small_packed) {
+        // small projected problems (config 1's SI, d <= 40): 4 warps of <= 16 rows
+        // and 2 column chunks — a 16-warp CTA's barriers cost more than the work
+        auto kern = tridiag_packed_kernel<128, 2, 16>;
+        const cudaError_t ap = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(
+            kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(packed_smem_bytes(65))));
+        BK_RET(ap);
+        kern<<<1, 128, packed_smem_bytes(d), s>>>(d, h, ldh, w.vref, w.tau, w.dg, w.off);
+        BK_RET(cudaGetLastError());
+        launched = true;
+    }
+    if (!launched && d <= kPackedUseMaxD && !force_coop && !no_packed) {
+        auto kern = tridiag_packed_kernel<kPkThreads, kPkM, kPkR>;
+        const cudaError_t ap = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(kern,
                                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                             static_cast<int>(packed_smem_bytes(kPackedMaxD))));
         BK_RET(ap);
-        tridiag_packed_kernel<<<1, kPkThreads, packed_smem_bytes(d), s>>>(d, h, ldh, w.vref, w.tau, w.dg, w.off);
+        kern<<<1, kPkThreads, packed_smem_bytes(d), s>>>(d, h, ldh, w.vref, w.tau, w.dg, w.off);
         BK_RET(cudaGetLastError());
         launched = true;
     }
