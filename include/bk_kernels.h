@@ -34,15 +34,29 @@ extern "C" {
 /* ---- K1 SpMM: Y = A X  (replaces spmv / spmv_block, proj/src/kernel.cpp:8-33) ---- */
 BK_API int bk_spmm_d(int n, const int32_t* row_ptr, const int32_t* col, const double* val,
                      const double* x, int ldx, int k, double* y, int ldy, void* stream);
-/* Cluster-tiled form (same Y, bit-identical): rows regrouped into tiles of `tile`
- * graph-local rows (rowid[i]: original row of ordered row i; rp2 / val2: the
- * full CSR in that order, each row's nonzeros in their original order); code[p]
- * = column, or -(slot + 1) when the column is row rowid[t*tile + slot] of the
- * same tile t — those X rows are read from the tile's shared-memory copy; nzmax >= the
- * largest nonzero count of a tile (its index slice is staged on chip too). */
-BK_API int bk_spmm_tiled_d(int n, int tile, int nzmax, const int32_t* rp2, const int32_t* code,
-                           const double* val2, const int32_t* rowid, const double* x, int ldx, int k, double* y,
-                           int ldy, void* stream);
+/* Window-staged form K1w (same Y, bit-identical): a HOST plan regroups the rows into
+ * tiles of graph-local rows and lists, per tile t, the X rows it needs — window
+ * wrow[wptr[t] .. wptr[t+1]): the tile's own rows first (they are also the Y rows
+ * it writes), then the distinct out-of-tile columns (halo).  rp2 / val2: the full
+ * CSR in tile order (each row's nonzeros in their original order); code[p]: the
+ * window slot of nonzero p.  The kernel stages a window's X rows (a column chunk
+ * at a time) and the tile's index slice in shared memory and reads every
+ * nonzero's X row on chip.  bk_spmm_win_plan: tile = 0 takes 64 rows per tile; wcap = 0
+ * applies the kernel's shared-memory rule (three CTAs per SM with >= 32-column chunks),
+ * wcap > 0 a plain cap on the slots per window; ok = 0 when the windows are too large or
+ * the graph has too little locality (the plain bk_spmm_d is then the kernel to use).
+ * All plan pointers are host memory owned by the plan; the caller uploads them. */
+BK_API int bk_spmm_win_plan(int n, const int32_t* row_ptr, const int32_t* col, const double* val, int tile,
+                            int wcap, void** plan);
+BK_API int bk_spmm_win_plan_info(const void* plan, int* ok, int* tile, int* ntiles, int* wmax, int* nzmax,
+                                 double* loads_per_row);
+BK_API int bk_spmm_win_plan_arrays(const void* plan, const int32_t** rp2, const int32_t** code,
+                                   const double** val2, const int32_t** wptr, const int32_t** wrow,
+                                   int64_t* wrow_len);
+BK_API void bk_spmm_win_plan_free(void* plan);
+BK_API int bk_spmm_win_d(int n, int tile, int ntiles, int wmax, int nzmax, const int32_t* rp2,
+                         const int32_t* code, const double* val2, const int32_t* wptr, const int32_t* wrow,
+                         const double* x, int ldx, int k, double* y, int ldy, void* stream);
 /* complex Hermitian twin: x, y, val interleaved (re, im); ld in complex elements */
 BK_API int bk_spmm_z(int n, const int32_t* row_ptr, const int32_t* col, const double* val,
                      const double* x, int ldx, int k, double* y, int ldy, void* stream);

@@ -402,6 +402,9 @@ int beig_result_diagnostics(const beig_result* r, int* cgs2_fallbacks, int* max_
     return BEIG_OK;
 }
 
+// the oracle has one SpMV loop (kernel.cpp:8-33 restated); no windowed variant
+long long beig_result_spmm_windowed(const beig_result*) { return 0; }
+
 void beig_release_device_cache(void) {}  // no device memory in the oracle
 
 // ---- analysis checks: outside the hot path; not restated by the oracle ----

@@ -134,6 +134,7 @@ SYMBOLS = {
     "beig_result_seconds": (C.c_double, [_P]),
     "beig_result_kernel_stats": (C.c_int, [_P, C.c_int, C.POINTER(KernelStat)]),
     "beig_result_diagnostics": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "beig_result_spmm_windowed": (C.c_longlong, [_P]),
     "beig_release_device_cache": (None, []),
     "beig_result_margins": (C.c_int, [_P, _DP, C.c_int]),
     "beig_harness_project_orthonormalize": (C.c_int, [_DP, C.c_int, C.c_int, _DP, C.c_int, C.c_double, _DP,
@@ -144,7 +145,8 @@ SYMBOLS = {
 REFERENCE_SYMBOLS = [s for s in SYMBOLS if s not in (
     "beig_matrix_from_csr", "beig_zmatrix_from_csr", "beig_matrix_is_complex",
     "beig_solve_ext_default", "beig_solve_ex", "beig_result_vectors_z", "beig_result_seconds",
-    "beig_result_kernel_stats", "beig_result_diagnostics", "beig_release_device_cache",
+    "beig_result_kernel_stats", "beig_result_diagnostics", "beig_result_spmm_windowed",
+    "beig_release_device_cache",
     "beig_harness_project_orthonormalize", "beig_harness_hl_trick", "beig_result_margins")]
 
 
@@ -415,7 +417,10 @@ class Result:
     def diagnostics(self) -> dict:
         fb, sw = C.c_int(), C.c_int()
         self.L.check(self.L.lib.beig_result_diagnostics(self.h, C.byref(fb), C.byref(sw)))
-        return {"cgs2_fallbacks": fb.value, "max_jacobi_sweeps": sw.value}
+        out = {"cgs2_fallbacks": fb.value, "max_jacobi_sweeps": sw.value}
+        if hasattr(self.L.lib, "beig_result_spmm_windowed"):
+            out["spmm_windowed"] = int(self.L.lib.beig_result_spmm_windowed(self.h))
+        return out
 
     @property
     def work(self) -> Work:

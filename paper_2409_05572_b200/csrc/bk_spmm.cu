@@ -245,188 +245,6 @@ __global__ void __launch_bounds__(256) spmm_d_half_kernel(int n, const int32_t* 
         }
 }
 
-// Cluster-tiled SpMM (bk_spmm_tiled_d): the rows are regrouped into tiles of
-// T graph-local rows (host-side BFS clustering, host/matrix.cpp), so most
-// nonzeros of a tile's rows point at rows of the same tile (7-point stencil,
-// T = 64: ~4^3 blobs, ~3/4 of the nonzeros).  A CTA stages, with cp.async, the
-// tile's own X rows AND its index slice (row pointers, original row ids,
-// (code, val) of every nonzero) in shared memory; the products then read all
-// indices and the in-tile X rows on chip and gather only the rest from L2/HBM
-// — one round trip per row (its out-of-tile gathers issued together) instead
-// of three dependent ones (row pointer -> (col, val) -> gathers).  Single
-// buffer, several CTAs per SM: one CTA's staging overlaps the others' products.
-// Per row the arithmetic and its order are the plain kernel's (nonzeros in
-// their original order), so Y is bit-identical.
-template <int VPL>
-__global__ void __launch_bounds__(256) spmm_d_tile_kernel(int n, int T, int ntiles, int nzmax,
-                                                           const int32_t* __restrict__ rp2,
-                                                           const int32_t* __restrict__ code,
-                                                           const double* __restrict__ val,
-                                                           const int32_t* __restrict__ rowid,
-                                                           const double* __restrict__ x, int ldx, int k, int kp,
-                                                           bool v16, double* __restrict__ y, int ldy) {
-    extern __shared__ __align__(16) double win[];  // T x kp X rows | nzmax vals | nzmax codes, T+1 rp, T ids
-    double* sval = win + static_cast<size_t>(T) * kp;
-    int* scode = reinterpret_cast<int*>(sval + nzmax);
-    int* srp = scode + nzmax;
-    int* sid = srp + T + 1;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int r0 = t * T, nr = min(T, n - r0);
-        const int p0 = __ldg(rp2 + r0), p1 = __ldg(rp2 + r0 + nr);
-        // index slice
-        for (int i = tid; i <= nr; i += blockDim.x) cp_async4(srp + i, rp2 + r0 + i);
-        for (int i = tid; i < nr; i += blockDim.x) cp_async4(sid + i, rowid + r0 + i);
-        for (int q = tid; q < p1 - p0; q += blockDim.x) {
-            cp_async4(scode + q, code + p0 + q);
-            cp_async8(sval + q, val + p0 + q, true);
-        }
-        // the tile's X rows: threads split by row, so each loads its row id once
-        const int tpr = max(1, static_cast<int>(blockDim.x) / T);  // threads per row
-        for (int sl = tid / tpr; sl < nr; sl += blockDim.x / tpr) {
-            const int row = __ldg(rowid + r0 + sl);
-            const double* src = x + static_cast<size_t>(row) * ldx;
-            double* dst = win + sl * kp;
-            if (v16) {
-                for (int c2 = (tid % tpr) * 2; c2 < kp; c2 += 2 * tpr) cp_async16(dst + c2, src + c2, true);
-            } else {
-                for (int c = tid % tpr; c < k; c += tpr) cp_async8(dst + c, src + c, true);
-            }
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-        for (int sl = warp; sl < nr; sl += nw) {
-            const int s = srp[sl] - p0, e = srp[sl + 1] - p0;
-            double acc[VPL];
-#pragma unroll
-            for (int u = 0; u < VPL; ++u) acc[u] = 0.0;
-            constexpr int G = 4;
-            for (int q0 = s; q0 < e; q0 += G) {
-                double xv[G][VPL], vv[G];
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    const bool live = q0 + q < e;
-                    const int c = live ? scode[q0 + q] : -1;
-                    vv[q] = live ? sval[q0 + q] : 0.0;
-                    if (c < 0) {  // in-tile row (or padding): shared memory
-                        const double* xr = win + (live ? -c - 1 : 0) * kp + lane;
-#pragma unroll
-                        for (int u = 0; u < VPL; ++u) xv[q][u] = live && lane + 32 * u < k ? xr[32 * u] : 0.0;
-                    } else {
-                        const double* xr = x + static_cast<size_t>(c) * ldx + lane;
-#pragma unroll
-                        for (int u = 0; u < VPL; ++u) xv[q][u] = lane + 32 * u < k ? __ldg(xr + 32 * u) : 0.0;
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < G; ++q)
-                    if (q0 + q < e)
-#pragma unroll
-                        for (int u = 0; u < VPL; ++u) acc[u] = fma(vv[q], xv[q][u], acc[u]);
-            }
-            double* yr = y + static_cast<size_t>(sid[sl]) * ldy + lane;
-#pragma unroll
-            for (int u = 0; u < VPL; ++u)
-                if (lane + 32 * u < k) yr[32 * u] = acc[u];
-        }
-        __syncthreads();  // the buffer is restaged for the next tile
-    }
-}
-
-// Half-warp form of the tiled kernel (16-byte X rows): two rows per warp, each
-// half-warp lane holding 2 columns per 16-byte load, so a nonzero costs half the
-// load / shared-memory instructions per row (the one-row-per-warp form is
-// issue-bound once the gathers stay on chip).
-template <int V2>
-__global__ void __launch_bounds__(256) spmm_d_tile2_kernel(int n, int T, int ntiles, int nzmax,
-                                                            const int32_t* __restrict__ rp2,
-                                                            const int32_t* __restrict__ code,
-                                                            const double* __restrict__ val,
-                                                            const int32_t* __restrict__ rowid,
-                                                            const double* __restrict__ x, int ldx, int k, int kp,
-                                                            double* __restrict__ y, int ldy) {
-    extern __shared__ __align__(16) double win[];  // T x kp X rows | nzmax vals | nzmax codes, T+1 rp, T ids
-    double* sval = win + static_cast<size_t>(T) * kp;
-    int* scode = reinterpret_cast<int*>(sval + nzmax);
-    int* srp = scode + nzmax;
-    int* sid = srp + T + 1;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    const int hl = lane & 15, half = lane >> 4;
-    const int k2 = (k + 1) >> 1, kp2 = kp >> 1, ldx2 = ldx >> 1, ldy2 = ldy >> 1;
-    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
-    const double2* w2 = reinterpret_cast<const double2*>(win);
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int r0 = t * T, nr = min(T, n - r0);
-        const int p0 = __ldg(rp2 + r0), p1 = __ldg(rp2 + r0 + nr);
-        for (int i = tid; i <= nr; i += blockDim.x) cp_async4(srp + i, rp2 + r0 + i);
-        for (int i = tid; i < nr; i += blockDim.x) cp_async4(sid + i, rowid + r0 + i);
-        for (int q = tid; q < p1 - p0; q += blockDim.x) {
-            cp_async4(scode + q, code + p0 + q);
-            cp_async8(sval + q, val + p0 + q, true);
-        }
-        const int tpr = max(1, static_cast<int>(blockDim.x) / T);
-        for (int sl = tid / tpr; sl < nr; sl += blockDim.x / tpr) {
-            const int row = __ldg(rowid + r0 + sl);
-            const double* src = x + static_cast<size_t>(row) * ldx;
-            double* dst = win + sl * kp;
-            for (int c2 = (tid % tpr) * 2; c2 < kp; c2 += 2 * tpr) cp_async16(dst + c2, src + c2, true);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-        for (int sb = 2 * warp; sb < nr; sb += 2 * nw) {
-            const int sl = sb + half;
-            const bool rowok = sl < nr;
-            const int s = rowok ? srp[sl] - p0 : 0, e = rowok ? srp[sl + 1] - p0 : 0;
-            double2 acc[V2];
-#pragma unroll
-            for (int u = 0; u < V2; ++u) acc[u] = make_double2(0.0, 0.0);
-            constexpr int G = 4;
-            for (int q0 = s; q0 < e; q0 += G) {
-                double2 xv[G][V2];
-                double vv[G];
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    const bool live = q0 + q < e;
-                    const int c = live ? scode[q0 + q] : -1;
-                    vv[q] = live ? sval[q0 + q] : 0.0;
-                    if (c < 0) {
-                        const double2* xr = w2 + (live ? -c - 1 : 0) * kp2 + hl;
-#pragma unroll
-                        for (int u = 0; u < V2; ++u)
-                            xv[q][u] = live && hl + 16 * u < k2 ? xr[16 * u] : make_double2(0.0, 0.0);
-                    } else {
-                        const double2* xr = x2 + static_cast<size_t>(c) * ldx2 + hl;
-#pragma unroll
-                        for (int u = 0; u < V2; ++u)
-                            xv[q][u] = hl + 16 * u < k2 ? __ldg(xr + 16 * u) : make_double2(0.0, 0.0);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < G; ++q)
-                    if (q0 + q < e)
-#pragma unroll
-                        for (int u = 0; u < V2; ++u) {
-                            acc[u].x = fma(vv[q], xv[q][u].x, acc[u].x);
-                            acc[u].y = fma(vv[q], xv[q][u].y, acc[u].y);
-                        }
-            }
-            if (rowok) {
-                double* yr = y + static_cast<size_t>(sid[sl]) * ldy;
-#pragma unroll
-                for (int u = 0; u < V2; ++u) {
-                    const int c = 2 * (hl + 16 * u);
-                    if (c + 1 < k) reinterpret_cast<double2*>(yr)[hl + 16 * u] = acc[u];
-                    else if (c < k) yr[c] = acc[u].x;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    (void)ldy2;
-}
-
 // tile rows per CTA step and resident CTAs per SM for spmm_d_kernel
 // (BK_SPMM_TILE / BK_SPMM_CPS override, for tuning runs only)
 struct SpmmShape {
@@ -515,58 +333,4 @@ extern "C" int bk_spmm_z(int n, const int32_t* rp, const int32_t* ci, const doub
     else
         spmm_z_kernel<6><<<grid, 256, 0, s>>>(n, rp, ci, v, xx, ldx, k, yy, ldy, sh.tile);
     BK_LAUNCHED();
-}
-
-extern "C" int bk_spmm_tiled_d(int n, int tile, int nzmax, const int32_t* rp2, const int32_t* code,
-                               const double* val2, const int32_t* rowid, const double* x, int ldx, int k, double* y,
-                               int ldy, void* stream) {
-    if (n <= 0 || k <= 0) return 0;
-    if (tile <= 0 || tile > 256 || nzmax < 0) return static_cast<int>(cudaErrorInvalidValue);
-    const cudaStream_t s = as_stream(stream);
-    // widths beyond 96 run as column chunks of <= 96 (the tile copy holds one chunk)
-    for (int c0 = 0; c0 < k; c0 += 96) {
-        const int kc = min(96, k - c0);
-        const double* xc = x + c0;
-        double* yc = y + c0;
-        const bool v16 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(xc) % 16 == 0);
-        // 16-byte copies take an even width; the extra column is inside the row (ld even > k)
-        const int kp = v16 ? (kc + 1) / 2 * 2 : kc;
-        if (v16 && kp > ldx - c0) return static_cast<int>(cudaErrorInvalidValue);
-        const size_t smem = sizeof(double) * (static_cast<size_t>(tile) * kp + nzmax) +
-                            sizeof(int) * (static_cast<size_t>(nzmax) + 2 * tile + 1);
-        if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidValue);
-        const int ntiles = ceil_div(n, tile);
-        static const int cps = [] {  // BK_SPMM_TILED_CPS: CTAs per SM (tuning runs)
-            const char* e = getenv("BK_SPMM_TILED_CPS");
-            return e ? max(1, atoi(e)) : 4;
-        }();
-        const int grid = max(1, min(ntiles, kSMs * cps));
-        auto launch = [&](auto kern) -> cudaError_t {
-            const cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       static_cast<int>(smem));
-            if (a != cudaSuccess) return a;
-            kern<<<grid, 256, smem, s>>>(n, tile, ntiles, nzmax, rp2, code, val2, rowid, xc, ldx, kc, kp, v16, yc,
-                                         ldy);
-            return cudaGetLastError();
-        };
-        // half-warp rows with 16-byte accesses when X and Y rows allow them
-        static const bool one_row = getenv("BK_SPMM_TILED_1ROW") != nullptr;  // tuning runs
-        const bool y16 = (ldy % 2 == 0) && (reinterpret_cast<uintptr_t>(yc) % 16 == 0);
-        if (v16 && y16 && !one_row) {
-            auto launch2 = [&](auto kern) -> cudaError_t {
-                const cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           static_cast<int>(smem));
-                if (a != cudaSuccess) return a;
-                kern<<<grid, 256, smem, s>>>(n, tile, ntiles, nzmax, rp2, code, val2, rowid, xc, ldx, kc, kp, yc,
-                                             ldy);
-                return cudaGetLastError();
-            };
-            if (kc <= 32) BK_RET(launch2(spmm_d_tile2_kernel<1>));
-            else if (kc <= 64) BK_RET(launch2(spmm_d_tile2_kernel<2>));
-            else BK_RET(launch2(spmm_d_tile2_kernel<3>));
-        } else if (kc <= 32) BK_RET(launch(spmm_d_tile_kernel<1>));
-        else if (kc <= 64) BK_RET(launch(spmm_d_tile_kernel<2>));
-        else BK_RET(launch(spmm_d_tile_kernel<3>));
-    }
-    return 0;
 }

@@ -890,7 +890,8 @@ __global__ void group_kernel(int n_need, const double* __restrict__ lam, const d
     for (int j = 0; j < n_need; ++j)
         if (j == 0 || lam[j] - lam[j - 1] > thr) gstart[g++] = j;
     gstart[g] = n_need;
-    *ngroups = g;
+    ngroups[0] = g;
+    ngroups[1] = g < n_need ? 1 : 0;  // some cluster has several members
 }
 
 // LU of T - lam I by Gaussian elimination with partial pivoting on the
@@ -968,7 +969,7 @@ __device__ void tri_apply(int d, const double* __restrict__ mult, const double* 
 __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restrict__ dg,
                                                      const double* __restrict__ off,
                                                      const double* __restrict__ lam, int n_need,
-                                                     double* __restrict__ u) {
+                                                     double* __restrict__ u, int steps, int from_u) {
     extern __shared__ double ism[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -996,8 +997,14 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
         tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < d ? fabs(off[i]) : 0.0));
     for (int o = 16; o > 0; o >>= 1) tnorm = fmax(tnorm, __shfl_xor_sync(0xffffffffu, tnorm, o));
     const double tiny = DBL_EPSILON * fmax(tnorm, DBL_MIN);
+    double* uj = u + static_cast<size_t>(j) * d;
     // deterministic pseudo-random start (splitmix64 of (j, i)): distinct starts
-    // make the vectors of a degenerate cluster independent
+    // make the vectors of a degenerate cluster independent; from_u: continue from
+    // the vector already in u (the second step, after the clusters of the first
+    // step's vectors were orthonormalised as blocks)
+    if (from_u) {
+        for (int i = lane; i < d; i += 32) b[i] = uj[i];
+    } else
     for (int i = lane; i < d; i += 32) {
         unsigned long long z = (static_cast<unsigned long long>(j) << 32) + static_cast<unsigned long long>(i) +
                                0x9e3779b97f4a7c15ULL;
@@ -1008,11 +1015,18 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
     }
     __syncwarp();
     const double shift = lam[j];
-    // two steps: with the shift accurate to ~eps ||T|| and clusters (gap < 1e-7 ||T||)
-    // treated as blocks, each step shrinks foreign components by <= eps/1e-7
+    // two steps in all (one per launch): with the shift accurate to ~eps ||T|| and
+    // clusters (gap < 1e-7 ||T||) treated as blocks, each step shrinks foreign
+    // components by <= eps/1e-7.  Inside a cluster a step weights the cluster's
+    // eigenvectors by 1/(lam_i - shift), differences of rounding size, so all
+    // members lean towards the same vector; two unbroken steps square that ratio
+    // and once in ~1e4 cluster solves left members parallel to 1e-7 — beyond what
+    // the block Cholesky recovers (config 2 `none`@64, iteration 549: a Ritz
+    // vector of norm^2 1 + 5e-6, the solve stagnated at 2 tol).  The caller
+    // therefore orthonormalises the clusters between the steps.
     if (lane == 0) tri_factor(d, dg, off, shift, tiny, mult, rinv, u1, u2, swp);
     __syncwarp();
-    for (int it = 0; it < 2; ++it) {
+    for (int it = 0; it < steps; ++it) {
         if (lane == 0) tri_apply(d, mult, rinv, u1, u2, swp, b);
         __syncwarp();
         double nn = 0.0;
@@ -1022,7 +1036,6 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
         for (int i = lane; i < d; i += 32) b[i] *= inv;
         __syncwarp();
     }
-    double* uj = u + static_cast<size_t>(j) * d;
     for (int i = lane; i < d; i += 32) uj[i] = b[i];
 }
 
@@ -1035,9 +1048,10 @@ __global__ void __launch_bounds__(1024) group_chol_kernel(int n_need, const doub
                                                            const int* __restrict__ gstart,
                                                            const int* __restrict__ ngroups, double* __restrict__ m,
                                                            double* __restrict__ gwork, int* __restrict__ ginfo,
-                                                           int smem_max_a) {
+                                                           int smem_max_a, const int* __restrict__ run_if) {
     extern __shared__ double dyn_s[];
     const int b = blockIdx.x;
+    if (run_if && *run_if == 0) return;
     if (b >= *ngroups) return;
     const int g0 = gstart[b], g = gstart[b + 1] - g0;
     const size_t o = static_cast<size_t>(g0) * n_need + g0;
@@ -1173,7 +1187,9 @@ __global__ void __launch_bounds__(256) backtr_g_kernel(int d, int n_need, const 
 }
 
 // u (column-major d x k) -> row-major scratch, and back
-__global__ void cm_to_rm_small(int d, int k, const double* __restrict__ cm, double* __restrict__ rm, int ldr) {
+__global__ void cm_to_rm_small(int d, int k, const double* __restrict__ cm, double* __restrict__ rm, int ldr,
+                               const int* __restrict__ run_if = nullptr) {
+    if (run_if && *run_if == 0) return;
     const int64_t total = static_cast<int64_t>(d) * k;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1181,7 +1197,9 @@ __global__ void cm_to_rm_small(int d, int k, const double* __restrict__ cm, doub
         rm[static_cast<size_t>(i) * ldr + c] = cm[e];
     }
 }
-__global__ void rm_to_cm_small(int d, int k, const double* __restrict__ rm, int ldr, double* __restrict__ cm) {
+__global__ void rm_to_cm_small(int d, int k, const double* __restrict__ rm, int ldr, double* __restrict__ cm,
+                               const int* __restrict__ run_if = nullptr) {
+    if (run_if && *run_if == 0) return;
     const int64_t total = static_cast<int64_t>(d) * k;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1514,38 +1532,52 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
     else
         bisect_kernel<<<ceil_div(n_need * 32, 64), 64, bsm, s>>>(d, w.dg, w.off, n_need, values, w.e2);
     group_kernel<<<1, 32, 0, s>>>(n_need, values, w.dg, w.off, d, w.gstart, w.ngroups);
-    {
-        const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 2 * (5 * static_cast<size_t>(d) + (d + 7) / 8));
-        const cudaError_t ai = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           static_cast<int>(sizeof(double) * 14 * kSyevMaxD)));
-        BK_RET(ai);
-        invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u);
-    }
-    cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need);
+    const int* has_clusters = w.ngroups + 1;  // device flag: some cluster has several members
+    // Schur complement in shared memory for clusters up to smax columns
+    int smax = n_need < 160 ? n_need : 160;
+    while (smax > 0 && static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8 > 28800) --smax;
+    const size_t gsm = sizeof(double) * (static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8);
+    BK_RET(BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(group_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   226 * 1024)));
+    const size_t ism = sizeof(double) * (2 * static_cast<size_t>(d) + 2 * (5 * static_cast<size_t>(d) + (d + 7) / 8));
+    BK_RET(BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(sizeof(double) * 14 * kSyevMaxD))));
     // clusters -> orthonormal blocks: Gram, per-cluster Cholesky (block-diagonal
-    // R^{-1}), update
-    {
-        int rc = bk_gram_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work, stream);
+    // R^{-1}), update; run_if: only when some cluster has several members
+    auto cluster_step = [&](const int* run_if) -> int {
+        cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need, run_if);
+        int rc = run_if ? bk_gram_if_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work,
+                                       run_if, stream)
+                        : bk_gram_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work, stream);
         if (rc) return rc;
         BK_RET(cudaMemsetAsync(w.m, 0, sizeof(double) * n_need * n_need, s));
-        // Schur complement in shared memory for clusters up to smax columns
-        int smax = n_need < 160 ? n_need : 160;
-        while (smax > 0 && static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8 > 28800) --smax;
-        const size_t gsm = sizeof(double) * (static_cast<size_t>(smax) * smax + 4 * static_cast<size_t>(n_need) + 8);
-        const cudaError_t ag = BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(group_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           226 * 1024));
-        BK_RET(ag);
-        group_chol_kernel<<<n_need, 1024, gsm, s>>>(n_need, w.gram, w.gstart, w.ngroups, w.m, w.scratch,
-                                                    w.ginfo, smax);
-        rc = bk_gemm_d(d, w.urm, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, w.u2rm, n_need, stream);
+        group_chol_kernel<<<n_need, 1024, gsm, s>>>(n_need, w.gram, w.gstart, w.ngroups, w.m, w.scratch, w.ginfo,
+                                                    smax, run_if);
+        return run_if ? bk_gemm_if_d(d, w.urm, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, w.u2rm, n_need, run_if,
+                                     stream)
+                      : bk_gemm_d(d, w.urm, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, w.u2rm, n_need, stream);
+    };
+    // inverse iteration, two steps; the clusters of the first step's vectors are
+    // orthonormalised before the second (see invit_kernel), skipped on the device
+    // when every wanted eigenvalue is isolated
+    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 0);
+    {
+        const int rc = cluster_step(has_clusters);
+        if (rc) return rc;
+        rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u2rm, n_need, w.u, has_clusters);
+    }
+    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 1);
+    {
+        const int rc = cluster_step(nullptr);
         if (rc) return rc;
     }
-    // two Newton-Schulz steps U <- U (3I - U^T U)/2: after the cluster step the
+    // three Newton-Schulz steps U <- U (3I - U^T U)/2: after the cluster step the
     // columns are orthonormal to O(eps ||T|| / gap) (gap >= 1e-7 ||T|| between
-    // clusters), so the error squares twice to ~1e-16 — GEMM-only
-    for (int pass = 0; pass < 2; ++pass) {
-        double* src = pass == 0 ? w.u2rm : w.urm;
-        double* dst = pass == 0 ? w.urm : w.u2rm;
+    // clusters) and a cluster's members to eps cond(G_cluster); the error squares
+    // per step (0.02 -> 3e-4 -> 7e-8 -> 4e-15) — GEMM-only
+    for (int pass = 0; pass < 3; ++pass) {
+        double* src = pass == 1 ? w.urm : w.u2rm;
+        double* dst = pass == 1 ? w.u2rm : w.urm;
         int rc = bk_gram_d(d, src, n_need, n_need, src, n_need, n_need, w.gram, n_need, gram_work, stream);
         if (rc) return rc;
         rc = bk_ns_coeff_d(n_need, w.gram, n_need, w.m, n_need, stream);
@@ -1553,7 +1585,6 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
         rc = bk_gemm_d(d, src, n_need, n_need, w.m, n_need, n_need, 1.0, 0.0, dst, n_need, stream);
         if (rc) return rc;
     }
-    std::swap(w.urm, w.u2rm);  // result in u2rm -> name it urm below
     rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.urm, n_need, w.u);
     BK_LAUNCHED();
 }

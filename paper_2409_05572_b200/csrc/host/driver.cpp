@@ -324,15 +324,23 @@ private:
         captured_ = 0;
     }
     double gap_ms_[K_CLASSES] = {};
+    int64_t spmm_win_calls_ = 0;  // K1 launches that ran as K1w
 
     // K1: algorithmic bytes nnz*12 + (n+1)*4 + 2*n*k*8
     void spmm(Blk x, int k, Blk y) {
         if (k <= 0) return;
         auto t = prof_begin();
-        if (cw_ == 1 && csr_->tile > 0)
-            BKC(bk_spmm_tiled_d(n_, csr_->tile, csr_->tile_nzmax, csr_->rp2.as<int32_t>(), csr_->code.as<int32_t>(),
-                                csr_->val2.d(), csr_->rowid.as<int32_t>(), x.p, x.ld, k, y.p, y.ld, st()));
-        else if (cw_ == 1)
+        // K1w once the handle's window plan is ready (bit-identical to K1, so the
+        // switch can happen mid-solve); 16-byte aligned views only
+        const bool win = cw_ == 1 && csr_->win_state.load(std::memory_order_acquire) == 2 && k >= 8 &&
+                         x.ld % 2 == 0 && y.ld % 2 == 0 && reinterpret_cast<uintptr_t>(x.p) % 16 == 0 &&
+                         reinterpret_cast<uintptr_t>(y.p) % 16 == 0;
+        if (win) {
+            const DeviceCsr::Win& w = csr_->win;
+            BKC(bk_spmm_win_d(n_, w.tile, w.ntiles, w.wmax, w.nzmax, w.rp2.as<int32_t>(), w.code.as<int32_t>(),
+                              w.val2.d(), w.wptr.as<int32_t>(), w.wrow.as<int32_t>(), x.p, x.ld, k, y.p, y.ld, st()));
+            ++spmm_win_calls_;
+        } else if (cw_ == 1)
             BKC(bk_spmm_d(n_, csr_->row_ptr.as<int32_t>(), csr_->col.as<int32_t>(), csr_->val.d(), x.p, x.ld, k, y.p,
                           y.ld, st()));
         else
@@ -868,6 +876,7 @@ private:
         out_.work.rr_dim = meter_.iter_rr_dim;
         out_.rr_flops = meter_.rr_flops;
         out_.cgs2_fallbacks = fallbacks_;
+        out_.spmm_windowed = spmm_win_calls_;
         if (std::getenv("BLOCKEIG_TIMING"))
             std::fprintf(stderr, "[blockeig] second Gram-Schmidt pass taken in %lld of %lld orthonormalisations; "
                          "speculative iterations %lld, redone %lld\n",

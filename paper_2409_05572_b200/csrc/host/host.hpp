@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <new>
 #include <cstdint>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <random>
@@ -103,6 +104,23 @@ private:
 // empty the device block cache (see matrix.cpp)
 void release_device_cache();
 
+// Host plan of the window-staged SpMM (K1w, host/tiling.cpp): rows regrouped into
+// tiles of graph-local rows; window t = wrow[wptr[t] .. wptr[t+1]) lists the X rows
+// tile t needs (its own rows first, then the halo); code[p] is the window slot of
+// nonzero p (rows in tile order, each row's nonzeros in their original order).
+struct WindowPlan {
+    bool ok = false;
+    int n = 0, tile = 0, ntiles = 0, wmax = 0, nzmax = 0;
+    double loads_per_row = 0.0;  // window slots per matrix row (X-row loads from L2)
+    std::vector<int32_t> rp2, code, wptr, wrow;
+    std::vector<double> val2;
+};
+double cluster_rows(int n, const int32_t* rp, const int32_t* col, int tile, std::vector<int32_t>& order);
+void build_windows(int n, const int32_t* rp, const int32_t* col, const double* val, int per, int tile,
+                   const std::vector<int32_t>& order, WindowPlan& w);
+bool plan_windows(int n, const int32_t* rp, const int32_t* col, const double* val, int per, int tile_req,
+                  int wcap, WindowPlan& w);
+
 // ---------------------------------------------------------------- matrix
 // Lower-triangle CSR with the reference invariants (proj/src/matio.cpp:17-35):
 // int64 row_ptr, int32 strictly increasing columns <= row.  Immutable after
@@ -114,11 +132,19 @@ struct DeviceCsr {
     int64_t nnz_full = 0;
     DevMem row_ptr, col, val;
     bool negated = false;
-    // cluster-tiled copy for bk_spmm_tiled_d (tile == 0: not built, the graph has
-    // too little locality); see cluster_rows() in host/matrix.cpp
-    int tile = 0, tile_nzmax = 0;
-    double in_tile_frac = 0.0;
-    DevMem rp2, code, val2, rowid;
+    // window-staged SpMM (K1w, bk_spmm_win_d): the plan is built and uploaded by a
+    // host thread started with the first solve on a real matrix of >= 65536 rows;
+    // win_state: 0 not started, 1 building, 2 ready, 3 unsuitable (or failed).
+    // K1w is bit-identical to the plain kernel, so a solve switches over as soon
+    // as the state reads 2.
+    struct Win {
+        int tile = 0, ntiles = 0, wmax = 0, nzmax = 0;
+        double loads_per_row = 0.0, plan_seconds = 0.0;
+        DevMem rp2, code, val2, wptr, wrow;
+    };
+    mutable std::atomic<int> win_state{0};
+    mutable Win win;
+    mutable std::future<void> win_job;  // joined by the destructor (std::async future)
 };
 
 class SparseSym {
@@ -159,6 +185,12 @@ private:
         std::mutex full_mu;
         bool full_ready = false;
         FullCsr full;
+        // the window-plan threads of the entries read `full`: join them before any
+        // member goes away (members are destroyed last-declared first)
+        ~DevCache() {
+            for (auto& e : entries)
+                if (e && e->win_job.valid()) e->win_job.wait();
+        }
     };
     std::shared_ptr<DevCache> dev_;
 };
@@ -285,6 +317,7 @@ struct SolveOutput {
     // device-side diagnostics (not part of the reference record)
     int cgs2_fallbacks = 0;
     int max_jacobi_sweeps = 0;
+    int64_t spmm_windowed = 0;  // K1 launches that ran as the window-staged K1w
     KernelStat kstats[K_CLASSES];
 };
 

@@ -6,9 +6,11 @@
 #include <algorithm>
 #include <atomic>
 #include <cctype>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <future>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -297,72 +299,6 @@ double SparseSym::norm_est() const {
     return est;
 }
 
-namespace {
-// Graph-local row order for the cluster-tiled SpMM: rows are grouped into tiles
-// of `tile` rows grown greedily over the sparsity graph — each step takes the
-// unplaced row with the most neighbours already in the tile (oldest first among
-// equals), which grows compact, cube-like blobs (7-point stencil, tile 64: 80 %
-// of the nonzeros in-tile, against 64 % for breadth-first balls); a tile is
-// seeded from the oldest row the previous tiles reached, so consecutive tiles
-// are neighbours.  Returns the order (ordered index -> row) and the fraction of
-// nonzeros whose column lies in the row's own tile.
-double cluster_rows(int n, const std::vector<int32_t>& rp, const std::vector<int32_t>& col, int tile,
-                    std::vector<int32_t>& order) {
-    order.clear();
-    order.reserve(n);
-    std::vector<int32_t> tile_of(static_cast<size_t>(n), -1), gain(static_cast<size_t>(n), 0);
-    std::vector<int32_t> frontier;  // global FIFO of reached rows (may repeat)
-    size_t fhead = 0;
-    int next_seed = 0;
-    constexpr int kB = 16;  // gain buckets (gains >= 15 share the last)
-    std::vector<int32_t> bucket[kB];
-    size_t bhead[kB];
-    std::vector<int32_t> touched;
-    while (static_cast<int>(order.size()) < n) {
-        const int t = static_cast<int>(order.size()) / tile;
-        const size_t start = order.size();
-        for (int g = 0; g < kB; ++g) {
-            bucket[g].clear();
-            bhead[g] = 0;
-        }
-        touched.clear();
-        auto seed = [&]() {
-            while (fhead < frontier.size() && tile_of[frontier[fhead]] >= 0) ++fhead;
-            if (fhead < frontier.size()) return frontier[fhead++];
-            while (next_seed < n && tile_of[next_seed] >= 0) ++next_seed;
-            return next_seed < n ? next_seed : -1;
-        };
-        while (order.size() - start < static_cast<size_t>(tile)) {
-            int u = -1;
-            for (int g = kB - 1; g > 0 && u < 0; --g) {
-                auto& b = bucket[g];
-                while (bhead[g] < b.size() &&
-                       (tile_of[b[bhead[g]]] >= 0 || std::min(gain[b[bhead[g]]], kB - 1) != g))
-                    ++bhead[g];
-                if (bhead[g] < b.size()) u = b[bhead[g]++];
-            }
-            if (u < 0 && (u = seed()) < 0) break;
-            tile_of[u] = t;
-            order.push_back(u);
-            for (int32_t p = rp[u]; p < rp[u + 1]; ++p) {
-                const int c = col[p];
-                if (tile_of[c] >= 0) continue;
-                if (gain[c]++ == 0) touched.push_back(c);
-                bucket[std::min(gain[c], kB - 1)].push_back(c);
-            }
-        }
-        for (int c : touched) {
-            if (tile_of[c] < 0) frontier.push_back(c);
-            gain[c] = 0;
-        }
-    }
-    int64_t in = 0;
-    for (int r = 0; r < n; ++r)
-        for (int32_t p = rp[r]; p < rp[r + 1]; ++p) in += tile_of[col[p]] == tile_of[r];
-    return rp[n] ? static_cast<double>(in) / rp[n] : 0.0;
-}
-}  // namespace
-
 // Expand the lower triangle to full CSR (int32) and upload once per
 // (device, sign); the upper entries are the mirrored (conjugated) lower ones.
 const SparseSym::FullCsr& SparseSym::full_csr() const {
@@ -453,47 +389,65 @@ const DeviceCsr& SparseSym::device_csr(int device, bool negate) const {
         cuda_check(cudaMemcpy(e->col.as<void>(), fcol.data(), sizeof(int32_t) * fcol.size(), cudaMemcpyHostToDevice), "upload");
         cuda_check(cudaMemcpy(e->val.as<void>(), fval.data(), sizeof(double) * fval.size(), cudaMemcpyHostToDevice), "upload");
     }
-    // cluster-tiled copy (real matrices; BLOCKEIG_SPMM_TILE = rows per tile).  Off by
-    // default: at parity with the plain K1 on config 2 (BFS tiles of 64 rows keep
-    // 64 % of the stencil's nonzeros in-tile), and it adds the clustering to a
-    // fresh handle's first solve
-    static const int tile = [] {
-        const char* v = std::getenv("BLOCKEIG_SPMM_TILE");
-        return v ? std::max(0, std::min(256, std::atoi(v))) : 0;
+    // window-staged SpMM plan (K1w): clustering, windows and their upload run on a
+    // host thread so a fresh handle's first solve starts at once on the plain
+    // kernel and switches over when the plan is ready (bit-identical products).
+    // Real matrices of >= 65536 rows; BLOCKEIG_SPMM_WIN=0 keeps the plain kernel.
+    // (BLOCKEIG_SPMM_WIN=2: wait for the plan here — tests and kernel timing runs)
+    static const int win_mode = [] {
+        const char* v = std::getenv("BLOCKEIG_SPMM_WIN");
+        return v ? std::atoi(v) : 1;
     }();
-    if (!complex_ && tile > 0 && n_ >= 8 * tile && nnz) {
-        std::vector<int32_t> order;
-        const double frac = cluster_rows(n_, frp, fcol, tile, order);
-        if (frac >= 0.5) {  // enough locality to pay for the shared-memory copy
-            std::vector<int32_t> pos(static_cast<size_t>(n_));
-            for (int i = 0; i < n_; ++i) pos[order[i]] = i;
-            std::vector<int32_t> rp2(static_cast<size_t>(n_) + 1, 0), code(static_cast<size_t>(nnz));
-            std::vector<double> val2(static_cast<size_t>(nnz));
-            int64_t q = 0;
-            for (int i = 0; i < n_; ++i) {
-                const int r = order[i];
-                for (int32_t p = frp[r]; p < frp[r + 1]; ++p, ++q) {
-                    const int c = fcol[p];
-                    code[q] = pos[c] / tile == i / tile ? -(pos[c] % tile) - 1 : c;
-                    val2[q] = fval[p];
+    const bool win_off = win_mode == 0;
+    if (!complex_ && !win_off && n_ >= 65536 && nnz) {
+        DeviceCsr* ep = e.get();
+        const FullCsr* fp = &full;  // owned by dev_, which outlives the entry
+        const bool neg_vals = negate;
+        ep->win_state.store(1, std::memory_order_release);
+        ep->win_job = std::async(std::launch::async, [ep, fp, neg_vals, device] {
+            try {
+                const auto t0 = std::chrono::steady_clock::now();
+                WindowPlan w;
+                const int n = static_cast<int>(fp->rp.size()) - 1;
+                std::vector<double> nv;
+                if (neg_vals) {
+                    nv.resize(fp->val.size());
+                    for (size_t i = 0; i < nv.size(); ++i) nv[i] = -fp->val[i];
                 }
-                rp2[i + 1] = static_cast<int32_t>(q);
+                const bool ok = plan_windows(n, fp->rp.data(), fp->col.data(), neg_vals ? nv.data() : fp->val.data(), 1,
+                                             0, 0, w);
+                if (!ok) {
+                    ep->win_state.store(3, std::memory_order_release);
+                    return;
+                }
+                cuda_check(cudaSetDevice(device), "cudaSetDevice");
+                cudaStream_t st = nullptr;
+                cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+                auto up = [&](DevMem& d, const void* src, size_t bytes) {
+                    d.alloc(bytes);
+                    cuda_check(cudaMemcpyAsync(d.p(), src, bytes, cudaMemcpyHostToDevice, st), "upload");
+                };
+                DeviceCsr::Win& o = ep->win;
+                up(o.rp2, w.rp2.data(), sizeof(int32_t) * w.rp2.size());
+                up(o.code, w.code.data(), sizeof(int32_t) * w.code.size());
+                up(o.val2, w.val2.data(), sizeof(double) * w.val2.size());
+                up(o.wptr, w.wptr.data(), sizeof(int32_t) * w.wptr.size());
+                up(o.wrow, w.wrow.data(), sizeof(int32_t) * w.wrow.size());
+                const cudaError_t se = cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+                cuda_check(se, "upload");
+                o.tile = w.tile;
+                o.ntiles = w.ntiles;
+                o.wmax = w.wmax;
+                o.nzmax = w.nzmax;
+                o.loads_per_row = w.loads_per_row;
+                o.plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                ep->win_state.store(2, std::memory_order_release);
+            } catch (...) {  // no plan: the plain kernel stays in use
+                ep->win_state.store(3, std::memory_order_release);
             }
-            int nzmax = 0;
-            for (int i = 0; i < n_; i += tile)
-                nzmax = std::max(nzmax, rp2[std::min(n_, i + tile)] - rp2[i]);
-            e->tile = tile;
-            e->tile_nzmax = nzmax;
-            e->in_tile_frac = frac;
-            e->rp2.alloc(sizeof(int32_t) * rp2.size());
-            e->code.alloc(sizeof(int32_t) * code.size());
-            e->val2.alloc(sizeof(double) * val2.size());
-            e->rowid.alloc(sizeof(int32_t) * order.size());
-            cuda_check(cudaMemcpy(e->rp2.as<void>(), rp2.data(), sizeof(int32_t) * rp2.size(), cudaMemcpyHostToDevice), "upload");
-            cuda_check(cudaMemcpy(e->code.as<void>(), code.data(), sizeof(int32_t) * code.size(), cudaMemcpyHostToDevice), "upload");
-            cuda_check(cudaMemcpy(e->val2.as<void>(), val2.data(), sizeof(double) * val2.size(), cudaMemcpyHostToDevice), "upload");
-            cuda_check(cudaMemcpy(e->rowid.as<void>(), order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice), "upload");
-        }
+        });
+        if (win_mode == 2) ep->win_job.wait();
     }
     cudaSetDevice(prev);
     dev_->entries.push_back(std::move(e));

@@ -172,3 +172,44 @@ def explain_divergence(hg, ho, mg, mo, i, tol, slack=10.0, values=None):
         if not math.isnan(slope) and abs(slope) <= 100 * dr:
             cands.append(("slope test", slope, 100 * dr))
     return cands[0] if cands else None
+
+
+def spmm_window_plan(lib, n, frp, fcol, fval, tile=0, wcap=0):
+    """Host plan of the window-staged SpMM (bk_spmm_win_plan, include/bk_kernels.h)
+    as numpy arrays: dict(ok, tile, ntiles, wmax, nzmax, loads_per_row, rp2, code,
+    val2, wptr, wrow).  `lib` is the ctypes CDLL of libblockeig_b200.so."""
+    import ctypes as C
+    lib.bk_spmm_win_plan.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                     C.POINTER(C.c_void_p)]
+    lib.bk_spmm_win_plan_info.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 5 + [C.POINTER(C.c_double)]
+    lib.bk_spmm_win_plan_arrays.argtypes = [C.c_void_p] + [C.POINTER(C.c_void_p)] * 5 + [C.POINTER(C.c_int64)]
+    lib.bk_spmm_win_plan_free.argtypes = [C.c_void_p]
+    lib.bk_spmm_win_plan_free.restype = None
+    frp = np.ascontiguousarray(frp, dtype=np.int32)
+    fcol = np.ascontiguousarray(fcol, dtype=np.int32)
+    fval = np.ascontiguousarray(fval, dtype=np.float64)
+    h = C.c_void_p()
+    rc = lib.bk_spmm_win_plan(n, frp.ctypes.data, fcol.ctypes.data, fval.ctypes.data, tile, wcap, C.byref(h))
+    assert rc == 0, rc
+    ok, t, nt, wmax, nzmax = (C.c_int() for _ in range(5))
+    lpr = C.c_double()
+    assert lib.bk_spmm_win_plan_info(h, ok, t, nt, wmax, nzmax, lpr) == 0
+    ptrs = [C.c_void_p() for _ in range(5)]
+    wl = C.c_int64()
+    assert lib.bk_spmm_win_plan_arrays(h, *[C.byref(q) for q in ptrs], C.byref(wl)) == 0
+    nnz = int(frp[-1])
+
+    def arr(q, ctype, count, dt):
+        if count == 0 or not q.value:
+            return np.zeros(0, dtype=dt)
+        return np.ctypeslib.as_array(C.cast(q, C.POINTER(ctype)), shape=(count,)).astype(dt, copy=True)
+    built = nt.value > 0
+    out = dict(ok=ok.value, tile=t.value, ntiles=nt.value, wmax=wmax.value, nzmax=nzmax.value,
+               loads_per_row=lpr.value,
+               rp2=arr(ptrs[0], C.c_int32, n + 1 if built else 0, np.int32),
+               code=arr(ptrs[1], C.c_int32, nnz if built else 0, np.int32),
+               val2=arr(ptrs[2], C.c_double, nnz if built else 0, np.float64),
+               wptr=arr(ptrs[3], C.c_int32, nt.value + 1 if built else 0, np.int32),
+               wrow=arr(ptrs[4], C.c_int32, wl.value, np.int32))
+    lib.bk_spmm_win_plan_free(h)
+    return out

@@ -176,6 +176,45 @@ def test_speculative_equals_synchronous(product):
         assert spec[k] == sync[k], k
 
 
+WIN_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+from paper_2409_05572_b200 import load
+from paper_2409_05572_b200 import workloads as W
+L = load()
+side = 42  # 74088 rows: above the 65536-row threshold of the window plan
+rp, col, val = W.grid_laplacian((side,) * 3)
+n = side ** 3
+out = {{}}
+for solver, kw in (("lobpcg", dict(n_ev=12, n_ex=20, max_iters=40, precond=1)), ("sd", dict(n_ev=6, n_ex=10, max_iters=25)),
+                   ("tracemin", dict(n_ev=6, n_ex=10, max_iters=6))):
+    a = L.from_csr(n, rp, col, val)
+    r = L.solve(a, solver, seed=5, tol=1e-9, strategy=L.strategy_config("fix"), **kw)
+    out[solver] = dict(status=r.status, values=list(map(float, r.values)), windowed=r.diagnostics["spmm_windowed"],
+                       hist=[[h["r_overall"], h["n_now"], h["event"], h["lock_count"], h["spmv_cols"]] for h in r.history],
+                       vec_sum=float(np.abs(r.vectors).sum()))
+print(json.dumps(out))
+"""
+
+
+def test_windowed_spmm_equals_plain_in_solves(product):
+    """Solves whose SpMM runs as the window-staged K1w (BLOCKEIG_SPMM_WIN=2: the plan
+    is awaited, every launch of >= 8 columns windowed) give the same history, values
+    and vectors, bit for bit, as solves on the plain K1 (BLOCKEIG_SPMM_WIN=0)."""
+    outs = []
+    for mode in ("2", "0"):
+        r = subprocess.run([sys.executable, "-c", WIN_SCRIPT.format(root=ROOT)], capture_output=True, text=True,
+                           env=dict(os.environ, BLOCKEIG_SPMM_WIN=mode), timeout=900, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    win, plain = outs
+    for k in win:
+        assert win[k]["windowed"] > 0 and plain[k]["windowed"] == 0, (k, win[k]["windowed"], plain[k]["windowed"])
+        for f in ("status", "values", "hist", "vec_sum"):
+            assert win[k][f] == plain[k][f], (k, f)
+
+
 # ---------------------------------------------------------------- acceptance (acceptance_test.cpp)
 def test_acceptance_solver_oracle(product):
     """acceptance_test.cpp:135-187: laplacian1d:400, n_ev 10, every solver x

@@ -86,44 +86,58 @@ def test_spmm_vs_oracle(bk, oracle, k):
     assert torch.equal(y2[:, :k], yd[:, :k])
 
 
-@pytest.mark.parametrize("k", [7, 40, 69, 96, 138])
-@pytest.mark.parametrize("perm", [False, True])
-def test_spmm_tiled_bit_identical(bk, k, perm):
-    """Cluster-tiled K1 (in-tile X rows from shared memory) == plain K1, bit for bit,
-    for any row order: each row's nonzeros keep their order."""
+@pytest.mark.parametrize("k", [1, 7, 26, 40, 69, 96, 138, 161, 300])
+@pytest.mark.parametrize("dims,tile,off", [((12, 11, 10), 64, 0), ((23, 19), 32, 8), ((31, 30, 29), 64, 0)])
+def test_spmm_windowed_bit_identical(bk, k, dims, tile, off):
+    """Window-staged K1w (X rows of a tile's window staged in shared memory by bulk
+    copies, column chunk by column chunk) == plain K1, bit for bit: each row keeps
+    its nonzeros in CSR order.  Covers ragged last tiles, odd widths, widths over
+    several chunks and X / Y views at a column offset inside wider blocks."""
     from paper_2409_05572_b200.workloads import grid_laplacian, full_from_lower
-    rp, col, val = grid_laplacian((12, 11, 10))
-    n = 12 * 11 * 10
+    from tests.helpers import spmm_window_plan
+    rp, col, val = grid_laplacian(dims)
+    n = int(np.prod(dims))
     full = full_from_lower(n, rp, col, val)
-    frp, fcol, fval = full.indptr.astype(np.int32), full.indices.astype(np.int32), full.data
-    tile = 64
-    order = np.random.default_rng(k).permutation(n).astype(np.int32) if perm else np.arange(n, dtype=np.int32)
-    pos = np.empty(n, dtype=np.int64)
-    pos[order] = np.arange(n)
-    rp2, code, val2 = [0], [], []
-    for i, r in enumerate(order):
-        for p in range(frp[r], frp[r + 1]):
-            c = fcol[p]
-            code.append(-(pos[c] % tile) - 1 if pos[c] // tile == i // tile else c)
-            val2.append(fval[p])
-        rp2.append(len(code))
-    ld = (k + 7) // 8 * 8 + 8
+    frp, fcol = full.indptr.astype(np.int32), full.indices.astype(np.int32)
+    fval = np.random.default_rng(7).standard_normal(full.data.size)  # distinct values: order matters
+    p = spmm_window_plan(bk, n, frp, fcol, fval, tile=tile, wcap=1 << 20)
+    ld = (k + 7) // 8 * 8 + 8 + off
     x = torch.randn(n, ld, dtype=torch.float64, device="cuda")
-    y1 = torch.zeros_like(x)
-    y2 = torch.zeros_like(x)
+    y1 = torch.full_like(x, 3.0)
+    y2 = torch.full_like(x, 3.0)
     f = bk
-    f.bk_spmm_tiled_d.argtypes = [C.c_int, C.c_int, C.c_int] + [_D] * 5 + [C.c_int, C.c_int, _D, C.c_int, _D]
-    nzmax = max(rp2[min(n, i + tile)] - rp2[i] for i in range(0, n, tile))
+    f.bk_spmm_win_d.argtypes = [C.c_int] * 5 + [_D] * 5 + [_D, C.c_int, C.c_int, _D, C.c_int, _D]
     t_rp, t_c, t_v = dev(frp), dev(fcol), dev(fval)
-    assert f.bk_spmm_d(n, ptr(t_rp), ptr(t_c), ptr(t_v), ptr(x), ld, k, ptr(y1), ld, stream()) == 0
-    r2 = dev(np.array(rp2, dtype=np.int32))
-    c2 = dev(np.array(code, dtype=np.int32))
-    v2 = dev(np.array(val2))
-    oid = dev(order)
-    assert f.bk_spmm_tiled_d(n, tile, nzmax, ptr(r2), ptr(c2), ptr(v2), ptr(oid), ptr(x), ld, k, ptr(y2), ld,
-                             stream()) == 0
+    xo = C.c_void_p(x.data_ptr() + 8 * off)
+    assert f.bk_spmm_d(n, ptr(t_rp), ptr(t_c), ptr(t_v), xo, ld, k, C.c_void_p(y1.data_ptr() + 8 * off), ld,
+                       stream()) == 0
+    d = {name: dev(p[name]) for name in ("rp2", "code", "val2", "wptr", "wrow")}
+    assert f.bk_spmm_win_d(n, p["tile"], p["ntiles"], p["wmax"], p["nzmax"], ptr(d["rp2"]), ptr(d["code"]),
+                           ptr(d["val2"]), ptr(d["wptr"]), ptr(d["wrow"]), xo, ld, k,
+                           C.c_void_p(y2.data_ptr() + 8 * off), ld, stream()) == 0
     torch.cuda.synchronize()
-    assert torch.equal(y1[:, :k], y2[:, :k])
+    assert torch.equal(y1, y2)  # the columns outside [off, off + k) untouched by both
+    want = full_from_lower(n, rp, col, val)
+    want.data = fval
+    np.testing.assert_allclose(y2[:, off:off + k].cpu().numpy(), want @ x[:, off:off + k].cpu().numpy(),
+                               rtol=0, atol=1e-12)
+
+
+def test_spmm_windowed_refuses_misaligned_views(bk):
+    from paper_2409_05572_b200.workloads import grid_laplacian, full_from_lower
+    from tests.helpers import spmm_window_plan
+    rp, col, val = grid_laplacian((8, 8, 8))
+    full = full_from_lower(512, rp, col, val)
+    frp, fcol, fval = full.indptr.astype(np.int32), full.indices.astype(np.int32), full.data
+    p = spmm_window_plan(bk, 512, frp, fcol, fval, tile=32, wcap=1 << 20)
+    d = {name: dev(p[name]) for name in ("rp2", "code", "val2", "wptr", "wrow")}
+    x = torch.randn(512, 16, dtype=torch.float64, device="cuda")
+    y = torch.zeros_like(x)
+    bk.bk_spmm_win_d.argtypes = [C.c_int] * 5 + [_D] * 5 + [_D, C.c_int, C.c_int, _D, C.c_int, _D]
+    rc = bk.bk_spmm_win_d(512, p["tile"], p["ntiles"], p["wmax"], p["nzmax"], ptr(d["rp2"]), ptr(d["code"]),
+                          ptr(d["val2"]), ptr(d["wptr"]), ptr(d["wrow"]), C.c_void_p(x.data_ptr() + 8), 16, 5,
+                          ptr(y), 16, stream())
+    assert rc != 0  # odd column offset: not 16-byte aligned, the caller keeps the plain kernel
 
 
 @pytest.mark.parametrize("n,a,b", [(1000, 13, 70), (262144, 96, 96), (5000, 288, 288), (77, 1, 1),
