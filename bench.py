@@ -472,6 +472,7 @@ def main():
             stats.append(res.kernel_stats())
         iters.append(res.iterations)
         rels.append(check(res))
+        windowed = res.diagnostics.get("spmm_windowed", 0)
     barrier(dist)
     clocks = sampler.stop()
     t_step = reduce_max(dist, float(np.mean(times)))
@@ -571,6 +572,9 @@ def main():
         "launches_by_kernel": launch_names,
         "roofline": roofline, "kernels": kernels,
         "untimed_ms_per_solve": t_step * 1e3 - total_ms / len(stats),
+        # SpMM launches of the last timed solve that ran as the window-staged K1w
+        # (real matrices with a local graph: config 2; 0 on the complex config 5)
+        "spmm_windowed_launches": int(windowed),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(ORACLE_SO) and not truncated:
         threads = os.cpu_count() or 1

@@ -256,7 +256,11 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(int n, const double*
     double* cs = smem + STAGES * TM * PX;  // STAGES x TK x PC
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int r0 = blockIdx.x * TM, c0 = blockIdx.y * TN;
+    // 1-D grid, the column tiles of a row panel adjacent: the CTAs that share X rows
+    // run together, so X is read from DRAM once (a 2-D grid read it once per column
+    // tile: 1.26x the algorithmic bytes on config 2's two-tile lifts)
+    const int nct = ceil_div(k, TN);
+    const int r0 = (blockIdx.x / nct) * TM, c0 = (blockIdx.x % nct) * TN;
     const int wm = (warp / WN) * (TM / WM), wn = (warp % WN) * (TN / WN);
 
     double acc[FM][FN][2];
@@ -674,7 +678,7 @@ int gemm_launch_v(int n, const double* x, int ldx, int d, const double* c, int l
     BK_RET(a1);
     BK_RET(a2);
     BK_RET(a3);
-    const dim3 grid(ceil_div(n, TM), ceil_div(k, TN));
+    const dim3 grid(ceil_div(n, TM) * ceil_div(k, TN));
     // 16-byte copies of C too when its view allows them (fewer copy instructions)
     if (aligned16(x, ldx) && aligned16(c, ldc))
         k16c<<<grid, WM * WN * 32, smem, s>>>(n, x, ldx, d, c, ldc, k, alpha, beta, y, ldy, run_if);

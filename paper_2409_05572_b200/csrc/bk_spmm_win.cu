@@ -203,9 +203,12 @@ __global__ void __launch_bounds__(256, 3) spmm_d_win_kernel(int n, int T, int nt
                 if (prefetched) cp_async_wait<1>();
                 else cp_async_wait<0>();
             }
-            __syncthreads();
-            mbar_wait(bar, phase);  // the window's rows
+            // one warp polls the window's mbarrier; the others sleep on the block
+            // barrier instead of spinning on try_wait (the polls of the CTAs still
+            // waiting took issue slots from the one multiplying)
+            if (warp == 0) mbar_wait(bar, phase);
             phase ^= 1;
+            __syncthreads();  // index slice and window visible to all
             for (int sl = grp; sl < nr; sl += ngrp) {
                 const int e = srp[sl + 1] - p0;
                 int q = srp[sl] - p0;

@@ -87,7 +87,7 @@ def check_block(product, a, w, res, tol_mult=1.0, north_star=False):
     return crit
 
 
-def check_trajectory(res, ref, tol):
+def check_trajectory(res, ref, tol, iter_slack=0.05):
     """identical (n_now, event, lock) trajectory, or a first split that a decision
     margin within rounding of its threshold explains (tests/test_gpu_flips.py);
     the iteration count may then move by the few iterations the last pairs take
@@ -101,7 +101,7 @@ def check_trajectory(res, ref, tol):
     assert why is not None, (i, hg[i], ho[i], res.margins[i])
     # after a named flip the runs lock / deflate different pairs for a while: the
     # iteration count may move by a few percent (none@96: 223 vs 229)
-    assert abs(res.iterations - ref["iterations"]) <= max(3, 0.05 * ref["iterations"]), \
+    assert abs(res.iterations - ref["iterations"]) <= max(3, iter_slack * ref["iterations"]), \
         (res.iterations, ref["iterations"], why)
     return i, why
 
@@ -166,6 +166,32 @@ def test_large_configs_prefix_match_oracle(product, name, make, iters, rtol):
     if iters >= 40:  # the shrink/expand cycle happened in both runs
         ev = [h["event"] for h in ref["history"]]
         assert 1 in ev and 2 in ev
+
+
+def test_config4_reduced_lattice_matches_oracle(product):
+    """config 4's operator (Anderson W = 16.5, A^2 explicit, the 128 pairs nearest the
+    band centre, 128 + 32 guard vectors, tol 1e-7) on a 24^3 lattice, run to
+    convergence by both libraries: the full-size run's first shrink comes at
+    iteration 316, hours into the oracle's run, so the strategy's whole
+    shrink / expand cycle (51 shrinks, 50 expansions in 875 iterations) is
+    compared here.  Values: eigenvalues of A^2 near 0 (4e-7 ...), so the bound is
+    absolute.  Both runs stop at the residual criterion tol (||A^2|| + |lam|) =
+    1.2e-5, which bounds each value's error (symmetric Bauer-Fike), and after a
+    trajectory split they stop at different iterates: atol 1e-8 (measured 4e-10)."""
+    w = W.config4(side=24)
+    ref = fixture(w.name)
+    assert ref["matrix_sha256"] == W.sha256(w.row_ptr, w.col, w.val)
+    assert ref["x0_sha256"] == W.sha256(w.x0)
+    a, res = run(product, w)
+    assert res.status == ref["status"] == 0
+    np.testing.assert_allclose(res.values, ref["values"], rtol=1e-9, atol=1e-8)
+    ev = [h["event"] for h in res.history]
+    assert ev.count(1) >= 10 and ev.count(2) >= 10  # the cycle ran on the device too
+    # after the (named) first split the two runs' shrink / expand cycles (12
+    # iterations each) are out of phase and the count moves by whole cycles:
+    # 942 against 875 iterations measured, bounded at 10 % here
+    print("config 4 (24^3) split:", check_trajectory(res, ref, w.cfg["tol"], iter_slack=0.10))
+    check_block(product, a, w, res, north_star=True)
 
 
 def test_config5_band_and_residuals(product):

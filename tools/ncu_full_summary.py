@@ -14,7 +14,7 @@ import sys
 
 # main kernels of each class, real and complex (3M) forms
 MAIN = {"gram": ["gram_kernel", "zgram3m_kernel"], "gemm": ["gemm_kernel", "zgemm3m_kernel"],
-        "spmm": ["spmm_d_kernel", "spmm_d_half_kernel", "spmm_z_kernel"]}
+        "spmm": ["spmm_d_kernel", "spmm_d_half_kernel", "spmm_d_win_kernel", "spmm_z_kernel"]}
 AUX = {"gram": ["gram_reduce", "zgram_reduce"]}
 
 
