@@ -87,21 +87,24 @@ __global__ void __launch_bounds__(256, 3) spmm_d_win_kernel(int n, int T, int nt
     // slot's columns (or the index slice after the last slot) and never store
     const char* xlane = reinterpret_cast<const char*>(xs) + hl * 16;
     // N nonzeros of one row: all their X reads issued, then the fmas in CSR order
-    auto step = [&](auto nc, int q, double2 (&acc)[V]) {
+    // N nonzeros of one row over VL 16-byte column groups: all their X reads issued,
+    // then the fmas in CSR order
+    auto step = [&](auto nc, auto vl, int q, auto& acc) {
         constexpr int N = decltype(nc)::value;
-        double2 xv[N][V];
+        constexpr int VL = decltype(vl)::value;
+        double2 xv[N][VL];
         double vv[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             const char* xr = xlane + soff[q + i] * rowbytes;
             vv[i] = sval[q + i];
 #pragma unroll
-            for (int u = 0; u < V; ++u) xv[i][u] = *reinterpret_cast<const double2*>(xr + u * (LPR * 16));
+            for (int u = 0; u < VL; ++u) xv[i][u] = *reinterpret_cast<const double2*>(xr + u * (LPR * 16));
         }
 #pragma unroll
         for (int i = 0; i < N; ++i)
 #pragma unroll
-            for (int u = 0; u < V; ++u) {
+            for (int u = 0; u < VL; ++u) {
                 acc[u].x = fma(vv[i], xv[i][u].x, acc[u].x);
                 acc[u].y = fma(vv[i], xv[i][u].y, acc[u].y);
             }
@@ -209,27 +212,37 @@ __global__ void __launch_bounds__(256, 3) spmm_d_win_kernel(int n, int T, int nt
             if (warp == 0) mbar_wait(bar, phase);
             phase ^= 1;
             __syncthreads();  // index slice and window visible to all
-            for (int sl = grp; sl < nr; sl += ngrp) {
-                const int e = srp[sl + 1] - p0;
-                int q = srp[sl] - p0;
-                double2 acc[V];
+            // the products of the tile's rows over the chunk's VL live column groups
+            // (a narrower last chunk skips the empty ones)
+            auto rows_pass = [&](auto vl) {
+                constexpr int VL = decltype(vl)::value;
+                for (int sl = grp; sl < nr; sl += ngrp) {
+                    const int e = srp[sl + 1] - p0;
+                    int q = srp[sl] - p0;
+                    double2 acc[VL];
 #pragma unroll
-                for (int u = 0; u < V; ++u) acc[u] = make_double2(0.0, 0.0);
-                for (; q + 4 <= e; q += 4) step(std::integral_constant<int, 4>{}, q, acc);
-                const int rem = e - q;
-                if (rem == 3) step(std::integral_constant<int, 3>{}, q, acc);
-                else if (rem == 2) step(std::integral_constant<int, 2>{}, q, acc);
-                else if (rem == 1) step(std::integral_constant<int, 1>{}, q, acc);
-                double* yr = y + static_cast<size_t>(sid[sl]) * ldy + c0;
+                    for (int u = 0; u < VL; ++u) acc[u] = make_double2(0.0, 0.0);
+                    for (; q + 4 <= e; q += 4) step(std::integral_constant<int, 4>{}, vl, q, acc);
+                    const int rem = e - q;
+                    if (rem == 3) step(std::integral_constant<int, 3>{}, vl, q, acc);
+                    else if (rem == 2) step(std::integral_constant<int, 2>{}, vl, q, acc);
+                    else if (rem == 1) step(std::integral_constant<int, 1>{}, vl, q, acc);
+                    double* yr = y + static_cast<size_t>(sid[sl]) * ldy + c0;
 #pragma unroll
-                for (int u = 0; u < V; ++u) {
-                    const int c = 2 * (hl + LPR * u);
-                    if (hl + LPR * u < kw2) {
-                        if (c0 + c + 1 < k) reinterpret_cast<double2*>(yr)[hl + LPR * u] = acc[u];
-                        else if (c0 + c < k) yr[c] = acc[u].x;
+                    for (int u = 0; u < VL; ++u) {
+                        const int c = 2 * (hl + LPR * u);
+                        if (hl + LPR * u < kw2) {
+                            if (c0 + c + 1 < k) reinterpret_cast<double2*>(yr)[hl + LPR * u] = acc[u];
+                            else if (c0 + c < k) yr[c] = acc[u].x;
+                        }
                     }
                 }
-            }
+            };
+            const int vlive = (kw2 + LPR - 1) / LPR;
+            if (vlive >= V) rows_pass(std::integral_constant<int, V>{});
+            else if (V > 3 && vlive == 3) rows_pass(std::integral_constant<int, (V > 3 ? 3 : 1)>{});
+            else if (V > 2 && vlive == 2) rows_pass(std::integral_constant<int, (V > 2 ? 2 : 1)>{});
+            else rows_pass(std::integral_constant<int, 1>{});
             __syncthreads();  // the window is restaged for the next chunk / tile
         }
         cur = nxt;
@@ -283,6 +296,11 @@ extern "C" int bk_spmm_win_d(int n, int tile, int ntiles, int wmax, int nzmax, c
     int nch = ceil_div(kr, kcmax);
     int kc = (ceil_div(kr, nch) + 3) & ~3;  // balanced chunks, whole 32-byte sectors when they fit
     if (kc > kcmax) kc = kcmax;
+    // whole 16-column lane groups instead when that costs no extra chunk: the last,
+    // narrower chunk then skips its empty groups (k = 69: 48 + 22 columns read 5 groups
+    // per nonzero where 36 + 34 read 6)
+    const int kc16 = (kc + 15) & ~15;
+    if (kc16 <= kcmax && kc16 <= 64 && ceil_div(kr, kc16) == nch) kc = kc16;
     nch = ceil_div(kr, kc);
     const size_t smem = 16 + 8 * static_cast<size_t>(wmax) * kc + 2 * idx_bytes + 1024;
     const int grid = max(1, min(ntiles, kSMs * cps));
