@@ -45,7 +45,10 @@ BK_API int bk_spmm_d(int n, const int32_t* row_ptr, const int32_t* col, const do
  * applies the kernel's shared-memory rule (three CTAs per SM with >= 32-column chunks),
  * wcap > 0 a plain cap on the slots per window; ok = 0 when the windows are too large or
  * the graph has too little locality (the plain bk_spmm_d is then the kernel to use).
- * All plan pointers are host memory owned by the plan; the caller uploads them. */
+ * All plan pointers are host memory owned by the plan; the caller uploads them.
+ * bk_spmm_win_d takes even ldx / ldy and x, y either both 16-byte aligned or both at an
+ * odd column of a 16-byte aligned block (the column in front is then read, never written);
+ * it returns cudaErrorMisalignedAddress otherwise. */
 BK_API int bk_spmm_win_plan(int n, const int32_t* row_ptr, const int32_t* col, const double* val, int tile,
                             int wcap, void** plan);
 BK_API int bk_spmm_win_plan_info(const void* plan, int* ok, int* tile, int* ntiles, int* wmax, int* nzmax,

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256, 3) spmm_d_win_kernel(int n, int T, int nt
                                                           const int32_t* __restrict__ wptr,
                                                           const int32_t* __restrict__ wrow,
                                                           const double* __restrict__ x, int ldx, int k, int kc,
-                                                          int nch, double* __restrict__ y, int ldy) {
+                                                          int nch, double* __restrict__ y, int ldy, int skip) {
     // mbarrier | wmax x kc X rows | 2 x (nzmax vals | nzmax slots | T + 1 row pointers | T row ids)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
@@ -232,8 +232,13 @@ __global__ void __launch_bounds__(256, 3) spmm_d_win_kernel(int n, int T, int nt
                     for (int u = 0; u < VL; ++u) {
                         const int c = 2 * (hl + LPR * u);
                         if (hl + LPR * u < kw2) {
-                            if (c0 + c + 1 < k) reinterpret_cast<double2*>(yr)[hl + LPR * u] = acc[u];
-                            else if (c0 + c < k) yr[c] = acc[u].x;
+                            if (c0 + c < skip) {  // the pad column in front of an odd view: never written
+                                if (c0 + c + 1 < k) yr[c + 1] = acc[u].y;
+                            } else if (c0 + c + 1 < k) {
+                                reinterpret_cast<double2*>(yr)[hl + LPR * u] = acc[u];
+                            } else if (c0 + c < k) {
+                                yr[c] = acc[u].x;
+                            }
                         }
                     }
                 }
@@ -265,10 +270,23 @@ extern "C" int bk_spmm_win_d(int n, int tile, int ntiles, int wmax, int nzmax, c
                              const double* x, int ldx, int k, double* y, int ldy, void* stream) {
     if (n <= 0 || k <= 0) return 0;
     if (tile <= 0 || ntiles <= 0 || wmax <= 0 || nzmax < 0) return static_cast<int>(cudaErrorInvalidValue);
-    // 16-byte row chunks: even leading dimensions and aligned bases (the blocks of
-    // the solver have ld % 8 == 0; an odd column offset is the caller's fallback)
-    if ((ldx & 1) || (ldy & 1) || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15))
+    // 16-byte row chunks: even leading dimensions and 16-byte aligned bases (the
+    // blocks of the solver have ld % 8 == 0).  Views of X and Y that both start at an
+    // odd column of their block are taken one column earlier — that column is
+    // multiplied along and never stored; other misalignments are the caller's
+    // fallback to bk_spmm_d.
+    if ((ldx & 1) || (ldy & 1)) return static_cast<int>(cudaErrorMisalignedAddress);
+    const unsigned mx = static_cast<unsigned>(reinterpret_cast<uintptr_t>(x) & 15);
+    const unsigned my = static_cast<unsigned>(reinterpret_cast<uintptr_t>(y) & 15);
+    int skip = 0;
+    if (mx == 8 && my == 8) {
+        skip = 1;
+        --x;
+        --y;
+        ++k;
+    } else if (mx || my) {
         return static_cast<int>(cudaErrorMisalignedAddress);
+    }
     const cudaStream_t s = as_stream(stream);
     const int kr = (k + 1) & ~1;
     // one index slice (16-byte multiple); + 1 KB at the end so lanes past the last
@@ -307,7 +325,7 @@ extern "C" int bk_spmm_win_d(int n, int tile, int ntiles, int wmax, int nzmax, c
     auto launch = [&](auto kern) -> int {
         BK_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<grid, 256, smem, s>>>(n, tile, ntiles, wmax, nzmax, rp2, code, val2, wptr, wrow, x, ldx, k, kc, nch, y,
-                                     ldy);
+                                     ldy, skip);
         BK_LAUNCHED();
     };
     // lanes per row: 8 (four rows per warp) when that wastes fewer lanes on the chunk

@@ -331,10 +331,10 @@ private:
         if (k <= 0) return;
         auto t = prof_begin();
         // K1w once the handle's window plan is ready (bit-identical to K1, so the
-        // switch can happen mid-solve); 16-byte aligned views only
+        // switch can happen mid-solve); X and Y views of the same column parity
         const bool win = cw_ == 1 && csr_->win_state.load(std::memory_order_acquire) == 2 && k >= 8 &&
-                         x.ld % 2 == 0 && y.ld % 2 == 0 && reinterpret_cast<uintptr_t>(x.p) % 16 == 0 &&
-                         reinterpret_cast<uintptr_t>(y.p) % 16 == 0;
+                         x.ld % 2 == 0 && y.ld % 2 == 0 &&
+                         reinterpret_cast<uintptr_t>(x.p) % 16 == reinterpret_cast<uintptr_t>(y.p) % 16;
         if (win) {
             const DeviceCsr::Win& w = csr_->win;
             BKC(bk_spmm_win_d(n_, w.tile, w.ntiles, w.wmax, w.nzmax, w.rp2.as<int32_t>(), w.code.as<int32_t>(),

@@ -87,12 +87,14 @@ def test_spmm_vs_oracle(bk, oracle, k):
 
 
 @pytest.mark.parametrize("k", [1, 7, 26, 40, 69, 96, 138, 161, 300])
-@pytest.mark.parametrize("dims,tile,off", [((12, 11, 10), 64, 0), ((23, 19), 32, 8), ((31, 30, 29), 64, 0)])
+@pytest.mark.parametrize("dims,tile,off", [((12, 11, 10), 64, 0), ((23, 19), 32, 8), ((31, 30, 29), 64, 0),
+                                           ((12, 11, 10), 64, 5), ((31, 30, 29), 64, 3)])
 def test_spmm_windowed_bit_identical(bk, k, dims, tile, off):
     """Window-staged K1w (X rows of a tile's window staged in shared memory by bulk
     copies, column chunk by column chunk) == plain K1, bit for bit: each row keeps
     its nonzeros in CSR order.  Covers ragged last tiles, odd widths, widths over
-    several chunks and X / Y views at a column offset inside wider blocks."""
+    several chunks and X / Y views at an even or odd column offset inside wider blocks
+    (odd: the kernel starts one column earlier and never writes that column)."""
     from paper_2409_05572_b200.workloads import grid_laplacian, full_from_lower
     from tests.helpers import spmm_window_plan
     rp, col, val = grid_laplacian(dims)
@@ -101,7 +103,7 @@ def test_spmm_windowed_bit_identical(bk, k, dims, tile, off):
     frp, fcol = full.indptr.astype(np.int32), full.indices.astype(np.int32)
     fval = np.random.default_rng(7).standard_normal(full.data.size)  # distinct values: order matters
     p = spmm_window_plan(bk, n, frp, fcol, fval, tile=tile, wcap=1 << 20)
-    ld = (k + 7) // 8 * 8 + 8 + off
+    ld = (k + off + 7) // 8 * 8 + 8
     x = torch.randn(n, ld, dtype=torch.float64, device="cuda")
     y1 = torch.full_like(x, 3.0)
     y2 = torch.full_like(x, 3.0)
