@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(256, 3) spmm_d_win_kernel(int n, int T, int nt
 
 
 
+
 }  // namespace
 }  // namespace bk
 
