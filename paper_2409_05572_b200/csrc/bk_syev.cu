@@ -969,7 +969,9 @@ __device__ void tri_apply(int d, const double* __restrict__ mult, const double* 
 __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restrict__ dg,
                                                      const double* __restrict__ off,
                                                      const double* __restrict__ lam, int n_need,
-                                                     double* __restrict__ u, int steps, int from_u) {
+                                                     double* __restrict__ u, int steps, int from_u,
+                                                     const double* __restrict__ src_rm,
+                                                     const int* __restrict__ use_rm, double* __restrict__ out_rm) {
     extern __shared__ double ism[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1002,8 +1004,15 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
     // make the vectors of a degenerate cluster independent; from_u: continue from
     // the vector already in u (the second step, after the clusters of the first
     // step's vectors were orthonormalised as blocks)
+    // (src_rm: the block-orthonormalised vectors, row-major d x n_need, when the
+    // device flag use_rm says the cluster step ran; out_rm: a row-major copy of the
+    // result for the Gram / update kernels — no separate transposition launches)
     if (from_u) {
-        for (int i = lane; i < d; i += 32) b[i] = uj[i];
+        if (src_rm && *use_rm) {
+            for (int i = lane; i < d; i += 32) b[i] = src_rm[static_cast<size_t>(i) * n_need + j];
+        } else {
+            for (int i = lane; i < d; i += 32) b[i] = uj[i];
+        }
     } else
     for (int i = lane; i < d; i += 32) {
         unsigned long long z = (static_cast<unsigned long long>(j) << 32) + static_cast<unsigned long long>(i) +
@@ -1037,6 +1046,8 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
         __syncwarp();
     }
     for (int i = lane; i < d; i += 32) uj[i] = b[i];
+    if (out_rm)
+        for (int i = lane; i < d; i += 32) out_rm[static_cast<size_t>(i) * n_need + j] = b[i];
 }
 
 // One CTA per cluster g (gstart[g] .. gstart[g+1]): Cholesky of the cluster's
@@ -1187,16 +1198,6 @@ __global__ void __launch_bounds__(256) backtr_g_kernel(int d, int n_need, const 
 }
 
 // u (column-major d x k) -> row-major scratch, and back
-__global__ void cm_to_rm_small(int d, int k, const double* __restrict__ cm, double* __restrict__ rm, int ldr,
-                               const int* __restrict__ run_if = nullptr) {
-    if (run_if && *run_if == 0) return;
-    const int64_t total = static_cast<int64_t>(d) * k;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(e / d), i = static_cast<int>(e % d);
-        rm[static_cast<size_t>(i) * ldr + c] = cm[e];
-    }
-}
 __global__ void rm_to_cm_small(int d, int k, const double* __restrict__ rm, int ldr, double* __restrict__ cm,
                                const int* __restrict__ run_if = nullptr) {
     if (run_if && *run_if == 0) return;
@@ -1544,8 +1545,7 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
                                                    static_cast<int>(sizeof(double) * 14 * kSyevMaxD))));
     // clusters -> orthonormal blocks: Gram, per-cluster Cholesky (block-diagonal
     // R^{-1}), update; run_if: only when some cluster has several members
-    auto cluster_step = [&](const int* run_if) -> int {
-        cm_to_rm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u, w.urm, n_need, run_if);
+    auto cluster_step = [&](const int* run_if) -> int {  // w.urm (written by invit_kernel) -> w.u2rm
         int rc = run_if ? bk_gram_if_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work,
                                        run_if, stream)
                         : bk_gram_d(d, w.urm, n_need, n_need, w.urm, n_need, n_need, w.gram, n_need, gram_work, stream);
@@ -1560,13 +1560,14 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
     // inverse iteration, two steps; the clusters of the first step's vectors are
     // orthonormalised before the second (see invit_kernel), skipped on the device
     // when every wanted eigenvalue is isolated
-    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 0);
+    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 0, nullptr,
+                                                            nullptr, w.urm);
     {
         const int rc = cluster_step(has_clusters);
         if (rc) return rc;
-        rm_to_cm_small<<<ceil_div(d * n_need, 256), 256, 0, s>>>(d, n_need, w.u2rm, n_need, w.u, has_clusters);
     }
-    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 1);
+    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 1, w.u2rm,
+                                                            has_clusters, w.urm);
     {
         const int rc = cluster_step(nullptr);
         if (rc) return rc;
