@@ -877,6 +877,7 @@ __global__ void __launch_bounds__(32 * W) bisect_multi_kernel(int d, const doubl
 }
 
 // ------------------------------------------------------------------ 3. inverse iteration
+constexpr int kSmallCluster = 8;  // clusters up to this size are orthonormalised by one fused kernel
 // groups of consecutive eigenvalues closer than gap_rel * ||T||; gstart[g], ngroups
 __global__ void group_kernel(int n_need, const double* __restrict__ lam, const double* __restrict__ dg,
                              const double* __restrict__ off, int d, int* __restrict__ gstart,
@@ -892,6 +893,9 @@ __global__ void group_kernel(int n_need, const double* __restrict__ lam, const d
     gstart[g] = n_need;
     ngroups[0] = g;
     ngroups[1] = g < n_need ? 1 : 0;  // some cluster has several members
+    int big = 0;
+    for (int c = 0; c < g; ++c) big |= gstart[c + 1] - gstart[c] > kSmallCluster;
+    ngroups[2] = big;  // some cluster is too large for cluster_orth_small_kernel
 }
 
 // LU of T - lam I by Gaussian elimination with partial pivoting on the
@@ -1048,6 +1052,97 @@ __global__ void __launch_bounds__(128) invit_kernel(int d, const double* __restr
     for (int i = lane; i < d; i += 32) uj[i] = b[i];
     if (out_rm)
         for (int i = lane; i < d; i += 32) out_rm[static_cast<size_t>(i) * n_need + j] = b[i];
+}
+
+// Small clusters (<= kSmallCluster members: the degenerate pairs, triples and
+// sextuples of lattice operators) in one launch: CTA b loads its cluster's columns of
+// U (column-major, contiguous) into shared memory, forms their Gram matrix with
+// fixed-order warp reductions, takes its Cholesky factor R in one thread and writes
+// U R^{-1} back in place (and, when asked, a row-major copy of every column it owns,
+// singletons included).  A pivot that lost more than 1e-12 of its diagonal, or a
+// larger cluster, raises *big, which runs the general path (Gram, per-cluster
+// skip-pivot Cholesky, update) after this kernel.
+__global__ void __launch_bounds__(128) cluster_orth_small_kernel(int d, int n_need, const int* __restrict__ gstart,
+                                                                  const int* __restrict__ ngroups,
+                                                                  double* __restrict__ u, double* __restrict__ out_rm,
+                                                                  int* __restrict__ big, const int* __restrict__ run_if) {
+    extern __shared__ double cols[];  // d x g, column c at cols + c * d
+    __shared__ double G[kSmallCluster][kSmallCluster], Ri[kSmallCluster][kSmallCluster];
+    __shared__ int ok;
+    if (run_if && *run_if == 0) return;
+    const int b = blockIdx.x;
+    if (b >= ngroups[0]) return;
+    const int g0 = gstart[b], g = gstart[b + 1] - g0;
+    if (g > kSmallCluster) return;  // ngroups[2] is already set by group_kernel
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* uc = u + static_cast<size_t>(g0) * d;
+    if (g == 1) {
+        if (out_rm)
+            for (int i = tid; i < d; i += blockDim.x) out_rm[static_cast<size_t>(i) * n_need + g0] = uc[i];
+        return;
+    }
+    for (int e = tid; e < d * g; e += blockDim.x) cols[e] = uc[e];
+    __syncthreads();
+    for (int p = warp; p < g * g; p += 4) {  // upper triangle, one warp per entry, fixed order
+        const int a = p / g, c = p - a * g;
+        if (a > c) continue;
+        double sum = 0.0;
+        for (int i = lane; i < d; i += 32) sum = fma(cols[a * d + i], cols[c * d + i], sum);
+        sum = warp_sum(sum);
+        if (lane == 0) G[a][c] = sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int good = 1;
+        // R upper triangular, G = R^T R; Ri = R^{-1}
+        double R[kSmallCluster][kSmallCluster];
+        for (int j = 0; j < g && good; ++j) {
+            double p = G[j][j];
+            for (int l = 0; l < j; ++l) p -= R[l][j] * R[l][j];
+            if (!(p > 1e-12 * G[j][j])) {
+                good = 0;
+                break;
+            }
+            const double r = sqrt(p);
+            R[j][j] = r;
+            for (int c = j + 1; c < g; ++c) {
+                double v = G[j][c];
+                for (int l = 0; l < j; ++l) v -= R[l][j] * R[l][c];
+                R[j][c] = v / r;
+            }
+        }
+        if (good)
+            for (int c = 0; c < g; ++c) {  // column c of R^{-1} by back substitution
+                for (int a = g - 1; a >= 0; --a) {
+                    if (a > c) {
+                        Ri[a][c] = 0.0;
+                        continue;
+                    }
+                    double v = a == c ? 1.0 : 0.0;
+                    for (int l = a + 1; l <= c; ++l) v -= R[a][l] * Ri[l][c];
+                    Ri[a][c] = v / R[a][a];
+                }
+            }
+        ok = good;
+        if (!good) *big = 1;
+    }
+    __syncthreads();
+    if (!ok) return;
+    for (int i = tid; i < d; i += blockDim.x) {
+        double xr[kSmallCluster];
+#pragma unroll
+        for (int a = 0; a < kSmallCluster; ++a) xr[a] = a < g ? cols[a * d + i] : 0.0;
+#pragma unroll
+        for (int c = 0; c < kSmallCluster; ++c) {
+            if (c >= g) break;
+            double v = 0.0;
+#pragma unroll
+            for (int a = 0; a < kSmallCluster; ++a)
+                if (a <= c) v = fma(xr[a], Ri[a][c], v);
+            uc[static_cast<size_t>(c) * d + i] = v;
+            if (out_rm) out_rm[static_cast<size_t>(i) * n_need + g0 + c] = v;
+        }
+    }
 }
 
 // One CTA per cluster g (gstart[g] .. gstart[g+1]): Cholesky of the cluster's
@@ -1560,16 +1655,24 @@ int tri_vectors(int d, int n_need, double* values, SyevWs& w, void* gram_work, v
     // inverse iteration, two steps; the clusters of the first step's vectors are
     // orthonormalised before the second (see invit_kernel), skipped on the device
     // when every wanted eigenvalue is isolated
+    int* big = w.ngroups + 2;  // device flag: the general cluster path is needed (set by group_kernel / the small kernel)
+    const size_t csm = sizeof(double) * static_cast<size_t>(d) * kSmallCluster;
+    BK_RET(BK_ONCE_PER_DEVICE(cudaFuncSetAttribute(cluster_orth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(sizeof(double) * kSyevMaxD * kSmallCluster))));
     invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 0, nullptr,
                                                             nullptr, w.urm);
+    // clusters between the steps: small ones in place in w.u by one fused kernel; the
+    // general path (w.urm -> w.u2rm) only when a cluster is large or a pivot was poor
+    cluster_orth_small_kernel<<<n_need, 128, csm, s>>>(d, n_need, w.gstart, w.ngroups, w.u, nullptr, big, has_clusters);
     {
-        const int rc = cluster_step(has_clusters);
+        const int rc = cluster_step(big);
         if (rc) return rc;
     }
-    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 1, w.u2rm,
-                                                            has_clusters, w.urm);
+    invit_kernel<<<ceil_div(n_need * 32, 64), 64, ism, s>>>(d, w.dg, w.off, values, n_need, w.u, 1, 1, w.u2rm, big,
+                                                            w.urm);
+    cluster_orth_small_kernel<<<n_need, 128, csm, s>>>(d, n_need, w.gstart, w.ngroups, w.u, w.u2rm, big, nullptr);
     {
-        const int rc = cluster_step(nullptr);
+        const int rc = cluster_step(big);
         if (rc) return rc;
     }
     // three Newton-Schulz steps U <- U (3I - U^T U)/2: after the cluster step the

@@ -131,7 +131,14 @@ def test_config2_matches_oracle_trajectory(product, strategy, n_ex):
     assert res.status == ref["status"] == 0
     np.testing.assert_allclose(res.values, ref["values"], rtol=1e-9)
     np.testing.assert_allclose(res.values, W.lap3d_eigs(64, 64), rtol=1e-9 if n_ex > 64 else 1e-8)
-    print(f"config 2 {strategy}@{n_ex} split:", check_trajectory(res, ref, w.cfg["tol"]))
+    # none@64: nev = 64 cuts the degenerate triple lambda_64 = lambda_65 = lambda_66 and the
+    # block has no guard vectors, so the last pair converges to whichever vector of
+    # the triple's eigenspace the block leans to, at a rate set by rounding-level
+    # components of the two excluded ones — the count is not determined to better
+    # than ~10 % (oracle 1857; this library 1935 and 1680 under two builds that
+    # differ only in the eigensolver's rounding); the first split is still named
+    slack = 0.15 if n_ex == 64 else 0.05
+    print(f"config 2 {strategy}@{n_ex} split:", check_trajectory(res, ref, w.cfg["tol"], iter_slack=slack))
     check_block(product, a, w, res, north_star=True)
 
 
