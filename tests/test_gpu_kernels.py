@@ -125,6 +125,46 @@ def test_spmm_windowed_bit_identical(bk, k, dims, tile, off):
                                rtol=0, atol=1e-12)
 
 
+@pytest.mark.parametrize("k", [8, 33, 70])
+def test_spmm_windowed_large_windows_and_empty_rows(bk, k):
+    """Windows far beyond 8 rows per lane group (a random graph: every tile's halo is
+    hundreds of rows, staged by the on-demand row-id loop), rows without nonzeros and
+    rows longer than one step group — still bit-identical to K1."""
+    from scipy.sparse import random as sprandom, csr_matrix
+    from tests.helpers import spmm_window_plan
+    n = 1500
+    rng = np.random.default_rng(3)
+    a = sprandom(n, n, density=0.006, random_state=5, format="csr", data_rvs=rng.standard_normal)
+    a = (a + a.T).tolil()
+    a[7, :] = 0.0   # empty rows
+    a[:, 7] = 0.0
+    a[640, :] = 0.0
+    a[:, 640] = 0.0
+    a[11, 100:160] = rng.standard_normal(60)  # a long row (and its mirror column)
+    a[100:160, 11] = a[11, 100:160].T
+    a = csr_matrix(a)
+    a.eliminate_zeros()
+    a.sort_indices()
+    frp, fcol, fval = a.indptr.astype(np.int32), a.indices.astype(np.int32), np.ascontiguousarray(a.data)
+    p = spmm_window_plan(bk, n, frp, fcol, fval, tile=64, wcap=1 << 20)
+    assert p["wmax"] > 300  # beyond 8 rows per lane group
+    ld = (k + 7) // 8 * 8
+    x = torch.randn(n, ld, dtype=torch.float64, device="cuda")
+    y1 = torch.full_like(x, -2.0)
+    y2 = torch.full_like(x, -2.0)
+    bk.bk_spmm_win_d.argtypes = [C.c_int] * 5 + [_D] * 5 + [_D, C.c_int, C.c_int, _D, C.c_int, _D]
+    t_rp, t_c, t_v = dev(frp), dev(fcol), dev(fval)
+    assert bk.bk_spmm_d(n, ptr(t_rp), ptr(t_c), ptr(t_v), ptr(x), ld, k, ptr(y1), ld, stream()) == 0
+    d = {name: dev(p[name]) for name in ("rp2", "code", "val2", "wptr", "wrow")}
+    assert bk.bk_spmm_win_d(n, p["tile"], p["ntiles"], p["wmax"], p["nzmax"], ptr(d["rp2"]), ptr(d["code"]),
+                            ptr(d["val2"]), ptr(d["wptr"]), ptr(d["wrow"]), ptr(x), ld, k, ptr(y2), ld,
+                            stream()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert float(y2[7, :k].abs().max()) == 0.0 and float(y2[640, :k].abs().max()) == 0.0
+    np.testing.assert_allclose(y2[:, :k].cpu().numpy(), a @ x[:, :k].cpu().numpy(), rtol=0, atol=1e-12)
+
+
 def test_spmm_windowed_refuses_misaligned_views(bk):
     from paper_2409_05572_b200.workloads import grid_laplacian, full_from_lower
     from tests.helpers import spmm_window_plan
