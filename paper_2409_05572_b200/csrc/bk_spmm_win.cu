@@ -2,16 +2,18 @@
 //
 // The plain K1 (bk_spmm.cu) gathers one X row per nonzero through L1/L2: on a
 // 7-point stencil that is ~5 L2 row loads per matrix row after L1 hits, and the
-// kernel sits at the L2 -> SM bandwidth, not at HBM (config 2: 0.37 of HBM).
+// kernel waits on those register-landing gathers (config 2: 0.37 of HBM).
 // Here a host plan (host/tiling.cpp) regroups the rows into tiles of graph-local
 // rows and lists each tile's window: its own rows plus the halo columns its
-// rows reference.  A CTA stages a window's X rows — one column chunk of kc
-// columns at a time, so the window fits beside the other resident CTAs — and the
-// tile's index slice (row pointers, row ids, (slot, val) per nonzero) in shared
-// memory with 16-byte cp.async, then every nonzero reads its X row from shared
-// memory: an X row crosses L2 -> SM once per tile that touches it (128-row
-// tiles of the 7-point stencil: 2.3 loads per matrix row).  Several CTAs per SM:
-// one CTA's staging overlaps the others' products.
+// rows reference.  A CTA stages a window's X rows in shared memory — one column
+// chunk of kc columns at a time, so the window fits beside the other resident
+// CTAs — with one bulk copy per row (cp.async.bulk completing on an mbarrier),
+// and the tile's index slice (row pointers, row ids, (slot, val) per nonzero)
+// with cp.async one tile ahead; tile descriptors and the window's row ids are
+// prefetched into registers.  Every nonzero then reads its X row from shared
+// memory: an X row crosses L2 -> SM once per tile that touches it (64-row
+// tiles of the 7-point stencil: 2.4 loads per matrix row).  Three CTAs per SM:
+// one CTA's copies run while the others multiply.
 //
 // Products: LPR lanes per matrix row (32/LPR rows per warp), each lane V x
 // double2 columns, four nonzeros' shared-memory reads in flight; a row's
@@ -19,7 +21,8 @@
 // does, so Y is bit-identical (proj/src/kernel.cpp:8-33 is the reference loop).
 // Algorithmic bytes as K1: 12 nnz + 4 (n + 1) + 16 n k; the on-chip gathers cost
 // nnz * k * 8 bytes of shared-memory bandwidth (128 B/clk/SM), which bounds
-// matrices with many nonzeros per row (config 4: 25 per row).
+// matrices with many nonzeros per row (config 4: 25 per row).  Measurements and
+// the variants tried: profiles/r02_spmm_win.md.
 #include <cstdlib>
 #include <type_traits>
 
